@@ -1,0 +1,222 @@
+/*
+ * tt.h -- C ABI of the B200-native tensor-permutation library (libtt.so),
+ * the hot path of arXiv 1705.01598 (cuTT).
+ *
+ * Citations: "P:Lnn" = /root/reference/PAPER.md line nn (paper text, used as
+ * the specification; the library shares no code with it).
+ *
+ * THE OPERATION (Section 2, Eq. (1) with the output stride read as
+ * c(i,O); P:L62-66 for the direction of the permutation; R1-R6):
+ *
+ *   A rank-n tensor with extents dims[0..n-1]; dims[0] is the stride-1
+ *   (fastest) dimension ("the first tensor dimension is the stride-1
+ *   dimension").  Dimensions are 0-based here (the paper is 1-based).
+ *   perm[j] is the INPUT dimension that becomes OUTPUT dimension j (the
+ *   paper's O = {w_j}), so the output extents are dims[perm[j]].
+ *   With S_in[i] = prod_{k<i} dims[k] and S_out[j] = prod_{k<j} dims[perm[k]]:
+ *
+ *       out[ sum_j x[perm[j]] * S_out[j] ] = in[ sum_i x[i] * S_in[i] ]
+ *
+ *   for every coordinate 0 <= x[i] < dims[i].  Elements are opaque 4- or
+ *   8-byte words copied bit-exactly (NaN payloads, -0.0, subnormals kept).
+ *   Out-of-place only.
+ *
+ * API SHAPE (Section 2.3): "a plan is first created, then executed,
+ * and finally destroyed, similarly to ... FFTW ... and cuFFT"; plan creation
+ * "takes as input the rank and dimension extents of the input tensor, as well
+ * as the permutation of the output tensor".  Unlike cuTT, a plan here owns no
+ * device memory (single-GPU plans): all kernel parameters travel in the
+ * launch's parameter block.
+ *
+ * ERRORS: every function returns tt_status_t; nothing throws across the ABI.
+ * Argument errors are reported synchronously.  tt_execute is stream-ordered
+ * and asynchronous: a fault inside the kernel surfaces on a later call or
+ * synchronisation of the stream (as TT_CUDA_ERROR from a later tt_* call).
+ *
+ * THREAD SAFETY: plans are immutable after creation; concurrent tt_execute
+ * calls on one single-GPU plan are safe.  A sharded plan owns staging
+ * buffers and must not be executed concurrently with itself.
+ */
+#ifndef TT_H_
+#define TT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define TT_VERSION 1
+#define TT_MAX_RANK 32          /* the warp-parallel decode handles h <= 32 terms */
+#define TT_NCCL_UNIQUE_ID_BYTES 128
+
+typedef struct tt_plan_s* tt_plan_t;
+typedef struct tt_comm_s* tt_comm_t;
+/* A cudaStream_t (CUstream) handle; NULL means the legacy default stream. */
+typedef void* tt_stream_t;
+
+typedef enum {
+    TT_SUCCESS = 0,
+    TT_INVALID_PLAN = 1,        /* NULL or destroyed plan handle                    */
+    TT_INVALID_PARAMETER = 2,   /* bad rank/extent/perm/pointer/in==out/alignment   */
+    TT_INVALID_DEVICE = 3,      /* current device differs from the plan's device    */
+    TT_UNSUPPORTED = 4,         /* elem_size not 4/8, shard extent not divisible    */
+    TT_CUDA_ERROR = 5,          /* a CUDA runtime call or launch failed             */
+    TT_NCCL_ERROR = 6,          /* an NCCL call failed                              */
+    TT_INTERNAL_ERROR = 7,      /* allocation failure or broken invariant           */
+    TT_BUFFER_TOO_SMALL = 8     /* tt_plan_describe: JSON truncated                 */
+} tt_status_t;
+
+/* Kernel families.  TT_KERNEL_AUTO lets the planner choose. */
+typedef enum {
+    TT_KERNEL_AUTO = 0,
+    TT_KERNEL_COPY = 1,     /* rank 1 after fusion (identity): memcpy-equivalent       */
+    TT_KERNEL_TILE = 2,     /* generic staged tile: Tiled / Packed / PackedSplit class  */
+    TT_KERNEL_ROWCOPY = 3,  /* fastest dim unchanged, long rows: TiledCopy class        */
+    TT_KERNEL_TILED2D = 4   /* two large disjoint fastest dims, 128-bit both sides      */
+} tt_kernel_t;
+
+/*
+ * Optional planner overrides (tests, calibration sweeps).  Zero-initialise and
+ * set only what you need; 0 always means "planner's choice".
+ */
+typedef struct {
+    int kernel;          /* tt_kernel_t; a family that cannot run the problem -> TT_UNSUPPORTED */
+    int run_in;          /* target contiguous input run, elements (TILE)          */
+    int run_out;         /* target contiguous output run, elements (TILE)         */
+    int threads;         /* threads per CTA (multiple of 32, <= 1024)              */
+    int ctas_per_sm;     /* persistent CTAs per SM (grid = num_sms * this)         */
+    int no_fusion;       /* 1 = skip dimension fusion / extent-1 removal (debug)   */
+} tt_plan_options_t;
+
+/* Device description for tt_plan_offline (planning without a GPU). */
+typedef struct {
+    int num_sms;                 /* 148 on B200                        */
+    int max_smem_per_block;      /* opt-in maximum, bytes (232448)     */
+    int max_smem_per_sm;         /* bytes (233472)                     */
+    int max_threads_per_sm;      /* 2048                               */
+    int regs_per_sm;             /* 65536                              */
+} tt_device_props_t;
+
+/*
+ * tt_plan -- create a plan for permuting a tensor of `rank` dims on the
+ * CURRENT CUDA device, to be enqueued on `stream`.
+ *   plan       out: receives the handle (set to NULL on failure).
+ *   rank       1..TT_MAX_RANK.
+ *   dims       host array [rank], every extent >= 1, product*elem_size < 2^62.
+ *   perm       host array [rank], a bijection on 0..rank-1 (gather form above).
+ *   elem_size  4 or 8 (else TT_UNSUPPORTED).
+ *   stream     stream used by tt_execute.
+ * The arrays are copied; the caller keeps ownership.  Host-only work plus
+ * device-attribute queries: no device allocation, no host<->device copy.
+ */
+tt_status_t tt_plan(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                    size_t elem_size, tt_stream_t stream);
+
+/* tt_plan with planner overrides (opts may be NULL = tt_plan). */
+tt_status_t tt_plan_ex(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                       size_t elem_size, tt_stream_t stream, const tt_plan_options_t* opts);
+
+/*
+ * tt_plan_offline -- plan for a DESCRIBED device without touching the CUDA
+ * runtime (works on a machine with no GPU).  The plan can be described but
+ * tt_execute on it returns TT_INVALID_DEVICE.  props may be NULL (B200 values).
+ */
+tt_status_t tt_plan_offline(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, const tt_device_props_t* props,
+                            const tt_plan_options_t* opts);
+
+/*
+ * tt_execute -- enqueue out = permute(in) on the plan's stream.
+ *   in, out  DEVICE pointers (or managed/mapped memory) of vol*elem_size
+ *            bytes each, aligned to elem_size, on the plan's device.
+ *            in == out -> TT_INVALID_PARAMETER (no in-place mode); other
+ *            overlaps are undefined.
+ * Asynchronous; does not synchronise.  Launches exactly one kernel.
+ */
+tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out);
+
+/*
+ * tt_execute_host -- end-to-end form: copy host_in (vol*elem_size bytes,
+ * preferably pinned) to the device buffer dev_in, permute into dev_out, copy
+ * dev_out back to host_out, all enqueued on the plan's stream.  Does not
+ * synchronise; the caller synchronises the stream before reading host_out.
+ */
+tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out,
+                            void* dev_in, void* dev_out);
+
+/* tt_destroy -- free the plan (and a sharded plan's staging buffers).
+ * tt_destroy(NULL) returns TT_INVALID_PLAN. */
+tt_status_t tt_destroy(tt_plan_t plan);
+
+/*
+ * tt_plan_describe -- NUL-terminated JSON description of the plan written to
+ * buf[len]: fused problem, kernel family, tile geometry (dims, extents,
+ * strides, smem layout), grid dims, launch shape, model prediction.
+ * TT_BUFFER_TOO_SMALL if it does not fit (buf then holds a truncated prefix).
+ */
+tt_status_t tt_plan_describe(tt_plan_t plan, char* buf, size_t len);
+
+/* Number of kernel launches one tt_execute / tt_execute_sharded performs. */
+int tt_plan_launches(tt_plan_t plan);
+
+/* Static string for a status code. */
+const char* tt_status_string(tt_status_t s);
+
+/* TT_VERSION of the loaded library. */
+int tt_version(void);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU (one box, one process per GPU).  The paper has no multi-GPU
+ * transpose ("we will only consider local tensor transposes"); this is
+ * the BASELINE.json north_star extension.
+ *
+ * Sharded layout: the global tensor (global_dims) is block-sharded along its
+ * OUTERMOST input dimension n-1; rank r holds slab r of extent
+ * global_dims[n-1]/nranks.  The output is block-sharded along its outermost
+ * OUTPUT dimension n-1 (input dimension perm[n-1]) the same way.
+ *   perm[n-1] == n-1 : local case, each rank permutes its slab (no traffic).
+ *   otherwise        : pack (local permute) -> ncclAlltoAll over NVLink ->
+ *                      unpack (local permute).
+ * ---------------------------------------------------------------------- */
+
+/* Fill id[TT_NCCL_UNIQUE_ID_BYTES] with a fresh ncclUniqueId (call on one
+ * rank, broadcast the bytes, e.g. with torch.distributed). */
+tt_status_t tt_comm_unique_id(void* id);
+
+/* Create an NCCL communicator on the current device. */
+tt_status_t tt_comm_init(tt_comm_t* comm, const void* nccl_unique_id, int nranks, int rank);
+
+tt_status_t tt_comm_destroy(tt_comm_t comm);
+
+/*
+ * tt_plan_sharded -- plan the sharded permutation of global_dims by perm.
+ * The shard extent global_dims[n-1] and, for the redistribution case,
+ * global_dims[perm[n-1]] must be divisible by nranks (else TT_UNSUPPORTED).
+ * Allocates 2 x shard bytes of device staging for the redistribution case.
+ */
+tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int rank, const int64_t* global_dims,
+                            const int* perm, size_t elem_size, tt_stream_t stream);
+
+/* Local input slab -> local output slab (device pointers, shard bytes each).
+ * Collective: every rank of the communicator must call it. */
+tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_local);
+
+/* Shard geometry of a sharded plan: local input dims and local output dims
+ * (output order), rank entries each. */
+tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* local_out_dims);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TT_H_ */

@@ -1,0 +1,94 @@
+"""Sharded (multi-GPU, one box) permutation: binding of tt_comm_* / tt_*_sharded.
+
+One process per GPU.  The NCCL unique id is created by rank 0 through the
+library and broadcast with ``torch.distributed`` (plumbing only); the
+exchange itself is the library's ncclAlltoAll on the plan's stream.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import lib, _check, _arrays, _stream_handle, _describe, _ptr, NCCL_UNIQUE_ID_BYTES
+
+
+def unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check(lib.tt_comm_unique_id(buf), "tt_comm_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """NCCL communicator on the current CUDA device."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != NCCL_UNIQUE_ID_BYTES:
+            raise ValueError("unique id must be 128 bytes")
+        self.nranks, self.rank = int(nranks), int(rank)
+        h = ctypes.c_void_p()
+        _check(lib.tt_comm_init(ctypes.byref(h), ctypes.create_string_buffer(uid, len(uid)),
+                                self.nranks, self.rank), "tt_comm_init")
+        self._h = h
+
+    @classmethod
+    def from_process_group(cls, group=None):
+        """Rank 0 makes the id, torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world, rank)
+
+    def destroy(self):
+        if self._h is not None:
+            _check(lib.tt_comm_destroy(self._h), "tt_comm_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class ShardedPlan:
+    """Permutation of a tensor block-sharded along its outermost input dim
+    (slab ``rank`` of ``global_dims[-1] / nranks``) into the output
+    block-sharded along its outermost output dim."""
+
+    def __init__(self, comm: Comm, global_dims, perm, elem_size: int, stream=None):
+        n, d, p = _arrays(global_dims, perm)
+        self.comm = comm
+        self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
+        h = ctypes.c_void_p()
+        _check(lib.tt_plan_sharded(ctypes.byref(h), comm._h, comm.rank, d, p, self.elem_size,
+                                   _stream_handle(stream)), "tt_plan_sharded")
+        self._h = h
+        a = (ctypes.c_int64 * n)()
+        b = (ctypes.c_int64 * n)()
+        _check(lib.tt_plan_shard_dims(h, a, b), "tt_plan_shard_dims")
+        self.local_in_dims = tuple(a)
+        self.local_out_dims = tuple(b)
+
+    def execute(self, in_local, out_local) -> None:
+        _check(lib.tt_execute_sharded(self._h, _ptr(in_local), _ptr(out_local)),
+               "tt_execute_sharded")
+
+    __call__ = execute
+
+    def describe(self) -> dict:
+        return _describe(self._h)
+
+    @property
+    def launches(self) -> int:
+        return lib.tt_plan_launches(self._h)
+
+    def destroy(self):
+        if self._h is not None:
+            _check(lib.tt_destroy(self._h), "tt_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass

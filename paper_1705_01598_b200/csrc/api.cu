@@ -1,0 +1,195 @@
+// api.cu -- the C ABI declared in include/tt.h (plan -> execute -> destroy,
+// P:L167).  Argument marshalling, device queries and launches only; the
+// planner lives in planner.cpp and the kernels in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "tt_internal.h"
+
+using namespace tt;
+
+namespace {
+
+Plan* as_plan(tt_plan_t h) {
+    Plan* p = reinterpret_cast<Plan*>(h);
+    if (p == nullptr || p->magic != 0x54545054u) return nullptr;
+    return p;
+}
+
+tt_status_t query_device(DeviceInfo& dev) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    dev.device = d;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_INVALID_DEVICE;
+    }
+    dev.num_sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d) == cudaSuccess)
+        dev.max_smem_per_block = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, d) == cudaSuccess)
+        dev.max_smem_per_sm = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxThreadsPerMultiProcessor, d) == cudaSuccess)
+        dev.max_threads_per_sm = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxRegistersPerMultiprocessor, d) == cudaSuccess)
+        dev.regs_per_sm = v;
+    cudaGetLastError();
+    return TT_SUCCESS;
+}
+
+tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, const int* perm,
+                      size_t elem_size, tt_stream_t stream, const DeviceInfo& dev,
+                      const tt_plan_options_t* opts, OccupancyFn occ) {
+    if (out == nullptr) return TT_INVALID_PARAMETER;
+    *out = nullptr;
+    tt_status_t st = validate(rank, dims, perm, elem_size);
+    if (st != TT_SUCCESS) return st;
+    Plan* p = new (std::nothrow) Plan();
+    if (p == nullptr) return TT_INTERNAL_ERROR;
+    p->device = dev.device;
+    p->stream = stream;
+    p->rank = rank;
+    p->dims.assign(dims, dims + rank);
+    p->perm.assign(perm, perm + rank);
+    const bool fuse = !(opts && opts->no_fusion);
+    p->prob = normalize(rank, dims, perm, (int)elem_size, fuse);
+    st = choose_plan(*p, dev, opts, occ);
+    if (st != TT_SUCCESS) {
+        delete p;
+        return st;
+    }
+    *out = reinterpret_cast<tt_plan_t>(p);
+    return TT_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tt_version(void) { return TT_VERSION; }
+
+const char* tt_status_string(tt_status_t s) {
+    switch (s) {
+        case TT_SUCCESS: return "TT_SUCCESS";
+        case TT_INVALID_PLAN: return "TT_INVALID_PLAN";
+        case TT_INVALID_PARAMETER: return "TT_INVALID_PARAMETER";
+        case TT_INVALID_DEVICE: return "TT_INVALID_DEVICE";
+        case TT_UNSUPPORTED: return "TT_UNSUPPORTED";
+        case TT_CUDA_ERROR: return "TT_CUDA_ERROR";
+        case TT_NCCL_ERROR: return "TT_NCCL_ERROR";
+        case TT_INTERNAL_ERROR: return "TT_INTERNAL_ERROR";
+        case TT_BUFFER_TOO_SMALL: return "TT_BUFFER_TOO_SMALL";
+        default: return "TT_UNKNOWN_STATUS";
+    }
+}
+
+tt_status_t tt_plan_ex(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                       size_t elem_size, tt_stream_t stream, const tt_plan_options_t* opts) {
+    if (plan == nullptr) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    tt_status_t st = validate(rank, dims, perm, elem_size);
+    if (st != TT_SUCCESS) return st;
+    DeviceInfo dev;
+    st = query_device(dev);
+    if (st != TT_SUCCESS) return st;
+    return make_plan(plan, rank, dims, perm, elem_size, stream, dev, opts, &cuda_occupancy);
+}
+
+tt_status_t tt_plan(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                    size_t elem_size, tt_stream_t stream) {
+    return tt_plan_ex(plan, rank, dims, perm, elem_size, stream, nullptr);
+}
+
+tt_status_t tt_plan_offline(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, const tt_device_props_t* props,
+                            const tt_plan_options_t* opts) {
+    DeviceInfo dev;
+    dev.device = -1;
+    if (props) {
+        if (props->num_sms > 0) dev.num_sms = props->num_sms;
+        if (props->max_smem_per_block > 0) dev.max_smem_per_block = props->max_smem_per_block;
+        if (props->max_smem_per_sm > 0) dev.max_smem_per_sm = props->max_smem_per_sm;
+        if (props->max_threads_per_sm > 0) dev.max_threads_per_sm = props->max_threads_per_sm;
+        if (props->regs_per_sm > 0) dev.regs_per_sm = props->regs_per_sm;
+    }
+    return make_plan(plan, rank, dims, perm, elem_size, nullptr, dev, opts, nullptr);
+}
+
+static tt_status_t check_exec(Plan* p, const void* in, void* out) {
+    if (p == nullptr) return TT_INVALID_PLAN;
+    if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
+    const uintptr_t mis = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
+                          (uintptr_t)(p->prob.esize - 1);
+    if (mis) return TT_INVALID_PARAMETER;
+    if (p->device < 0) return TT_INVALID_DEVICE;
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    if (d != p->device) return TT_INVALID_DEVICE;
+    return TT_SUCCESS;
+}
+
+tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out) {
+    Plan* p = as_plan(plan);
+    tt_status_t st = check_exec(p, in, out);
+    if (st != TT_SUCCESS) return st;
+    if (p->shard) return TT_INVALID_PLAN;  // sharded plans use tt_execute_sharded
+    int e = launch_plan(*p, in, out, p->stream);
+    return e == 0 ? TT_SUCCESS : TT_CUDA_ERROR;
+}
+
+tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out, void* dev_in,
+                            void* dev_out) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr) return TT_INVALID_PLAN;
+    if (host_in == nullptr || host_out == nullptr) return TT_INVALID_PARAMETER;
+    tt_status_t st = check_exec(p, dev_in, dev_out);
+    if (st != TT_SUCCESS) return st;
+    if (p->shard) return TT_INVALID_PLAN;
+    const size_t bytes = (size_t)p->prob.vol * (size_t)p->prob.esize;
+    cudaStream_t s = static_cast<cudaStream_t>(p->stream);
+    if (cudaMemcpyAsync(dev_in, host_in, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    if (launch_plan(*p, dev_in, dev_out, p->stream) != 0) return TT_CUDA_ERROR;
+    if (cudaMemcpyAsync(host_out, dev_out, bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    return TT_SUCCESS;
+}
+
+tt_status_t tt_plan_describe(tt_plan_t plan, char* buf, size_t len) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr) return TT_INVALID_PLAN;
+    if (buf == nullptr || len == 0) return TT_INVALID_PARAMETER;
+    std::string s = describe_json(*p);
+    if (s.size() + 1 > len) {
+        std::memcpy(buf, s.data(), len - 1);
+        buf[len - 1] = '\0';
+        return TT_BUFFER_TOO_SMALL;
+    }
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return TT_SUCCESS;
+}
+
+int tt_plan_launches(tt_plan_t plan) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr) return -1;
+    return 1;
+}
+
+tt_status_t tt_destroy(tt_plan_t plan) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr) return TT_INVALID_PLAN;
+    p->magic = 0;
+    delete p;
+    return TT_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,592 @@
+// planner.cpp -- host planner: validate (row a-1), normalise/fuse (a-2),
+// classify (a-3), choose parameters with the B200 model (a-4), materialise
+// the kernel parameter block (a-5), describe.  No CUDA runtime calls here, so
+// the planner runs on a machine without a GPU (tt_plan_offline).
+//
+// Citations: P:Lnn = PAPER.md line nn (arXiv 1705.01598).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "tt_internal.h"
+
+namespace tt {
+
+// --------------------------------------------------------------------------
+// a-1 validate (P:L167 plan inputs; P:L82 h <= 32; R7-R11)
+// --------------------------------------------------------------------------
+tt_status_t validate(int rank, const int64_t* dims, const int* perm, size_t elem_size) {
+    if (rank < 1 || rank > kMaxDims || dims == nullptr || perm == nullptr)
+        return TT_INVALID_PARAMETER;
+    bool seen[kMaxDims] = {};
+    long double vol = 1;
+    for (int i = 0; i < rank; ++i) {
+        if (dims[i] < 1) return TT_INVALID_PARAMETER;
+        if (perm[i] < 0 || perm[i] >= rank || seen[perm[i]]) return TT_INVALID_PARAMETER;
+        seen[perm[i]] = true;
+        vol *= (long double)dims[i];
+    }
+    if (elem_size != 4 && elem_size != 8) return TT_UNSUPPORTED;
+    if (vol * (long double)elem_size >= (long double)(1LL << 62)) return TT_INVALID_PARAMETER;
+    return TT_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// a-2 normalise: drop extent-1 dims (they never change a position, Eq. (1)
+// P:L56 has a zero term for them) and fuse input dims i, i+1 that appear as
+// ..., i, i+1, ... in the output order: both layouts then see them as one
+// dimension of extent d[i]*d[i+1] (c(i+1,.) = c(i,.) * d(i) on both sides).
+// --------------------------------------------------------------------------
+static void fill_strides(Problem& pr) {
+    int64_t acc = 1;
+    for (int i = 0; i < pr.n; ++i) { pr.sin[i] = acc; acc *= pr.d[i]; }
+    acc = 1;
+    for (int j = 0; j < pr.n; ++j) { pr.sout[pr.p[j]] = acc; acc *= pr.d[pr.p[j]]; }
+    pr.vol = acc;
+}
+
+Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, bool fuse) {
+    Problem pr;
+    pr.esize = esize;
+    if (!fuse) {
+        pr.n = rank;
+        for (int i = 0; i < rank; ++i) { pr.d[i] = dims[i]; pr.p[i] = perm[i]; }
+        fill_strides(pr);
+        return pr;
+    }
+    // drop extent-1 dims
+    int newIdx[kMaxDims];
+    int n1 = 0;
+    int64_t d1[kMaxDims];
+    for (int i = 0; i < rank; ++i) {
+        if (dims[i] > 1) { newIdx[i] = n1; d1[n1++] = dims[i]; }
+        else newIdx[i] = -1;
+    }
+    int p1[kMaxDims];
+    int m = 0;
+    for (int j = 0; j < rank; ++j)
+        if (newIdx[perm[j]] >= 0) p1[m++] = newIdx[perm[j]];
+    if (n1 == 0) {  // every extent is 1: a one-element copy
+        pr.n = 1; pr.d[0] = 1; pr.p[0] = 0;
+        fill_strides(pr);
+        return pr;
+    }
+    // group output positions into runs of consecutive input dims
+    int gStart[kMaxDims], gLen[kMaxDims], ng = 0;
+    for (int j = 0; j < n1;) {
+        int s = p1[j], len = 1;
+        while (j + len < n1 && p1[j + len] == s + len) ++len;
+        gStart[ng] = s; gLen[ng] = len; ++ng;
+        j += len;
+    }
+    // groups sorted by input start give the fused input order
+    int order[kMaxDims];
+    for (int g = 0; g < ng; ++g) order[g] = g;
+    std::sort(order, order + ng, [&](int x, int y) { return gStart[x] < gStart[y]; });
+    int rankOf[kMaxDims];
+    for (int r = 0; r < ng; ++r) {
+        int g = order[r];
+        rankOf[g] = r;
+        int64_t e = 1;
+        for (int k = 0; k < gLen[g]; ++k) e *= d1[gStart[g] + k];
+        pr.d[r] = e;
+    }
+    pr.n = ng;
+    for (int g = 0; g < ng; ++g) pr.p[g] = rankOf[g];  // groups are in output order
+    fill_strides(pr);
+    return pr;
+}
+
+// --------------------------------------------------------------------------
+// a-4 model.  Constants are B200 measurements: the
+// sustained copy bandwidth of MEASURED_PEAKS.json and per-tile / per-slot
+// costs fitted from calibration sweeps (bench_suite.py --calibrate).
+// --------------------------------------------------------------------------
+namespace model {
+constexpr double kBwBytesPerUs = 6.3e6;   // achievable streaming read+write (MEASURED_PEAKS hbm_gbs ~6.5e6)
+constexpr double kSector = 32.0;          // L2 sector bytes (32-byte lines)
+constexpr double kClockMHz = 1800.0;      // SM clock under a memory-bound load
+constexpr double kIssuePerClk = 4.0;      // warp-instructions per SM per clock
+constexpr double kTileInstr = 90.0;       // per warp per tile: Alg. 1 decode, barrier, loop
+constexpr double kTileInstr64 = 160.0;    // same with 64-bit index arithmetic
+constexpr double kSlotInstr = 11.0;       // per warp per slot: LDG, STS, LDS, STG, masks, address
+constexpr double kLaunchUs = 3.0;         // launch + tail
+constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row locality overhead
+}  // namespace model
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Expected sectors touched by a run of `bytes` starting at an address that is
+// a multiple of `align` bytes (align a power of two).
+static double run_sectors(double bytes, int64_t align) {
+    if (align >= 32) return std::ceil(bytes / model::kSector);
+    // start offset uniform over the multiples of align inside a sector
+    double s = 0;
+    int cnt = 0;
+    for (int64_t off = 0; off < 32; off += align, ++cnt)
+        s += std::ceil((off + bytes) / model::kSector);
+    return s / cnt;
+}
+
+static int64_t pow2_align(int64_t x) {  // largest power of two dividing x (x>0), capped
+    if (x == 0) return 1 << 20;
+    int64_t a = 1;
+    while ((x % (a * 2)) == 0 && a < (1 << 20)) a *= 2;
+    return a;
+}
+
+struct TileCand {
+    TileParams tp{};
+    int64_t runIn = 0, runOut = 0;   // contiguous run lengths (elements) inside a full tile
+    int threads = 0, nreg = 0;
+    double cost_us = 1e30;
+    double dram_eff = 0;
+    int smem = 0;
+    bool ok = false;
+};
+
+// Shared-memory wavefronts for one warp access of element positions pos[32].
+static int warp_wavefronts(const int* pos, int nlanes, int esize) {
+    if (nlanes <= 0) return 0;
+    if (esize == 4) {
+        int worst = 0;
+        for (int b = 0; b < 32; ++b) {
+            int distinct[32], nd = 0;
+            for (int l = 0; l < nlanes; ++l) {
+                if ((pos[l] & 31) != b) continue;
+                bool dup = false;
+                for (int q = 0; q < nd; ++q) dup |= distinct[q] == pos[l];
+                if (!dup) distinct[nd++] = pos[l];
+            }
+            worst = std::max(worst, nd);
+        }
+        return worst;
+    }
+    // 8-byte elements: two half-warp phases, 16 bank pairs each
+    int total = 0;
+    for (int half = 0; half < 2; ++half) {
+        int worst = 0;
+        for (int b = 0; b < 16; ++b) {
+            int distinct[16], nd = 0;
+            for (int l = half * 16; l < std::min(nlanes, half * 16 + 16); ++l) {
+                if ((pos[l] & 15) != b) continue;
+                bool dup = false;
+                for (int q = 0; q < nd; ++q) dup |= distinct[q] == pos[l];
+                if (!dup) distinct[nd++] = pos[l];
+            }
+            worst = std::max(worst, nd);
+        }
+        total += worst;
+    }
+    return total;
+}
+
+// Exact bank-conflict cost of a smem layout over the whole tile (the paper's
+// TPR_shmem "calculated at runtime using the element positions given by
+// Equation (6)"), both the staging store (input order) and the
+// transposed read (output order).
+static long smem_cost(const TileParams& tp, int esize, int padEvery, int pad) {
+    const int V = tp.V;
+    const int nw = (V + 31) / 32;
+    const int step = std::max(1, nw / 8);  // sample ~8 warps (cf. P:L244's 10 samples)
+    long cost = 0;
+    int pos[32];
+    // staging store: consecutive k
+    for (int w = 0; w * 32 < V; w += step) {
+        int nl = std::min(32, V - w * 32);
+        for (int l = 0; l < nl; ++l) { int k = w * 32 + l; pos[l] = k + (k / padEvery) * pad; }
+        cost += warp_wavefronts(pos, nl, esize);
+    }
+    // transposed read: consecutive k' in output order -> pSh (Eq. 6)
+    for (int w = 0; w * 32 < V; w += step) {
+        int nl = std::min(32, V - w * 32);
+        for (int l = 0; l < nl; ++l) {
+            int kk = w * 32 + l, sh = 0;
+            for (int jj = 0; jj < tp.a; ++jj) {
+                int t = tp.tOutOrder[jj];
+                int c = kk % tp.tExt[t];
+                kk /= tp.tExt[t];
+                sh += c * tp.tCin[t];
+            }
+            pos[l] = sh + (sh / padEvery) * pad;
+        }
+        cost += warp_wavefronts(pos, nl, esize);
+    }
+    return cost;
+}
+
+// Build the tile of candidate run targets (Tin, Tout) in elements.
+static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
+                           const DeviceInfo& dev, int forceThreads) {
+    TileCand c;
+    const int n = pr.n;
+    int64_t need[kMaxDims];
+    for (int i = 0; i < n; ++i) need[i] = 1;
+    int inSplit = -1, outSplit = -1;
+    // input side: M_m = first input dims, last one possibly split
+    {
+        int64_t P = 1;
+        for (int i = 0; i < n; ++i) {
+            if (P * pr.d[i] >= Tin) {
+                int64_t ch = std::min(pr.d[i], ceil_div(Tin, P));
+                need[i] = std::max(need[i], ch);
+                if (ch < pr.d[i]) inSplit = i;
+                break;
+            }
+            need[i] = pr.d[i];
+            P *= pr.d[i];
+        }
+    }
+    // output side: M_k = first output dims
+    {
+        int64_t P = 1;
+        for (int j = 0; j < n; ++j) {
+            int i = pr.p[j];
+            if (P * pr.d[i] >= Tout) {
+                int64_t ch = std::min(pr.d[i], ceil_div(Tout, P));
+                need[i] = std::max(need[i], ch);
+                if (ch < pr.d[i]) outSplit = i;
+                break;
+            }
+            need[i] = pr.d[i];
+            P *= pr.d[i];
+        }
+    }
+    long double V = 1;
+    for (int i = 0; i < n; ++i) V *= (long double)need[i];
+    if (V > Vmax) return c;
+
+    TileParams& tp = c.tp;
+    std::memset(&tp, 0, sizeof(tp));
+    tp.V = (int32_t)V;
+    // tile dims: need > 1, ascending input dim
+    int tileOf[kMaxDims];
+    tp.a = 0;
+    for (int i = 0; i < n; ++i) {
+        tileOf[i] = -1;
+        if (need[i] > 1) {
+            tileOf[i] = tp.a;
+            tp.tExt[tp.a] = (int32_t)need[i];
+            tp.tSin[tp.a] = pr.sin[i];
+            tp.tSout[tp.a] = pr.sout[i];
+            ++tp.a;
+        }
+    }
+    {
+        int32_t acc = 1;
+        for (int t = 0; t < tp.a; ++t) { tp.tCin[t] = acc; acc *= tp.tExt[t]; }
+        int jj = 0;
+        acc = 1;
+        for (int j = 0; j < n; ++j) {
+            int t = tileOf[pr.p[j]];
+            if (t < 0) continue;
+            tp.tOutOrder[jj++] = t;
+            tp.tCout[t] = acc;
+            acc *= tp.tExt[t];
+        }
+    }
+    // grid dims (M̄_mk plus chunk indices of split dims): split dims first,
+    // then the rest in input order (one common order, R3)
+    int gridDim_[kMaxDims], ng = 0;
+    bool isSplit[kMaxDims] = {};
+    for (int i = 0; i < n; ++i) isSplit[i] = need[i] > 1 && need[i] < pr.d[i];
+    if (inSplit >= 0 && isSplit[inSplit]) gridDim_[ng++] = inSplit;
+    if (outSplit >= 0 && outSplit != inSplit && isSplit[outSplit]) gridDim_[ng++] = outSplit;
+    for (int i = 0; i < n; ++i) {
+        if (need[i] == 1) gridDim_[ng++] = i;
+        else if (isSplit[i] && i != inSplit && i != outSplit) gridDim_[ng++] = i;  // cannot happen
+    }
+    tp.h = ng;
+    tp.nSplit = 0;
+    int64_t acc = 1;
+    for (int g = 0; g < ng; ++g) {
+        int i = gridDim_[g];
+        int64_t ext = ceil_div(pr.d[i], need[i]);
+        tp.gC[g] = acc;
+        tp.gD[g] = ext;
+        tp.gSin[g] = need[i] * pr.sin[i];
+        tp.gSout[g] = need[i] * pr.sout[i];
+        acc *= ext;
+        if (isSplit[i]) {
+            int s = tp.nSplit++;
+            tp.splitLane[s] = g;
+            tp.splitChunk[s] = (int32_t)need[i];
+            tp.splitExt[s] = pr.d[i];
+            tp.splitTile[s] = tileOf[i];
+            tp.splitTail[s] = (int32_t)(pr.d[i] - (ext - 1) * need[i]);
+        }
+    }
+    tp.nTiles = acc;
+    for (int s = 0; s < tp.nSplit; ++s)
+        if (tp.splitChunk[s] > 256) return c;  // kernel packs split coordinates in 8 bits
+
+    // contiguous runs inside a full tile
+    {
+        int64_t r = 1;
+        for (int i = 0; i < n; ++i) {
+            r *= need[i];
+            if (need[i] < pr.d[i]) break;
+        }
+        c.runIn = std::min<int64_t>(r, tp.V);
+        r = 1;
+        for (int j = 0; j < n; ++j) {
+            int i = pr.p[j];
+            r *= need[i];
+            if (need[i] < pr.d[i]) break;
+        }
+        c.runOut = std::min<int64_t>(r, tp.V);
+    }
+
+    // threads x slots: NT*NREG >= V, NREG in {1,2,4,8}, NT multiple of 32
+    {
+        int bestT = 0, bestR = 0;
+        long bestWaste = 1L << 40;
+        for (int R : {8, 4, 2, 1}) {
+            int T = (int)ceil_div(tp.V, R);
+            T = (int)ceil_div(T, 32) * 32;
+            if (forceThreads) {
+                if ((long)forceThreads * R < tp.V) continue;
+                T = forceThreads;
+            }
+            if (T > 512) continue;
+            if (T < 64 && R > 1) continue;
+            long waste = (long)T * R - tp.V;
+            // prefer 128..512 threads, then least waste
+            long pen = waste + ((T < 128 || T > 512) ? tp.V : 0);
+            if (pen < bestWaste) { bestWaste = pen; bestT = T; bestR = R; }
+        }
+        if (bestT == 0) return c;
+        c.threads = bestT;
+        c.nreg = bestR;
+    }
+
+    // smem footprint with the worst-case padding (layout chosen for the winner)
+    {
+        int64_t words = tp.V + tp.V / 8 + 8;
+        c.smem = (int)(2 * ((words + 3) / 4 * 4) * pr.esize);
+        if (c.smem > dev.max_smem_per_block) return c;
+    }
+
+    // model: DRAM sectors of full tiles + slot issue + per-tile overhead
+    {
+        const double E = pr.esize;
+        int64_t aIn = 256;  // allocations are at least 256-byte aligned
+        for (int t = 0; t < tp.a; ++t)
+            if (tp.tSin[t] >= c.runIn) aIn = std::min(aIn, pow2_align(tp.tSin[t] * pr.esize));
+        for (int g = 0; g < tp.h; ++g) aIn = std::min(aIn, pow2_align(tp.gSin[g] * pr.esize));
+        int64_t aOut = 256;
+        for (int t = 0; t < tp.a; ++t)
+            if (tp.tSout[t] >= c.runOut) aOut = std::min(aOut, pow2_align(tp.tSout[t] * pr.esize));
+        for (int g = 0; g < tp.h; ++g) aOut = std::min(aOut, pow2_align(tp.gSout[g] * pr.esize));
+        aIn = std::max<int64_t>(aIn, pr.esize);
+        aOut = std::max<int64_t>(aOut, pr.esize);
+        double secIn = run_sectors(c.runIn * E, aIn) * ((double)tp.V / c.runIn);
+        double secOut = run_sectors(c.runOut * E, aOut) * ((double)tp.V / c.runOut);
+        // partial-sector reads of neighbouring runs usually hit in L2; partial
+        // writes cost a read-modify-write -- weight them fully.
+        double usefulSec = 2.0 * tp.V * E / model::kSector;
+        double modelSec = 0.5 * (secIn + tp.V * E / model::kSector) + secOut +
+                          ((double)tp.V / c.runIn + (double)tp.V / c.runOut) * model::kRunBytes /
+                              model::kSector;
+        c.dram_eff = usefulSec / modelSec;
+        // slots of ragged tiles are partly idle but still issued
+        const double bytes = (double)tp.nTiles * modelSec * model::kSector;
+        const double t_mem = bytes / model::kBwBytesPerUs;
+        const double warps = c.threads / 32.0;
+        const double perTile = warps * ((pr.vol >= (int64_t(1) << 31) ? model::kTileInstr64
+                                                                      : model::kTileInstr) +
+                                        c.nreg * model::kSlotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
+        const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
+                               std::max(1, dev.num_sms) / model::kClockMHz;
+        c.cost_us = std::max(t_mem, t_issue) + 0.25 * std::min(t_mem, t_issue) + model::kLaunchUs;
+    }
+    c.ok = true;
+    return c;
+}
+
+// Shared-memory layout: pick (padEvery, pad) with the fewest modelled
+// wavefronts (the L x (L+1) padding of P:L123 generalised), then footprint.
+static void choose_smem(TileParams& tp, int esize) {
+    const int ideal = esize == 4 ? 1 : 2;
+    const int nw = (tp.V + 31) / 32;
+    const int sampled = (nw + std::max(1, nw / 8) - 1) / std::max(1, nw / 8);
+    long best = smem_cost(tp, esize, 1 << 30, 0);
+    int bestEvery = 1 << 30, bestPad = 0;
+    if (best > (long)2 * sampled * ideal) {
+        std::vector<int> everies;
+        for (int t = 1; t < tp.a; ++t)
+            if (tp.tCin[t] >= 2 && tp.tCin[t] < tp.V) everies.push_back(tp.tCin[t]);
+        everies.push_back(32);
+        for (int ev : everies) {
+            for (int pad : {1, 2, 4}) {
+                if ((int64_t)(tp.V / ev) * pad > tp.V / 8) continue;  // footprint bound of build_tile
+                long cst = smem_cost(tp, esize, ev, pad);
+                if (cst < best || (cst == best && ev > bestEvery)) {
+                    best = cst; bestEvery = ev; bestPad = pad;
+                }
+            }
+        }
+    }
+    tp.padEvery = bestEvery;
+    tp.pad = bestPad;
+    int64_t words = tp.V + (bestPad ? (int64_t)((tp.V - 1) / bestEvery) * bestPad : 0) + 1;
+    tp.sbuf = (int32_t)((words + 3) / 4 * 4);
+}
+
+int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
+    int regs = 40 + q.nreg * (q.esize == 8 ? 6 : 5) + (q.idx64 ? q.nreg * 2 : 0);
+    regs = (regs + 7) / 8 * 8;
+    int byRegs = dev.regs_per_sm / std::max(1, regs * q.threads);
+    int byThreads = dev.max_threads_per_sm / std::max(1, q.threads);
+    int bySmem = q.smem > 0 ? dev.max_smem_per_sm / (q.smem + 1024) : 32;
+    return std::max(1, std::min(std::min(byRegs, byThreads), std::min(bySmem, 32)));
+}
+
+// --------------------------------------------------------------------------
+// a-3 classify + a-4 choose + a-5 materialise
+// --------------------------------------------------------------------------
+tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
+                        OccupancyFn occ) {
+    const Problem& pr = plan.prob;
+    KernelChoice& kc = plan.kc;
+    const int forced = opts ? opts->kernel : TT_KERNEL_AUTO;
+    const int E = pr.esize;
+
+    kc.idx64 = pr.vol >= (int64_t(1) << 31);
+
+    // (i) rank 1 after fusion: copy (identity; "trivial" permutation)
+    if (pr.n == 1 && (forced == TT_KERNEL_AUTO || forced == TT_KERNEL_COPY)) {
+        kc.kernel = TT_KERNEL_COPY;
+        kc.threads = opts && opts->threads ? opts->threads : 512;
+        kc.vec = 16 / E;
+        int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : 4;
+        int64_t chunks = ceil_div(pr.vol * E, 16 * 4 * (int64_t)kc.threads);
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)dev.num_sms * perSm));
+        kc.predicted_us = 2.0 * pr.vol * E / model::kBwBytesPerUs + model::kLaunchUs;
+        kc.model_dram_eff = 1.0;
+        return TT_SUCCESS;
+    }
+    if (forced == TT_KERNEL_COPY) return TT_UNSUPPORTED;
+    if (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE) return TT_UNSUPPORTED;
+
+    // generic staged tile (Tiled / Packed / PackedSplit classes)
+    const int Vmax = (E == 4) ? 8192 : 4096;
+    std::vector<int64_t> targets;
+    for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
+        targets.push_back(std::max<int64_t>(2, b / E));
+    TileCand best;
+    const int forceThreads = opts ? opts->threads : 0;
+    for (int64_t ti : targets) {
+        for (int64_t to : targets) {
+            int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
+            int64_t Tout = opts && opts->run_out ? opts->run_out : to;
+            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads);
+            if (!c.ok) continue;
+            if (!best.ok || c.cost_us < best.cost_us) best = c;
+        }
+    }
+    if (!best.ok) {
+        // fall back to the smallest legal tile
+        for (int64_t t = 2; t <= 64 && !best.ok; t *= 2) {
+            TileCand c = build_tile(pr, t, t, 12288, dev, forceThreads);
+            if (c.ok) best = c;
+        }
+    }
+    if (!best.ok) return TT_INTERNAL_ERROR;
+
+    plan.tile = best.tp;
+    choose_smem(plan.tile, E);
+    kc.kernel = TT_KERNEL_TILE;
+    kc.threads = best.threads;
+    kc.nreg = best.nreg;
+    kc.smem = 2 * plan.tile.sbuf * E;
+    kc.vec = 1;
+    kc.predicted_us = best.cost_us;
+    kc.model_dram_eff = best.dram_eff;
+    OccQuery q{TT_KERNEL_TILE, E, kc.nreg, 1, kc.threads, kc.smem, kc.idx64};
+    int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
+    if (perSm <= 0) perSm = estimate_occupancy(q, dev);
+    kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
+    return TT_SUCCESS;
+}
+
+// --------------------------------------------------------------------------
+// describe (JSON)
+// --------------------------------------------------------------------------
+template <typename T>
+static void arr(std::ostringstream& o, const T* v, int n) {
+    o << "[";
+    for (int i = 0; i < n; ++i) o << (i ? "," : "") << (long long)v[i];
+    o << "]";
+}
+
+static const char* kernel_name(int k) {
+    switch (k) {
+        case TT_KERNEL_COPY: return "copy";
+        case TT_KERNEL_TILE: return "tile";
+        case TT_KERNEL_ROWCOPY: return "rowcopy";
+        case TT_KERNEL_TILED2D: return "tiled2d";
+        default: return "auto";
+    }
+}
+
+std::string describe_json(const Plan& plan) {
+    std::ostringstream o;
+    const Problem& pr = plan.prob;
+    const KernelChoice& kc = plan.kc;
+    o << "{\"version\":" << TT_VERSION << ",\"device\":" << plan.device
+      << ",\"rank\":" << plan.rank << ",\"dims\":";
+    arr(o, plan.dims.data(), plan.rank);
+    o << ",\"perm\":";
+    arr(o, plan.perm.data(), plan.rank);
+    o << ",\"elem_size\":" << pr.esize << ",\"vol\":" << (long long)pr.vol;
+    o << ",\"fused\":{\"rank\":" << pr.n << ",\"dims\":";
+    arr(o, pr.d, pr.n);
+    o << ",\"perm\":";
+    arr(o, pr.p, pr.n);
+    o << "},\"kernel\":\"" << kernel_name(kc.kernel) << "\",\"threads\":" << kc.threads
+      << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
+      << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
+      << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
+      << ",\"model_dram_eff\":" << kc.model_dram_eff;
+    if (kc.kernel == TT_KERNEL_TILE) {
+        const TileParams& t = plan.tile;
+        o << ",\"tile\":{\"V\":" << t.V << ",\"sbuf\":" << t.sbuf << ",\"nTiles\":"
+          << (long long)t.nTiles << ",\"padEvery\":" << t.padEvery << ",\"pad\":" << t.pad
+          << ",\"ext\":";
+        arr(o, t.tExt, t.a);
+        o << ",\"cin\":";
+        arr(o, t.tCin, t.a);
+        o << ",\"cout\":";
+        arr(o, t.tCout, t.a);
+        o << ",\"out_order\":";
+        arr(o, t.tOutOrder, t.a);
+        o << ",\"sin\":";
+        arr(o, t.tSin, t.a);
+        o << ",\"sout\":";
+        arr(o, t.tSout, t.a);
+        o << ",\"split_tile\":";
+        arr(o, t.splitTile, t.nSplit);
+        o << ",\"split_lane\":";
+        arr(o, t.splitLane, t.nSplit);
+        o << ",\"split_chunk\":";
+        arr(o, t.splitChunk, t.nSplit);
+        o << ",\"split_ext\":";
+        arr(o, t.splitExt, t.nSplit);
+        o << ",\"grid_c\":";
+        arr(o, t.gC, t.h);
+        o << ",\"grid_d\":";
+        arr(o, t.gD, t.h);
+        o << ",\"grid_sin\":";
+        arr(o, t.gSin, t.h);
+        o << ",\"grid_sout\":";
+        arr(o, t.gSout, t.h);
+        o << "}";
+    }
+    o << "}";
+    return o.str();
+}
+
+}  // namespace tt

@@ -1,0 +1,155 @@
+// tt_internal.h -- plan representation shared by the host planner
+// (planner.cpp, no CUDA runtime calls) and the launch layer (api.cu /
+// kernels.cu).  Citations: P:Lnn = PAPER.md line nn (arXiv 1705.01598).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tt.h"
+
+namespace tt {
+
+constexpr int kMaxDims = TT_MAX_RANK;
+
+// ---------------------------------------------------------------------------
+// Normalised problem (row a-2): extent-1 dims dropped, in-order runs fused.
+// dims[0] stride-1; output dim j is input dim perm[j].
+// ---------------------------------------------------------------------------
+struct Problem {
+    int n = 0;
+    int64_t d[kMaxDims] = {};
+    int p[kMaxDims] = {};
+    int esize = 4;
+    int64_t vol = 1;
+    int64_t sin[kMaxDims] = {};   // c(i, I): input stride of input dim i
+    int64_t sout[kMaxDims] = {};  // c(i, O): output stride of input dim i
+};
+
+// ---------------------------------------------------------------------------
+// Generic staged-tile kernel parameters (Eqs. 2-6).
+//
+// A tile is the sub-volume M_mk (the union of the first input dims M_m and
+// the first output dims M_k), with at most one split dim per side
+// (PackedSplit).  Tile dims are listed in input order; the kernel
+// reads a tile with input-order index k (Eq. 4), stages it in shared memory
+// at position pos(k) = k + (k / padEvery) * pad, and writes it with
+// output-order index k' (Eqs. 5, 6).  The remaining dims (and the chunk
+// index of split dims) are the "major" grid dims M̄_mk decoded per tile with
+// the warp-parallel Algorithm 1 in ONE common order for both the
+// read and the write base (reading R3).
+// ---------------------------------------------------------------------------
+struct TileParams {
+    int64_t nTiles;
+    int32_t V;          // tile volume (elements)
+    int32_t sbuf;       // elements per shared-memory buffer incl. padding
+    int32_t a;          // number of tile dims
+    int32_t h;          // number of grid dims (<= 32, one warp lane each)
+    int32_t padEvery;   // smem layout: pos(k) = k + (k / padEvery) * pad
+    int32_t pad;
+    int32_t nSplit;     // number of split tile dims (0..2)
+    int32_t splitLane[2];   // grid lane carrying the split dim's chunk index
+    int32_t splitChunk[2];  // tile extent of the split dim
+    int32_t splitTile[2];   // tile-dim index of the split dim
+    int32_t splitTail[2];   // valid extent of the last chunk (== chunk if it divides)
+    int64_t splitExt[2];    // full extent of the split dim
+    // tile dims (tile-input order, i.e. ascending input dimension)
+    int32_t tExt[kMaxDims];       // tile extent
+    int32_t tCin[kMaxDims];       // c(q_i, M_mk^I): cumulative volume, tile-input order
+    int32_t tCout[kMaxDims];      // c(q_i, M_mk^O): cumulative volume, tile-output order
+    int32_t tOutOrder[kMaxDims];  // tile dims in output order (indices into the above)
+    int64_t tSin[kMaxDims];       // c(q_i, I): global input stride
+    int64_t tSout[kMaxDims];      // c(q_i, O): global output stride
+    // grid dims, one per warp lane (Alg. 1): b -> mod(floor(b / gC), gD) * stride
+    int64_t gC[kMaxDims];
+    int64_t gD[kMaxDims];
+    int64_t gSin[kMaxDims];
+    int64_t gSout[kMaxDims];
+};
+
+// Row-copy (fastest dim unchanged, long rows; TiledCopy class P:L141): each
+// row of `row` contiguous elements is contiguous on both sides.  Rows are
+// enumerated in OUTPUT order over the remaining dims.
+struct RowParams {
+    int64_t row;        // elements per row (fused dim 0)
+    int64_t nRows;
+    int32_t h;          // remaining dims
+    int64_t rC[kMaxDims];     // cumulative row count in output order
+    int64_t rD[kMaxDims];     // extent
+    int64_t rSin[kMaxDims];   // input stride
+    int64_t rSout[kMaxDims];  // output stride
+};
+
+// Two-dimensional tiled transpose of the fused problem's dims (0, p0) with
+// all other dims as a batch (Tiled class), 128-bit accesses.
+struct Tiled2DParams {
+    int64_t d0, d1;           // input dim 0 (stride 1) and output-fastest input dim p0
+    int64_t sIn1;             // input stride of dim p0
+    int64_t sOut0;            // output stride of dim 0
+    int64_t tiles0, tiles1;   // tiles along d0, d1
+    int64_t nTiles;           // tiles0 * tiles1 * batch
+    int32_t h;                // batch dims
+    int64_t bC[kMaxDims], bD[kMaxDims], bSin[kMaxDims], bSout[kMaxDims];
+};
+
+struct KernelChoice {
+    int kernel = TT_KERNEL_AUTO;   // tt_kernel_t
+    int threads = 0;
+    int nreg = 0;                  // slots per thread (TILE)
+    int vec = 1;                   // elements per vector access
+    int grid = 0;
+    int smem = 0;                  // dynamic shared memory bytes
+    bool idx64 = false;
+    int tile0 = 0, tile1 = 0;      // TILED2D tile
+    double predicted_us = 0.0;
+    double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
+};
+
+struct DeviceInfo {
+    int device = -1;               // -1: offline plan
+    int num_sms = 148;
+    int max_smem_per_block = 232448;
+    int max_smem_per_sm = 233472;
+    int max_threads_per_sm = 2048;
+    int regs_per_sm = 65536;
+};
+
+// Occupancy oracle: CTAs per SM for a kernel configuration (launch layer
+// supplies the CUDA answer; offline plans use an estimate).
+struct OccQuery {
+    int kernel, esize, nreg, vec, threads, smem;
+    bool idx64;
+};
+typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
+
+struct ShardInfo;  // defined in dist.cpp
+
+struct Plan {
+    uint32_t magic = 0x54545054u;  // "TTPT"
+    int device = -1;
+    void* stream = nullptr;
+    int rank = 0;
+    std::vector<int64_t> dims;     // as given
+    std::vector<int> perm;
+    Problem prob;                  // fused
+    KernelChoice kc;
+    TileParams tile{};
+    RowParams row{};
+    Tiled2DParams t2d{};
+    ShardInfo* shard = nullptr;    // sharded plans only
+};
+
+// planner.cpp ---------------------------------------------------------------
+tt_status_t validate(int rank, const int64_t* dims, const int* perm, size_t elem_size);
+Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, bool fuse);
+tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
+                        OccupancyFn occ);
+std::string describe_json(const Plan& plan);
+int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev);
+
+// kernels.cu ----------------------------------------------------------------
+int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev);
+int launch_plan(const Plan& plan, const void* in, void* out, void* stream);  // cudaError_t
+
+}  // namespace tt

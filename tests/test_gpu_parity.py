@@ -1,0 +1,245 @@
+"""GPU parity: libtt.so's CUDA path vs the CPU oracle, element by element,
+bit-exact (tolerance 0, also for float payloads: DESIGN.md reading R12).
+
+Every call goes through the C ABI (the ctypes binding).  Inputs are the
+seeded words of tt_workloads (shared generator, no permutation arithmetic).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1705_01598_b200 as tt
+from oracle import oracle as orc
+import tt_workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+_TD = {4: torch.int32, 8: torch.int64}
+_ND = {4: np.int32, 8: np.int64}
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests (no CPU fallback)")
+    return torch.device("cuda", 0)
+
+
+def to_dev(words):
+    esize = words.dtype.itemsize
+    return torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
+
+
+def run_gpu(dims, perm, words, offset=0, **opts):
+    """Permute on the GPU through tt_plan/tt_execute; returns numpy words."""
+    esize = words.dtype.itemsize
+    n = words.size
+    src = torch.empty(n + offset, dtype=_TD[esize], device=_dev())
+    src[offset:] = to_dev(words)
+    dst = torch.full((n + offset,), -0x21524111, dtype=_TD[esize], device=_dev())
+    plan = tt.Plan(dims, perm, esize, **opts)
+    plan.execute(src[offset:], dst[offset:])
+    torch.cuda.synchronize()
+    out = dst[offset:].cpu().numpy().view(words.dtype)
+    if offset:
+        assert (dst[:offset].cpu().numpy() == -0x21524111).all(), "wrote before the output"
+    plan.destroy()
+    return out
+
+
+def check(dims, perm, esize, seed=1, **opts):
+    words = wl.random_words(int(np.prod(dims)), esize, seed)
+    got = run_gpu(dims, perm, words, **opts)
+    want = orc.permute_threaded(dims, perm, words)
+    if not np.array_equal(got, want):
+        bad = np.nonzero(got != want)[0]
+        raise AssertionError(f"{dims} {perm} e{esize} {opts}: {bad.size} mismatches, first at "
+                             f"{bad[:8].tolist()}")
+
+
+def test_s0_config0():
+    c = wl.s0()
+    check(c.dims, c.perm, c.esize, seed=c.seed)
+    # index-encoded input reproduces the hand-worked golden values
+    got = run_gpu(c.dims, c.perm, wl.index_words(455, 4))
+    assert got[:12].tolist() == [0, 91, 182, 273, 364, 1, 92, 183, 274, 365, 2, 93]
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+def test_exhaustive_tiny(esize):
+    """Every permutation of rank <= 4 with extents in {1, 2, 3, 5}."""
+    for rank in (1, 2, 3, 4):
+        for dims in itertools.product((1, 2, 3, 5), repeat=rank):
+            if rank == 4 and dims.count(1) > 1:
+                continue
+            words = wl.random_words(int(np.prod(dims)), esize, sum(dims))
+            for perm in itertools.permutations(range(rank)):
+                got = run_gpu(dims, perm, words)
+                np.testing.assert_array_equal(got, orc.permute(dims, perm, words),
+                                              err_msg=f"{dims} {perm}")
+
+
+RANDOM_SHAPES = [
+    ((67, 45), (1, 0)),
+    ((1000, 999), (1, 0)),
+    ((4096, 33), (1, 0)),
+    ((33, 4096), (1, 0)),
+    ((7, 13, 5), (2, 0, 1)),
+    ((129, 65, 7), (2, 1, 0)),
+    ((300, 5, 3, 17), (0, 3, 2, 1)),        # fastest dim unchanged
+    ((2, 300, 3, 17), (0, 3, 2, 1)),        # fastest unchanged, short rows
+    ((5, 3, 2, 4, 35, 33, 37, 40), (7, 4, 0, 5, 2, 6, 3, 1)),  # Set-2 shape
+    ((2, 3, 4, 3, 2, 2, 3, 2, 20, 18, 22, 24), tuple(range(11, -1, -1))),
+    ((11, 4, 3, 5, 3, 2, 6, 8, 7, 10, 3, 3), (0, 7, 8, 1, 3, 9, 2, 4, 5, 10, 11, 6)),
+    ((1, 77, 1, 3, 1), (4, 3, 2, 1, 0)),    # extent-1 dims
+    ((1025, 3, 2), (2, 1, 0)),              # large first input, small first output (PackedSplit)
+    ((3, 2, 1025), (2, 1, 0)),
+]
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("dims,perm", RANDOM_SHAPES)
+def test_shapes(dims, perm, esize):
+    vol = int(np.prod(dims))
+    if vol > 4_000_000:
+        # keep the oracle in seconds: scale down, keep perm and raggedness
+        c = wl.scaled(wl.Case("x", dims, perm, esize, 3), 2_000_000)
+        dims = c.dims
+    check(dims, perm, esize)
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("run", [(2, 2), (8, 3), (32, 32), (64, 16), (16, 256), (256, 256)])
+def test_forced_tiles(run, esize):
+    """Force tile geometries so splits, ragged chunks and paddings all occur."""
+    for dims, perm in [((37, 29, 11), (2, 0, 1)), ((130, 70), (1, 0)), ((9, 8, 7, 6, 5), (3, 4, 0, 2, 1))]:
+        check(dims, perm, esize, run_in=run[0], run_out=run[1])
+
+
+@pytest.mark.parametrize("threads", [64, 96, 256, 512])
+def test_forced_threads(threads):
+    check((97, 89, 3), (1, 2, 0), 4, threads=threads)
+    check((97, 89, 3), (1, 2, 0), 8, threads=threads)
+
+
+def test_copy_kernel_alignment():
+    for esize in (4, 8):
+        for n in (1, 3, 17, 1000, 4099):
+            words = wl.random_words(n, esize, n)
+            for off in (0, 1, 2, 3):
+                got = run_gpu((n,), (0,), words, offset=off)
+                np.testing.assert_array_equal(got, words)
+        check((5, 6, 7), (0, 1, 2), esize)
+
+
+def test_misaligned_pointers():
+    for esize in (4, 8):
+        for dims, perm in [((67, 45), (1, 0)), ((7, 13, 5), (2, 0, 1)), ((30, 40, 3), (0, 2, 1))]:
+            words = wl.random_words(int(np.prod(dims)), esize, 9)
+            for off in (1, 3):
+                got = run_gpu(dims, perm, words, offset=off)
+                np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
+
+
+@pytest.mark.parametrize("idx", range(0, 57, 4))
+def test_ttc_suite_scaled(idx):
+    c = wl.s2_ttc()[idx]
+    s = wl.scaled(c, 1_500_000)
+    check(s.dims, s.perm, s.esize, seed=c.seed)
+
+
+@pytest.mark.parametrize("rank", range(2, 13))
+def test_random_suite_scaled(rank):
+    cases = [c for c in wl.s3_random(per_cell=2, ranks=[rank]) if c.tags[0] == "S3"]
+    for c in cases[::3]:
+        s = wl.scaled(c, 1_000_000)
+        check(s.dims, s.perm, s.esize, seed=c.seed)
+
+
+def test_set2_shapes_scaled():
+    for c in [x for x in wl.s3_random(per_cell=0, set2_random=6) if x.tags[0] == "SET2"]:
+        s = wl.scaled(c, 2_000_000)
+        check(s.dims, s.perm, s.esize, seed=c.seed)
+
+
+def _sampled_full(case, n_samples=1 << 20, **opts):
+    """Full-size run in bench.py's launch configuration, checked on sampled
+    positions computed one by one by the oracle, plus the multiset-sum
+    invariant over all elements."""
+    words = case.words()
+    esize = case.esize
+    src = to_dev(words)
+    dst = torch.empty_like(src)
+    plan = tt.Plan(case.dims, case.perm, esize, **opts)
+    plan.execute(src, dst)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(case.seed & 0xFFFF)
+    pos = np.concatenate([rng.integers(0, case.vol, size=n_samples),
+                          np.arange(min(4096, case.vol)),
+                          np.arange(max(0, case.vol - 4096), case.vol)])
+    got = dst[torch.from_numpy(pos).to(dst.device)].cpu().numpy().view(words.dtype)
+    want = orc.permute_sample(case.dims, case.perm, words, pos)
+    np.testing.assert_array_equal(got, want)
+    # wrapping sums of the bit patterns are permutation invariant
+    assert int(dst.sum(dtype=torch.int64)) == int(src.sum(dtype=torch.int64))
+    plan.destroy()
+    del src, dst
+    torch.cuda.empty_cache()
+
+
+def test_full_size_s1():
+    _sampled_full(wl.s1())
+
+
+def test_full_size_suite_samples():
+    for c in wl.s2_ttc()[::19] + [wl.s5_sharded()[4]]:
+        _sampled_full(c, n_samples=1 << 18)
+    s3 = wl.s3_random(per_cell=1)
+    for c in s3[::97]:
+        _sampled_full(c, n_samples=1 << 18)
+
+
+def test_index64_path():
+    """Volume >= 2^31 elements exercises the 64-bit index kernels."""
+    c = wl.Case("big", (65539, 32771), (1, 0), 4, 123)
+    assert c.vol >= (1 << 31)
+    _sampled_full(c, n_samples=1 << 16)
+
+
+def test_stream_and_errors():
+    s = torch.cuda.Stream()
+    words = wl.random_words(6000, 4, 1)
+    src = to_dev(words)
+    dst = torch.empty_like(src)
+    plan = tt.Plan((60, 100), (1, 0), 4, stream=s)
+    with torch.cuda.stream(s):
+        plan.execute(src, dst)
+    s.synchronize()
+    np.testing.assert_array_equal(dst.cpu().numpy().view(np.uint32), orc.permute((60, 100), (1, 0), words))
+    with pytest.raises(tt.TTError):
+        plan.execute(src, src)
+    plan.destroy()
+    with pytest.raises(tt.TTError):
+        plan.execute(src, dst)
+
+
+def test_execute_host_roundtrip():
+    dims, perm = (300, 200, 3), (2, 0, 1)
+    words = wl.random_words(180000, 8, 4)
+    hin = torch.from_numpy(words.view(np.int64).copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    din = torch.empty(hin.shape, dtype=torch.int64, device=_dev())
+    dout = torch.empty_like(din)
+    plan = tt.Plan(dims, perm, 8)
+    plan.execute_host(hin, hout, din, dout)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hout.numpy().view(np.uint64), orc.permute(dims, perm, words))
+
+
+def test_permute_torch_matches_torch_semantics():
+    x = torch.arange(2 * 3 * 4 * 5, dtype=torch.float32, device=_dev()).reshape(2, 3, 4, 5)
+    for axes in [(3, 2, 1, 0), (0, 2, 1, 3), (1, 3, 0, 2)]:
+        y = tt.permute_torch(x, axes)
+        assert torch.equal(y, x.permute(*axes).contiguous())

@@ -1,0 +1,211 @@
+"""CPU tests of libtt.so's host side: exports, validation, normalisation,
+classification, and the planner's tile geometry (through tt_plan_offline and a
+plan interpreter that replays the kernel's index arithmetic on the host and is
+compared with the oracle).  No CUDA device needed."""
+import ctypes
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1705_01598_b200 as tt
+from oracle import oracle as orc
+import tt_workloads as wl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    with open(os.path.join(ROOT, "include", "tt.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"\b(tt_[a-z_]+)\s*\(", hdr))
+    assert {"tt_plan", "tt_execute", "tt_destroy", "tt_plan_describe", "tt_comm_init",
+            "tt_plan_sharded", "tt_execute_sharded", "tt_comm_destroy",
+            "tt_status_string"} <= declared
+    lib = ctypes.CDLL(tt.library_path)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert tt.lib.tt_version() == 1
+    assert tt.lib.tt_status_string(0) == b"TT_SUCCESS"
+    assert tt.lib.tt_status_string(4) == b"TT_UNSUPPORTED"
+
+
+def _offline_status(dims, perm, esize):
+    n = len(dims)
+    h = ctypes.c_void_p()
+    d = (ctypes.c_int64 * max(1, n))(*dims)
+    p = (ctypes.c_int * max(1, n))(*perm)
+    st = tt.lib.tt_plan_offline(ctypes.byref(h), n, d, p, esize, None, None)
+    if st == 0:
+        tt.lib.tt_destroy(h)
+    return st
+
+
+def test_validation():
+    assert _offline_status((2, 3), (1, 0), 4) == 0
+    assert _offline_status((), (), 4) == 2            # rank 0
+    assert _offline_status((2, 3), (0, 0), 4) == 2    # not a bijection
+    assert _offline_status((2, 3), (0, 2), 4) == 2
+    assert _offline_status((2, 0), (1, 0), 4) == 2    # extent 0 (reading R9)
+    assert _offline_status((2, 3), (1, 0), 2) == 4    # elem size (R11)
+    assert _offline_status((2, 3), (1, 0), 16) == 4
+    assert _offline_status([2] * 33, list(range(33)), 4) == 2  # rank > 32
+    assert _offline_status([1 << 31, 1 << 31], (1, 0), 8) == 2  # vol*E >= 2^62
+    assert tt.lib.tt_destroy(None) == 1
+    assert tt.lib.tt_execute(None, None, None) == 1
+
+
+def test_offline_plan_cannot_execute():
+    n, d, p = 2, (ctypes.c_int64 * 2)(4, 4), (ctypes.c_int * 2)(1, 0)
+    h = ctypes.c_void_p()
+    assert tt.lib.tt_plan_offline(ctypes.byref(h), n, d, p, 4, None, None) == 0
+    assert tt.lib.tt_execute(h, 16, 1024) == 3       # TT_INVALID_DEVICE
+    assert tt.lib.tt_execute(h, 16, 16) == 2         # in == out
+    assert tt.lib.tt_execute(h, 16, 1026) == 2       # misaligned
+    assert tt.lib.tt_destroy(h) == 0
+
+
+@pytest.mark.parametrize("dims,perm,fdims,fperm", [
+    ((112, 112, 112, 104), (2, 3, 0, 1), (12544, 11648), (1, 0)),
+    ((3, 4, 5, 6), (1, 0, 3, 2), (3, 4, 5, 6), (1, 0, 3, 2)),
+    ((7, 13, 5), (2, 0, 1), (91, 5), (1, 0)),
+    ((5, 6, 7), (0, 1, 2), (210,), (0,)),
+    ((5, 1, 7, 1), (3, 2, 1, 0), (5, 7), (1, 0)),
+    ((1, 1), (1, 0), (1,), (0,)),
+    ((2, 3, 4, 5, 6), (0, 3, 4, 1, 2), (2, 12, 30), (0, 2, 1)),
+])
+def test_normalisation(dims, perm, fdims, fperm):
+    j = tt.plan_offline(dims, perm, 4)
+    assert tuple(j["fused"]["dims"]) == fdims
+    assert tuple(j["fused"]["perm"]) == fperm
+    assert j["kernel"] == ("copy" if len(fdims) == 1 else "tile")
+
+
+def interpret_tile_plan(j, words):
+    """Replay the tile kernel's index arithmetic (kernels.cu) for plan JSON j:
+    Algorithm-1 decode of the tile base, Eq. (4) input-order minor offsets,
+    staging positions, Eq. (5)/(6) output-order offsets, ragged-chunk masks."""
+    t = j["tile"]
+    V, a = t["V"], len(t["ext"])
+    ext, cin, order = t["ext"], t["cin"], t["out_order"]
+    sin, sout = t["sin"], t["sout"]
+    pe, pad = t["padEvery"], t["pad"]
+    st, sl, sc, se = t["split_tile"], t["split_lane"], t["split_chunk"], t["split_ext"]
+    tails = [se[s] - (-(-se[s] // sc[s]) - 1) * sc[s] for s in range(len(st))]
+    gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
+    vol = int(np.prod(j["dims"]))
+    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
+    written = np.zeros(vol, dtype=np.int64)
+    # per-slot tables
+    gin, pin, cin_s = [], [], []
+    for k in range(V):
+        rem, off, cs = k, 0, [0, 0]
+        for i in range(a):
+            c = rem % ext[i]
+            rem //= ext[i]
+            off += c * sin[i]
+            for s in range(len(st)):
+                if st[s] == i:
+                    cs[s] = c
+        gin.append(off)
+        pin.append(k + (k // pe) * pad)
+        cin_s.append(cs)
+    assert len(set(pin)) == V and max(pin) < t["sbuf"]
+    gout, psh, cout_s = [], [], []
+    for k in range(V):
+        rem, off, sh, cs = k, 0, 0, [0, 0]
+        for ti in order:
+            c = rem % ext[ti]
+            rem //= ext[ti]
+            off += c * sout[ti]
+            sh += c * cin[ti]
+            for s in range(len(st)):
+                if st[s] == ti:
+                    cs[s] = c
+        gout.append(off)
+        psh.append(sh + (sh // pe) * pad)
+        cout_s.append(cs)
+    for tile in range(t["nTiles"]):
+        q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
+        ib = sum(q[g] * gSi[g] for g in range(len(gC)))
+        ob = sum(q[g] * gSo[g] for g in range(len(gC)))
+        ragged = [q[sl[s]] == gD[sl[s]] - 1 for s in range(len(st))]
+        smem = {}
+        for k in range(V):
+            if all((not ragged[s]) or cin_s[k][s] < tails[s] for s in range(len(st))):
+                smem[pin[k]] = words[ib + gin[k]]
+        for k in range(V):
+            if all((not ragged[s]) or cout_s[k][s] < tails[s] for s in range(len(st))):
+                out[ob + gout[k]] = smem[psh[k]]
+                written[ob + gout[k]] += 1
+    assert (written == 1).all(), "tile decomposition must cover every output once"
+    return out
+
+
+CASES = [
+    ((7, 13, 5), (2, 0, 1)),
+    ((67, 45), (1, 0)),
+    ((5, 3, 2, 4, 7, 6), (4, 0, 5, 2, 3, 1)),
+    ((2, 3, 4, 3, 2, 2, 3, 2, 5, 4), tuple(range(9, -1, -1))),
+    ((33, 9, 70), (0, 2, 1)),
+    ((3, 100, 7), (1, 2, 0)),
+    ((300, 5, 3), (1, 2, 0)),
+    ((129, 65), (1, 0)),
+    ((4, 5, 6, 7), (3, 1, 0, 2)),
+]
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("dims,perm", CASES)
+def test_plan_interpreter_matches_oracle(dims, perm, esize):
+    j = tt.plan_offline(dims, perm, esize)
+    words = wl.random_words(int(np.prod(dims)), esize, 77)
+    want = orc.permute(dims, perm, words)
+    if j["kernel"] == "copy":
+        np.testing.assert_array_equal(words, want)
+        return
+    # the interpreter works on the fused problem the plan describes
+    fj = dict(j)
+    fj["dims"] = j["fused"]["dims"]
+    got = interpret_tile_plan(fj, words)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("run", [(2, 2), (4, 16), (16, 4), (64, 64), (3, 5)])
+def test_forced_runs_cover(run):
+    dims, perm = (11, 6, 9, 5), (2, 3, 1, 0)
+    j = tt.plan_offline(dims, perm, 4, run_in=run[0], run_out=run[1])
+    words = wl.random_words(int(np.prod(dims)), 4, 5)
+    fj = dict(j)
+    fj["dims"] = j["fused"]["dims"]
+    np.testing.assert_array_equal(interpret_tile_plan(fj, words), orc.permute(dims, perm, words))
+
+
+def test_split_chunks_and_smem_bounds_on_suites():
+    """Planner invariants over the benchmark suites: chunks <= 256, staging
+    positions < 2^14, smem within the B200 opt-in limit, tiles <= 2^31."""
+    cases = [wl.s1()] + wl.s2_ttc() + wl.s3_random(per_cell=1) + wl.s4_alignment()[:3]
+    kinds = {}
+    for c in cases:
+        j = tt.plan_offline(c.dims, c.perm, c.esize)
+        kinds[j["kernel"]] = kinds.get(j["kernel"], 0) + 1
+        if j["kernel"] != "tile":
+            continue
+        t = j["tile"]
+        assert all(ch <= 256 for ch in t["split_chunk"])
+        assert t["sbuf"] < (1 << 14)
+        assert j["smem"] <= 232448
+        assert t["nTiles"] < (1 << 31)
+        assert t["V"] <= j["threads"] * j["nreg"]
+    assert kinds.get("tile", 0) > 50
+
+
+def test_s1_plan_shape():
+    j = tt.plan_offline((16384, 16384), (1, 0), 4)
+    assert j["kernel"] == "tile"
+    t = j["tile"]
+    # both runs at least 128 bytes, bank-conflict-free staging
+    assert min(t["ext"]) * 4 >= 128
+    assert j["grid"] >= 148
