@@ -195,20 +195,39 @@ tt_status_t tt_comm_init(tt_comm_t* comm, const void* nccl_unique_id, int nranks
 tt_status_t tt_comm_destroy(tt_comm_t comm);
 
 /*
- * tt_plan_sharded -- plan the sharded permutation of global_dims by perm.
- * The shard extent global_dims[n-1] and, for the redistribution case,
- * global_dims[perm[n-1]] must be divisible by nranks (else TT_UNSUPPORTED).
- * Allocates 2 x shard bytes of device staging for the redistribution case.
+ * tt_plan_sharded -- plan the sharded permutation of a tensor of `rank` dims
+ * with global extents global_dims[rank] by perm[rank] (same conventions as
+ * tt_plan) on the communicator's device; the process rank and the rank count
+ * come from `comm`.  global_dims[rank-1] and, for the redistribution case,
+ * global_dims[perm[rank-1]] must be divisible by the number of ranks (else
+ * TT_UNSUPPORTED).  The redistribution case allocates 2 x shard bytes of
+ * device staging (freed by tt_destroy).
  */
 tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int rank, const int64_t* global_dims,
                             const int* perm, size_t elem_size, tt_stream_t stream);
 
-/* Local input slab -> local output slab (device pointers, shard bytes each).
- * Collective: every rank of the communicator must call it. */
+/*
+ * tt_plan_sharded_offline -- the same geometry and sub-plans for process
+ * `proc` of `nranks` without a communicator or GPU (describe only; executing
+ * returns TT_INVALID_DEVICE).
+ */
+tt_status_t tt_plan_sharded_offline(tt_plan_t* plan, int nranks, int proc, int rank,
+                                    const int64_t* global_dims, const int* perm, size_t elem_size);
+
+/*
+ * tt_execute_sharded -- local input slab -> local output slab (device
+ * pointers, shard bytes each), enqueued on the plan's stream.  Collective:
+ * every rank of the communicator must call it.  Local case: 1 kernel;
+ * redistribution: pack kernel, ncclAlltoAll, unpack kernel.
+ */
 tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_local);
 
-/* Shard geometry of a sharded plan: local input dims and local output dims
- * (output order), rank entries each. */
+/* Milliseconds of the last tt_execute_sharded's pack / all-to-all / unpack
+ * (synchronises on that execution); zeros for the local case. */
+tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3);
+
+/* Shard geometry: local input dims and local output dims (output order),
+ * `rank` entries each (either pointer may be NULL). */
 tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* local_out_dims);
 
 #if defined(__GNUC__)

@@ -18,7 +18,7 @@ import os
 __all__ = [
     "TTError", "Plan", "plan_offline", "permute_torch", "lib", "library_path",
     "KERNEL_AUTO", "KERNEL_COPY", "KERNEL_TILE", "KERNEL_ROWCOPY", "KERNEL_TILED2D",
-    "Comm", "ShardedPlan", "unique_id",
+    "Comm", "ShardedPlan", "unique_id", "plan_sharded_offline",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,6 +73,9 @@ def _load():
         "tt_comm_init": [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int],
         "tt_comm_destroy": [vp],
         "tt_plan_sharded": [ctypes.POINTER(vp), vp, ctypes.c_int, i64p, ip, ctypes.c_size_t, vp],
+        "tt_plan_sharded_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    i64p, ip, ctypes.c_size_t],
+        "tt_sharded_timings": [vp, ctypes.POINTER(ctypes.c_float)],
         "tt_execute_sharded": [vp, vp, vp],
         "tt_plan_shard_dims": [vp, i64p, i64p],
     }
@@ -236,4 +239,4 @@ def permute_torch(x, axes, out=None, stream=None, **opts):
     return out
 
 
-from ._dist import Comm, ShardedPlan, unique_id  # noqa: E402
+from ._dist import Comm, ShardedPlan, unique_id, plan_sharded_offline  # noqa: E402

@@ -60,7 +60,7 @@ class ShardedPlan:
         self.comm = comm
         self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
         h = ctypes.c_void_p()
-        _check(lib.tt_plan_sharded(ctypes.byref(h), comm._h, comm.rank, d, p, self.elem_size,
+        _check(lib.tt_plan_sharded(ctypes.byref(h), comm._h, n, d, p, self.elem_size,
                                    _stream_handle(stream)), "tt_plan_sharded")
         self._h = h
         a = (ctypes.c_int64 * n)()
@@ -78,6 +78,12 @@ class ShardedPlan:
     def describe(self) -> dict:
         return _describe(self._h)
 
+    def timings(self):
+        """(pack, all-to-all, unpack) milliseconds of the last execute."""
+        ms = (ctypes.c_float * 3)()
+        _check(lib.tt_sharded_timings(self._h, ms), "tt_sharded_timings")
+        return tuple(float(x) for x in ms)
+
     @property
     def launches(self) -> int:
         return lib.tt_plan_launches(self._h)
@@ -92,3 +98,16 @@ class ShardedPlan:
             self.destroy()
         except Exception:
             pass
+
+
+def plan_sharded_offline(nranks: int, proc: int, global_dims, perm, elem_size: int) -> dict:
+    """Sharded geometry and sub-plans for process ``proc`` of ``nranks``,
+    without a communicator or GPU (JSON description)."""
+    n, d, p = _arrays(global_dims, perm)
+    h = ctypes.c_void_p()
+    _check(lib.tt_plan_sharded_offline(ctypes.byref(h), int(nranks), int(proc), n, d, p,
+                                       int(elem_size)), "tt_plan_sharded_offline")
+    try:
+        return _describe(h)
+    finally:
+        lib.tt_destroy(h)

@@ -12,7 +12,7 @@
 
 using namespace tt;
 
-namespace {
+namespace tt {
 
 Plan* as_plan(tt_plan_t h) {
     Plan* p = reinterpret_cast<Plan*>(h);
@@ -42,9 +42,9 @@ tt_status_t query_device(DeviceInfo& dev) {
     return TT_SUCCESS;
 }
 
-tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, const int* perm,
-                      size_t elem_size, tt_stream_t stream, const DeviceInfo& dev,
-                      const tt_plan_options_t* opts, OccupancyFn occ) {
+tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
+                        size_t elem_size, void* stream, const DeviceInfo& dev,
+                        const tt_plan_options_t* opts, OccupancyFn occ) {
     if (out == nullptr) return TT_INVALID_PARAMETER;
     *out = nullptr;
     tt_status_t st = validate(rank, dims, perm, elem_size);
@@ -63,11 +63,28 @@ tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
-    *out = reinterpret_cast<tt_plan_t>(p);
+    *out = p;
     return TT_SUCCESS;
 }
 
-}  // namespace
+void destroy_plan(Plan* p) {
+    if (p == nullptr) return;
+    if (p->shard) destroy_shard(p->shard);
+    p->shard = nullptr;
+    p->magic = 0;
+    delete p;
+}
+
+}  // namespace tt
+
+static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, const int* perm,
+                             size_t elem_size, tt_stream_t stream, const DeviceInfo& dev,
+                             const tt_plan_options_t* opts, OccupancyFn occ) {
+    Plan* p = nullptr;
+    tt_status_t st = create_plan(&p, rank, dims, perm, elem_size, stream, dev, opts, occ);
+    if (out) *out = reinterpret_cast<tt_plan_t>(p);
+    return st;
+}
 
 extern "C" {
 
@@ -168,7 +185,7 @@ tt_status_t tt_plan_describe(tt_plan_t plan, char* buf, size_t len) {
     Plan* p = as_plan(plan);
     if (p == nullptr) return TT_INVALID_PLAN;
     if (buf == nullptr || len == 0) return TT_INVALID_PARAMETER;
-    std::string s = describe_json(*p);
+    std::string s = p->shard ? describe_shard_json(*p) : describe_json(*p);
     if (s.size() + 1 > len) {
         std::memcpy(buf, s.data(), len - 1);
         buf[len - 1] = '\0';
@@ -181,14 +198,14 @@ tt_status_t tt_plan_describe(tt_plan_t plan, char* buf, size_t len) {
 int tt_plan_launches(tt_plan_t plan) {
     Plan* p = as_plan(plan);
     if (p == nullptr) return -1;
+    if (p->shard) return shard_launches(p->shard);
     return 1;
 }
 
 tt_status_t tt_destroy(tt_plan_t plan) {
     Plan* p = as_plan(plan);
     if (p == nullptr) return TT_INVALID_PLAN;
-    p->magic = 0;
-    delete p;
+    destroy_plan(p);
     return TT_SUCCESS;
 }
 

@@ -65,8 +65,8 @@ struct TileBase {
 // same decode order serves both sums (reading R3).  A lane holding
 // a split dim also reports whether this tile is that dim's ragged last chunk
 // (PackedSplit edge), gathered with one ballot.
-template <typename I>
-__device__ __forceinline__ TileBase<I> decode_tile(const TileParams& p, I t, int lane) {
+template <typename I, typename P>
+__device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
     I vin = 0, vout = 0;
     bool ragged = false;
     if (lane < p.h) {
@@ -193,6 +193,105 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
 }
 
 // ---------------------------------------------------------------------------
+// vectorised 2-D tiled transpose (Tiled class)
+// ---------------------------------------------------------------------------
+template <typename W, int VW> struct VecOf;
+template <> struct VecOf<uint32_t, 4> { typedef uint4 T; };
+template <> struct VecOf<uint32_t, 2> { typedef uint2 T; };
+template <> struct VecOf<uint32_t, 1> { typedef uint32_t T; };
+template <> struct VecOf<uint64_t, 2> { typedef ulonglong2 T; };
+template <> struct VecOf<uint64_t, 1> { typedef unsigned long long T; };
+
+// A 256-thread CTA is a 16 x 16 grid of VW x VW micro-tiles; each thread owns
+// R micro-tiles stacked along B, so a tile is TA = 16*VW (along A, the input's
+// contiguous dim) by TB = 16*VW*R (along B, the output's contiguous dim).
+//   load : VW vector loads per micro-tile, lanes adjacent along A (coalesced);
+//   regs : VW x VW transpose in registers;
+//   smem : output-major rows of TB elements, 16-byte chunks XOR-swizzled by
+//          the row's micro-tile index (the bank-conflict fix of P:L123's
+//          L x (L+1) padding, without the padding);
+//   store: vector loads of whole chunks, lanes adjacent along B (coalesced).
+template <typename W, int VW, int R, typename I>
+__global__ void __launch_bounds__(256)
+tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in, W* __restrict__ out) {
+    typedef typename VecOf<W, VW>::T V;
+    constexpr int TA = 16 * VW;
+    constexpr int TB = 16 * VW * R;
+    constexpr int CPR = TB / VW;                 // vector chunks per smem row (power of two)
+    constexpr int CHUNKS = TA * CPR / 256;       // chunks each thread stores
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* const sm = reinterpret_cast<V*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int ta = tid & 15;                     // micro-tile column along A
+    const int tbg = tid >> 4;                    // micro-tile row group along B
+
+    const I nTiles = (I)p.nTiles;
+    I t = (I)blockIdx.x;
+    if (t >= nTiles) return;
+    const I stride = (I)gridDim.x;
+    const I sInB = (I)p.sInB;
+    const I sOutA = (I)p.sOutA;
+
+    W v[R][VW][VW];  // v[i][k][j]: element (a = ta*VW + j, b = (tbg + 16 i)*VW + k)
+    auto load = [&](const TileBase<I>& tb) {
+        const int limA = (tb.mask & (1u << 14)) ? p.splitTail[0] : TA;
+        const int limB = (tb.mask & (1u << 15)) ? p.splitTail[1] : TB;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int b0 = (tbg + 16 * i) * VW;
+            if (ta * VW < limA && b0 < limB) {
+#pragma unroll
+                for (int k = 0; k < VW; ++k) {
+                    const V x = __ldg(reinterpret_cast<const V*>(in + (tb.in + (I)(b0 + k) * sInB + ta * VW)));
+                    *reinterpret_cast<V*>(&v[i][k][0]) = x;
+                }
+            }
+        }
+    };
+
+    TileBase<I> cur = decode_tile<I>(p, t, lane);
+    load(cur);
+    int buf = 0;
+    for (; t < nTiles; t += stride) {
+        V* const sb = sm + buf * (TA * CPR);
+        // register transpose + swizzled staging: output row a = ta*VW + j
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int j = 0; j < VW; ++j) {
+                W w[VW];
+#pragma unroll
+                for (int k = 0; k < VW; ++k) w[k] = v[i][k][j];
+                const int a = ta * VW + j;
+                const int c = (tbg + 16 * i) ^ (ta & (CPR - 1));
+                sb[a * CPR + c] = *reinterpret_cast<const V*>(w);
+            }
+        }
+        __syncthreads();
+        const TileBase<I> now = cur;
+        const I tn = t + stride;
+        if (tn < nTiles) {
+            cur = decode_tile<I>(p, tn, lane);
+            load(cur);
+        }
+        const int limA = (now.mask & (1u << 14)) ? p.splitTail[0] : TA;
+        const int limB = (now.mask & (1u << 15)) ? p.splitTail[1] : TB;
+#pragma unroll
+        for (int u = 0; u < CHUNKS; ++u) {
+            const int q = tid + 256 * u;
+            const int a = q / CPR;
+            const int c = q % CPR;
+            if (a < limA && c * VW < limB) {
+                const V x = sb[a * CPR + (c ^ ((a / VW) & (CPR - 1)))];
+                *reinterpret_cast<V*>(out + (now.out + (I)a * sOutA + c * VW)) = x;
+            }
+        }
+        buf ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 template <typename W, int NREG, typename I>
@@ -217,9 +316,23 @@ static const void* pick_tile(int esize, int nreg, bool idx64) {
 #undef TT_PICK
 }
 
+static const void* pick_tiled2d(int esize, int vec, bool idx64) {
+    if (esize == 4) {
+        if (vec == 4) return idx64 ? (const void*)&tiled2d_kernel<uint32_t, 4, 1, int64_t>
+                                   : (const void*)&tiled2d_kernel<uint32_t, 4, 1, int32_t>;
+        if (vec == 2) return idx64 ? (const void*)&tiled2d_kernel<uint32_t, 2, 2, int64_t>
+                                   : (const void*)&tiled2d_kernel<uint32_t, 2, 2, int32_t>;
+    } else if (vec == 2) {
+        return idx64 ? (const void*)&tiled2d_kernel<uint64_t, 2, 1, int64_t>
+                     : (const void*)&tiled2d_kernel<uint64_t, 2, 1, int32_t>;
+    }
+    return nullptr;
+}
+
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
-    if (q.kernel != TT_KERNEL_TILE) return 0;
-    const void* fn = pick_tile(q.esize, q.nreg, q.idx64);
+    const void* fn = q.kernel == TT_KERNEL_TILE      ? pick_tile(q.esize, q.nreg, q.idx64)
+                     : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.idx64)
+                                                     : nullptr;
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dev.max_smem_per_block) != cudaSuccess) {
@@ -249,16 +362,26 @@ int launch_plan(const Plan& plan, const void* in, void* out, void* stream_) {
                 static_cast<const uint64_t*>(in), static_cast<uint64_t*>(out), n, vec16);
         return (int)cudaGetLastError();
     }
-    if (kc.kernel == TT_KERNEL_TILE) {
-        const void* fn = pick_tile(E, kc.nreg, kc.idx64);
+    if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
+        bool t2 = kc.kernel == TT_KERNEL_TILED2D;
+        int threads = kc.threads, grid = kc.grid, smem = kc.smem;
+        if (t2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
+                   (uintptr_t)(kc.vec * E - 1)) != 0) {
+            // pointers not aligned to the vector width: generic tile fallback
+            t2 = false;
+            threads = kc.fb_threads;
+            grid = kc.fb_grid;
+            smem = kc.fb_smem;
+        }
+        const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.idx64) : pick_tile(E, kc.nreg, kc.idx64);
         if (!fn) return (int)cudaErrorInvalidConfiguration;
-        if (kc.smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kc.smem);
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return (int)e;
         }
-        const TileParams* pp = &plan.tile;
-        void* args[] = {(void*)pp, (void*)&in, (void*)&out};
-        return (int)cudaLaunchKernel(fn, dim3(kc.grid), dim3(kc.threads), args, kc.smem, stream);
+        const void* pp = t2 ? (const void*)&plan.t2d : (const void*)&plan.tile;
+        void* args[] = {const_cast<void*>(pp), (void*)&in, (void*)&out};
+        return (int)cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
     }
     return (int)cudaErrorInvalidConfiguration;
 }

@@ -435,6 +435,53 @@ static void choose_smem(TileParams& tp, int esize) {
     tp.sbuf = (int32_t)((words + 3) / 4 * 4);
 }
 
+// Vectorised 2-D tiled kernel (TT_KERNEL_TILED2D): A = input dim 0, B = p[0].
+// Returns false if the problem is not of that class or the vector width
+// would be 1.  TA = 16*VW, TB = 16*VW*R with (VW, R) = (4,1) | (2,2) for 4-byte
+// and (2,1) for 8-byte words (kernels.cu instantiations).
+static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta, int& tb,
+                          double& fill) {
+    if (pr.n < 2 || pr.p[0] == 0) return false;
+    const int B = pr.p[0];
+    const int64_t dA = pr.d[0], dB = pr.d[B];
+    int R = 1;
+    vec = 0;
+    if (pr.esize == 4) {
+        if (dA % 4 == 0 && dB % 4 == 0) { vec = 4; R = 1; }
+        else if (dA % 2 == 0 && dB % 2 == 0) { vec = 2; R = 2; }
+    } else if (dA % 2 == 0 && dB % 2 == 0) {
+        vec = 2; R = 1;
+    }
+    if (vec == 0) return false;
+    ta = 16 * vec;
+    tb = 16 * vec * R;
+    std::memset(&t, 0, sizeof(t));
+    t.nSplit = 2;
+    t.splitLane[0] = 0;
+    t.splitLane[1] = 1;
+    t.splitChunk[0] = ta;
+    t.splitChunk[1] = tb;
+    const int64_t nA = ceil_div(dA, ta), nB = ceil_div(dB, tb);
+    t.splitTail[0] = (int32_t)(dA - (nA - 1) * ta);
+    t.splitTail[1] = (int32_t)(dB - (nB - 1) * tb);
+    t.sInB = pr.sin[B];
+    t.sOutA = pr.sout[0];
+    int g = 0;
+    int64_t acc = 1;
+    auto add = [&](int64_t ext, int64_t sIn, int64_t sOut) {
+        t.gC[g] = acc; t.gD[g] = ext; t.gSin[g] = sIn; t.gSout[g] = sOut;
+        acc *= ext; ++g;
+    };
+    add(nA, (int64_t)ta * pr.sin[0], (int64_t)ta * pr.sout[0]);
+    add(nB, (int64_t)tb * pr.sin[B], (int64_t)tb * pr.sout[B]);
+    for (int i = 1; i < pr.n; ++i)
+        if (i != B) add(pr.d[i], pr.sin[i], pr.sout[i]);
+    t.h = g;
+    t.nTiles = acc;
+    fill = (double)pr.vol / ((double)acc * ta * tb);
+    return true;
+}
+
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     int regs = 40 + q.nreg * (q.esize == 8 ? 6 : 5) + (q.idx64 ? q.nreg * 2 : 0);
     regs = (regs + 7) / 8 * 8;
@@ -469,7 +516,12 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         return TT_SUCCESS;
     }
     if (forced == TT_KERNEL_COPY) return TT_UNSUPPORTED;
-    if (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE) return TT_UNSUPPORTED;
+    if (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE && forced != TT_KERNEL_TILED2D)
+        return TT_UNSUPPORTED;
+    int vec2d = 0, ta2d = 0, tb2d = 0;
+    double fill2d = 0;
+    const bool can2d = build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d);
+    if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
     const int Vmax = (E == 4) ? 8192 : 4096;
@@ -509,6 +561,33 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
     kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
+    // the generic tile stays in the plan as the fallback for pointers that
+    // are not aligned to the 2-D kernel's vector width
+    kc.fb_threads = kc.threads;
+    kc.fb_grid = kc.grid;
+    kc.fb_smem = kc.smem;
+
+    // Vectorised 2-D tiled kernel when the tiles are mostly full: it moves
+    // VW elements per instruction on both sides (model: its issue cost is a
+    // fraction of the generic kernel's, DRAM sectors are whole).
+    const bool want2d = forced == TT_KERNEL_TILED2D ||
+                        (forced == TT_KERNEL_AUTO && can2d && fill2d >= 0.6 &&
+                         !(opts && (opts->run_in || opts->run_out)));
+    if (want2d) {
+        kc.kernel = TT_KERNEL_TILED2D;
+        kc.vec = vec2d;
+        kc.tile0 = ta2d;
+        kc.tile1 = tb2d;
+        kc.threads = 256;
+        kc.smem = 2 * ta2d * tb2d * E;
+        OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64};
+        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q2, dev) : 0);
+        if (per2 <= 0) per2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
+        const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
+        kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;
+        kc.model_dram_eff = 1.0;
+    }
     return TT_SUCCESS;
 }
 
@@ -551,7 +630,24 @@ std::string describe_json(const Plan& plan) {
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
       << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
       << ",\"model_dram_eff\":" << kc.model_dram_eff;
-    if (kc.kernel == TT_KERNEL_TILE) {
+    if (kc.kernel == TT_KERNEL_TILED2D) {
+        const Tiled2DParams& t = plan.t2d;
+        o << ",\"tiled2d\":{\"TA\":" << kc.tile0 << ",\"TB\":" << kc.tile1 << ",\"nTiles\":"
+          << (long long)t.nTiles << ",\"tails\":";
+        arr(o, t.splitTail, 2);
+        o << ",\"sInB\":" << (long long)t.sInB << ",\"sOutA\":" << (long long)t.sOutA
+          << ",\"grid_c\":";
+        arr(o, t.gC, t.h);
+        o << ",\"grid_d\":";
+        arr(o, t.gD, t.h);
+        o << ",\"grid_sin\":";
+        arr(o, t.gSin, t.h);
+        o << ",\"grid_sout\":";
+        arr(o, t.gSout, t.h);
+        o << "},\"fallback\":{\"kernel\":\"tile\",\"threads\":" << kc.fb_threads
+          << ",\"grid\":" << kc.fb_grid << ",\"smem\":" << kc.fb_smem << ",\"nreg\":" << kc.nreg << "}";
+    }
+    if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
         const TileParams& t = plan.tile;
         o << ",\"tile\":{\"V\":" << t.V << ",\"sbuf\":" << t.sbuf << ",\"nTiles\":"
           << (long long)t.nTiles << ",\"padEvery\":" << t.padEvery << ",\"pad\":" << t.pad

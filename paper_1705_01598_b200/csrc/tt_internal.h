@@ -81,16 +81,24 @@ struct RowParams {
     int64_t rSout[kMaxDims];  // output stride
 };
 
-// Two-dimensional tiled transpose of the fused problem's dims (0, p0) with
-// all other dims as a batch (Tiled class), 128-bit accesses.
+// Two-dimensional vectorised tiled transpose (Tiled class): the
+// fused problem's input dim A = 0 (stride 1) and the output-fastest input
+// dim B = perm[0] form TA x TB tiles; every other dim is a batch dim.  Each
+// thread moves VW x VW micro-tiles with VW-element vector accesses on both
+// sides (register transpose + XOR-swizzled shared memory), which needs
+// d[A] % VW == 0, d[B] % VW == 0 and VW*E-aligned pointers.  The grid
+// fields mirror TileParams (lane 0 = chunk index along A, lane 1 along B,
+// then batch dims), decoded by the same Algorithm-1 routine.
 struct Tiled2DParams {
-    int64_t d0, d1;           // input dim 0 (stride 1) and output-fastest input dim p0
-    int64_t sIn1;             // input stride of dim p0
-    int64_t sOut0;            // output stride of dim 0
-    int64_t tiles0, tiles1;   // tiles along d0, d1
-    int64_t nTiles;           // tiles0 * tiles1 * batch
-    int32_t h;                // batch dims
-    int64_t bC[kMaxDims], bD[kMaxDims], bSin[kMaxDims], bSout[kMaxDims];
+    int64_t nTiles;
+    int32_t h;
+    int32_t nSplit;          // always 2 (A and B)
+    int32_t splitLane[2];    // 0, 1
+    int32_t splitChunk[2];   // TA, TB
+    int32_t splitTail[2];    // valid extent of the last chunk along A / B
+    int64_t sInB;            // input stride of dim B (elements)
+    int64_t sOutA;           // output stride of dim A (elements)
+    int64_t gC[kMaxDims], gD[kMaxDims], gSin[kMaxDims], gSout[kMaxDims];
 };
 
 struct KernelChoice {
@@ -102,6 +110,7 @@ struct KernelChoice {
     int smem = 0;                  // dynamic shared memory bytes
     bool idx64 = false;
     int tile0 = 0, tile1 = 0;      // TILED2D tile
+    int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
 };
@@ -147,6 +156,19 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
                         OccupancyFn occ);
 std::string describe_json(const Plan& plan);
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev);
+
+// api.cu --------------------------------------------------------------------
+Plan* as_plan(tt_plan_t h);
+tt_status_t query_device(DeviceInfo& dev);
+tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
+                        size_t elem_size, void* stream, const DeviceInfo& dev,
+                        const tt_plan_options_t* opts, OccupancyFn occ);
+void destroy_plan(Plan* p);
+
+// dist.cu -------------------------------------------------------------------
+void destroy_shard(ShardInfo* s);
+int shard_launches(const ShardInfo* s);
+std::string describe_shard_json(const Plan& plan);
 
 // kernels.cu ----------------------------------------------------------------
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev);

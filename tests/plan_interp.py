@@ -1,0 +1,101 @@
+"""Host replay of libtt's kernel index arithmetic from a plan's JSON
+description (tt_plan_describe), used by the CPU tests to check the planner's
+geometry against the oracle without a GPU.  Test infrastructure only."""
+import numpy as np
+
+
+def interpret_tile_plan(j, words):
+    """Replay the tile kernel's index arithmetic (kernels.cu) for plan JSON j:
+    Algorithm-1 decode of the tile base, Eq. (4) input-order minor offsets,
+    staging positions, Eq. (5)/(6) output-order offsets, ragged-chunk masks."""
+    t = j["tile"]
+    V, a = t["V"], len(t["ext"])
+    ext, cin, order = t["ext"], t["cin"], t["out_order"]
+    sin, sout = t["sin"], t["sout"]
+    pe, pad = t["padEvery"], t["pad"]
+    st, sl, sc, se = t["split_tile"], t["split_lane"], t["split_chunk"], t["split_ext"]
+    tails = [se[s] - (-(-se[s] // sc[s]) - 1) * sc[s] for s in range(len(st))]
+    gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
+    vol = int(np.prod(j["dims"]))
+    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
+    written = np.zeros(vol, dtype=np.int64)
+    # per-slot tables
+    gin, pin, cin_s = [], [], []
+    for k in range(V):
+        rem, off, cs = k, 0, [0, 0]
+        for i in range(a):
+            c = rem % ext[i]
+            rem //= ext[i]
+            off += c * sin[i]
+            for s in range(len(st)):
+                if st[s] == i:
+                    cs[s] = c
+        gin.append(off)
+        pin.append(k + (k // pe) * pad)
+        cin_s.append(cs)
+    assert len(set(pin)) == V and max(pin) < t["sbuf"]
+    gout, psh, cout_s = [], [], []
+    for k in range(V):
+        rem, off, sh, cs = k, 0, 0, [0, 0]
+        for ti in order:
+            c = rem % ext[ti]
+            rem //= ext[ti]
+            off += c * sout[ti]
+            sh += c * cin[ti]
+            for s in range(len(st)):
+                if st[s] == ti:
+                    cs[s] = c
+        gout.append(off)
+        psh.append(sh + (sh // pe) * pad)
+        cout_s.append(cs)
+    for tile in range(t["nTiles"]):
+        q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
+        ib = sum(q[g] * gSi[g] for g in range(len(gC)))
+        ob = sum(q[g] * gSo[g] for g in range(len(gC)))
+        ragged = [q[sl[s]] == gD[sl[s]] - 1 for s in range(len(st))]
+        smem = {}
+        for k in range(V):
+            if all((not ragged[s]) or cin_s[k][s] < tails[s] for s in range(len(st))):
+                smem[pin[k]] = words[ib + gin[k]]
+        for k in range(V):
+            if all((not ragged[s]) or cout_s[k][s] < tails[s] for s in range(len(st))):
+                out[ob + gout[k]] = smem[psh[k]]
+                written[ob + gout[k]] += 1
+    assert (written == 1).all(), "tile decomposition must cover every output once"
+    return out
+
+
+def interpret_tiled2d_plan(j, words):
+    """Replay the 2-D kernel's tile geometry: grid decode (Algorithm 1),
+    ragged limits, and out[ob + a*sOutA + b] = in[ib + b*sInB + a]."""
+    t = j["tiled2d"]
+    TA, TB = t["TA"], t["TB"]
+    gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
+    vol = int(np.prod(j["dims"]))
+    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
+    written = np.zeros(vol, dtype=np.int64)
+    for tile in range(t["nTiles"]):
+        q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
+        ib = sum(q[g] * gSi[g] for g in range(len(gC)))
+        ob = sum(q[g] * gSo[g] for g in range(len(gC)))
+        limA = t["tails"][0] if q[0] == gD[0] - 1 else TA
+        limB = t["tails"][1] if q[1] == gD[1] - 1 else TB
+        a = np.arange(limA)[:, None]
+        b = np.arange(limB)[None, :]
+        dst = (ob + a * t["sOutA"] + b).ravel()
+        out[dst] = words[(ib + b * t["sInB"] + a).ravel()]
+        written[dst] += 1
+    assert (written == 1).all(), "2-D tiles must cover every output once"
+    return out
+
+
+
+def interpret_plan(j, words):
+    """Output of a (non-sharded) plan description applied to ``words``."""
+    if j["kernel"] == "copy":
+        return np.array(words, copy=True)
+    fj = dict(j)
+    fj["dims"] = j["fused"]["dims"]
+    if j["kernel"] == "tiled2d":
+        return interpret_tiled2d_plan(fj, words)
+    return interpret_tile_plan(fj, words)

@@ -118,6 +118,20 @@ def test_forced_tiles(run, esize):
         check(dims, perm, esize, run_in=run[0], run_out=run[1])
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+def test_forced_tiled2d(esize):
+    """The vectorised 2-D kernel on full, ragged and batched tiles."""
+    shapes = [((64, 64), (1, 0)), ((132, 36), (1, 0)), ((6, 10, 7), (1, 2, 0)),
+              ((34, 3, 98), (2, 1, 0)), ((8, 5, 12, 3), (2, 3, 0, 1)), ((70, 50), (1, 0)),
+              ((1000, 998), (1, 0)), ((36, 7, 44, 3), (2, 0, 3, 1)), ((2, 4, 6), (2, 0, 1))]
+    for dims, perm in shapes:
+        check(dims, perm, esize, kernel=tt.KERNEL_TILED2D)
+        # pointers misaligned for the vector width take the generic fallback
+        words = wl.random_words(int(np.prod(dims)), esize, 8)
+        got = run_gpu(dims, perm, words, offset=1, kernel=tt.KERNEL_TILED2D)
+        np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)

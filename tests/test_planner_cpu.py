@@ -13,6 +13,7 @@ import pytest
 import paper_1705_01598_b200 as tt
 from oracle import oracle as orc
 import tt_workloads as wl
+from plan_interp import interpret_tile_plan, interpret_tiled2d_plan, interpret_plan
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -80,68 +81,7 @@ def test_normalisation(dims, perm, fdims, fperm):
     j = tt.plan_offline(dims, perm, 4)
     assert tuple(j["fused"]["dims"]) == fdims
     assert tuple(j["fused"]["perm"]) == fperm
-    assert j["kernel"] == ("copy" if len(fdims) == 1 else "tile")
-
-
-def interpret_tile_plan(j, words):
-    """Replay the tile kernel's index arithmetic (kernels.cu) for plan JSON j:
-    Algorithm-1 decode of the tile base, Eq. (4) input-order minor offsets,
-    staging positions, Eq. (5)/(6) output-order offsets, ragged-chunk masks."""
-    t = j["tile"]
-    V, a = t["V"], len(t["ext"])
-    ext, cin, order = t["ext"], t["cin"], t["out_order"]
-    sin, sout = t["sin"], t["sout"]
-    pe, pad = t["padEvery"], t["pad"]
-    st, sl, sc, se = t["split_tile"], t["split_lane"], t["split_chunk"], t["split_ext"]
-    tails = [se[s] - (-(-se[s] // sc[s]) - 1) * sc[s] for s in range(len(st))]
-    gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
-    vol = int(np.prod(j["dims"]))
-    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
-    written = np.zeros(vol, dtype=np.int64)
-    # per-slot tables
-    gin, pin, cin_s = [], [], []
-    for k in range(V):
-        rem, off, cs = k, 0, [0, 0]
-        for i in range(a):
-            c = rem % ext[i]
-            rem //= ext[i]
-            off += c * sin[i]
-            for s in range(len(st)):
-                if st[s] == i:
-                    cs[s] = c
-        gin.append(off)
-        pin.append(k + (k // pe) * pad)
-        cin_s.append(cs)
-    assert len(set(pin)) == V and max(pin) < t["sbuf"]
-    gout, psh, cout_s = [], [], []
-    for k in range(V):
-        rem, off, sh, cs = k, 0, 0, [0, 0]
-        for ti in order:
-            c = rem % ext[ti]
-            rem //= ext[ti]
-            off += c * sout[ti]
-            sh += c * cin[ti]
-            for s in range(len(st)):
-                if st[s] == ti:
-                    cs[s] = c
-        gout.append(off)
-        psh.append(sh + (sh // pe) * pad)
-        cout_s.append(cs)
-    for tile in range(t["nTiles"]):
-        q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
-        ib = sum(q[g] * gSi[g] for g in range(len(gC)))
-        ob = sum(q[g] * gSo[g] for g in range(len(gC)))
-        ragged = [q[sl[s]] == gD[sl[s]] - 1 for s in range(len(st))]
-        smem = {}
-        for k in range(V):
-            if all((not ragged[s]) or cin_s[k][s] < tails[s] for s in range(len(st))):
-                smem[pin[k]] = words[ib + gin[k]]
-        for k in range(V):
-            if all((not ragged[s]) or cout_s[k][s] < tails[s] for s in range(len(st))):
-                out[ob + gout[k]] = smem[psh[k]]
-                written[ob + gout[k]] += 1
-    assert (written == 1).all(), "tile decomposition must cover every output once"
-    return out
+    assert j["kernel"] in (("copy",) if len(fdims) == 1 else ("tile", "tiled2d"))
 
 
 CASES = [
@@ -169,8 +109,32 @@ def test_plan_interpreter_matches_oracle(dims, perm, esize):
     # the interpreter works on the fused problem the plan describes
     fj = dict(j)
     fj["dims"] = j["fused"]["dims"]
-    got = interpret_tile_plan(fj, words)
+    got = interpret_tile_plan(fj, words)   # generic tile (also the 2-D kernel's fallback)
     np.testing.assert_array_equal(got, want)
+    if j["kernel"] == "tiled2d":
+        np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), want)
+
+
+@pytest.mark.parametrize("dims,perm,esize", [
+    ((64, 64), (1, 0), 4), ((132, 36), (1, 0), 4), ((6, 10, 7), (1, 2, 0), 4),
+    ((34, 3, 98), (2, 1, 0), 8), ((8, 5, 12, 3), (2, 3, 0, 1), 4), ((70, 50), (1, 0), 8),
+])
+def test_tiled2d_geometry(dims, perm, esize):
+    j = tt.plan_offline(dims, perm, esize, kernel=tt.KERNEL_TILED2D)
+    assert j["kernel"] == "tiled2d"
+    words = wl.random_words(int(np.prod(dims)), esize, 3)
+    fj = dict(j)
+    fj["dims"] = j["fused"]["dims"]
+    np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), orc.permute(dims, perm, words))
+
+
+def test_tiled2d_rejects_odd_or_unchanged():
+    with pytest.raises(tt.TTError):
+        tt.plan_offline((13, 64), (1, 0), 4, kernel=tt.KERNEL_TILED2D)
+    with pytest.raises(tt.TTError):
+        tt.plan_offline((64, 8, 8), (0, 2, 1), 4, kernel=tt.KERNEL_TILED2D)
+    with pytest.raises(tt.TTError):
+        tt.plan_offline((64, 63), (1, 0), 8, kernel=tt.KERNEL_TILED2D)
 
 
 @pytest.mark.parametrize("run", [(2, 2), (4, 16), (16, 4), (64, 64), (3, 5)])
@@ -204,8 +168,8 @@ def test_split_chunks_and_smem_bounds_on_suites():
 
 def test_s1_plan_shape():
     j = tt.plan_offline((16384, 16384), (1, 0), 4)
-    assert j["kernel"] == "tile"
-    t = j["tile"]
-    # both runs at least 128 bytes, bank-conflict-free staging
+    assert j["kernel"] == "tiled2d" and j["vec"] == 4
+    assert j["tiled2d"]["TA"] * 4 >= 128 and j["tiled2d"]["TB"] * 4 >= 128
+    t = j["tile"]  # fallback: both runs at least 128 bytes
     assert min(t["ext"]) * 4 >= 128
     assert j["grid"] >= 148
