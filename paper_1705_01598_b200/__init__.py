@@ -43,7 +43,7 @@ class TTError(RuntimeError):
 class PlanOptions(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int), ("run_in", ctypes.c_int), ("run_out", ctypes.c_int),
                 ("threads", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
-                ("no_fusion", ctypes.c_int)]
+                ("no_fusion", ctypes.c_int), ("grid_order", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -108,9 +108,10 @@ def _arrays(dims, perm):
     return len(dims), (ctypes.c_int64 * len(dims))(*dims), (ctypes.c_int * len(perm))(*perm)
 
 
-def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False):
+def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
+             grid_order=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
-                       1 if no_fusion else 0)
+                       1 if no_fusion else 0, int(grid_order))
 
 
 def _ptr(x) -> int:

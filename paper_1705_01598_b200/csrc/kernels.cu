@@ -202,22 +202,25 @@ template <> struct VecOf<uint32_t, 1> { typedef uint32_t T; };
 template <> struct VecOf<uint64_t, 2> { typedef ulonglong2 T; };
 template <> struct VecOf<uint64_t, 1> { typedef unsigned long long T; };
 
-// A 256-thread CTA is a 16 x 16 grid of VW x VW micro-tiles; each thread owns
-// R micro-tiles stacked along B, so a tile is TA = 16*VW (along A, the input's
-// contiguous dim) by TB = 16*VW*R (along B, the output's contiguous dim).
-//   load : VW vector loads per micro-tile, lanes adjacent along A (coalesced);
+// A 256-thread CTA is a 16 x 16 grid of threads; each thread owns MA x MB
+// micro-tiles of VW x VW elements (MA along A, MB along B), so a tile is
+// TA = 16*VW*MA (along A, the input's contiguous dim) by TB = 16*VW*MB (along
+// B, the output's contiguous dim).
+//   load : VW vector loads per micro-tile, lanes adjacent along A (coalesced,
+//          16 lanes x VW*E bytes contiguous per row and per ma);
 //   regs : VW x VW transpose in registers;
-//   smem : output-major rows of TB elements, 16-byte chunks XOR-swizzled by
-//          the row's micro-tile index (the bank-conflict fix of P:L123's
-//          L x (L+1) padding, without the padding);
-//   store: vector loads of whole chunks, lanes adjacent along B (coalesced).
-template <typename W, int VW, int R, typename I>
+//   smem : output-major rows of TB elements in VW-element chunks, chunk index
+//          XOR-swizzled by the row's micro-tile index (the bank-conflict fix of
+//          P:L123's L x (L+1) padding, without the padding);
+//   store: whole chunks, lanes adjacent along B (coalesced).
+// Double-buffered: the next tile's loads are in flight during the stores.
+template <typename W, int VW, int MA, int MB, typename I>
 __global__ void __launch_bounds__(256)
 tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in, W* __restrict__ out) {
     typedef typename VecOf<W, VW>::T V;
-    constexpr int TA = 16 * VW;
-    constexpr int TB = 16 * VW * R;
-    constexpr int CPR = TB / VW;                 // vector chunks per smem row (power of two)
+    constexpr int TA = 16 * VW * MA;
+    constexpr int TB = 16 * VW * MB;
+    constexpr int CPR = TB / VW;                 // chunks per smem row (power of two)
     constexpr int CHUNKS = TA * CPR / 256;       // chunks each thread stores
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V* const sm = reinterpret_cast<V*>(smem_raw);
@@ -233,18 +236,23 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
     const I sInB = (I)p.sInB;
     const I sOutA = (I)p.sOutA;
 
-    W v[R][VW][VW];  // v[i][k][j]: element (a = ta*VW + j, b = (tbg + 16 i)*VW + k)
+    // v[mb][ma][k][j]: element (a = (ta + 16 ma)*VW + j, b = (tbg + 16 mb)*VW + k)
+    W v[MB][MA][VW][VW];
     auto load = [&](const TileBase<I>& tb) {
         const int limA = (tb.mask & (1u << 14)) ? p.splitTail[0] : TA;
         const int limB = (tb.mask & (1u << 15)) ? p.splitTail[1] : TB;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int b0 = (tbg + 16 * i) * VW;
-            if (ta * VW < limA && b0 < limB) {
+        for (int mb = 0; mb < MB; ++mb) {
+            const int b0 = (tbg + 16 * mb) * VW;
 #pragma unroll
-                for (int k = 0; k < VW; ++k) {
-                    const V x = __ldg(reinterpret_cast<const V*>(in + (tb.in + (I)(b0 + k) * sInB + ta * VW)));
-                    *reinterpret_cast<V*>(&v[i][k][0]) = x;
+            for (int k = 0; k < VW; ++k) {
+#pragma unroll
+                for (int ma = 0; ma < MA; ++ma) {
+                    const int a0 = (ta + 16 * ma) * VW;
+                    if (a0 < limA && b0 < limB) {
+                        const V x = __ldg(reinterpret_cast<const V*>(in + (tb.in + (I)(b0 + k) * sInB + a0)));
+                        *reinterpret_cast<V*>(&v[mb][ma][k][0]) = x;
+                    }
                 }
             }
         }
@@ -255,17 +263,20 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
     int buf = 0;
     for (; t < nTiles; t += stride) {
         V* const sb = sm + buf * (TA * CPR);
-        // register transpose + swizzled staging: output row a = ta*VW + j
+        // register transpose + swizzled staging: output row a = (ta + 16 ma)*VW + j
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
+        for (int mb = 0; mb < MB; ++mb) {
 #pragma unroll
-            for (int j = 0; j < VW; ++j) {
-                W w[VW];
+            for (int ma = 0; ma < MA; ++ma) {
 #pragma unroll
-                for (int k = 0; k < VW; ++k) w[k] = v[i][k][j];
-                const int a = ta * VW + j;
-                const int c = (tbg + 16 * i) ^ (ta & (CPR - 1));
-                sb[a * CPR + c] = *reinterpret_cast<const V*>(w);
+                for (int j = 0; j < VW; ++j) {
+                    W w[VW];
+#pragma unroll
+                    for (int k = 0; k < VW; ++k) w[k] = v[mb][ma][k][j];
+                    const int a = (ta + 16 * ma) * VW + j;
+                    const int c = (tbg + 16 * mb) ^ ((ta + 16 * ma) & (CPR - 1));
+                    sb[a * CPR + c] = *reinterpret_cast<const V*>(w);
+                }
             }
         }
         __syncthreads();
@@ -316,22 +327,34 @@ static const void* pick_tile(int esize, int nreg, bool idx64) {
 #undef TT_PICK
 }
 
-static const void* pick_tiled2d(int esize, int vec, bool idx64) {
-    if (esize == 4) {
-        if (vec == 4) return idx64 ? (const void*)&tiled2d_kernel<uint32_t, 4, 1, int64_t>
-                                   : (const void*)&tiled2d_kernel<uint32_t, 4, 1, int32_t>;
-        if (vec == 2) return idx64 ? (const void*)&tiled2d_kernel<uint32_t, 2, 2, int64_t>
-                                   : (const void*)&tiled2d_kernel<uint32_t, 2, 2, int32_t>;
-    } else if (vec == 2) {
-        return idx64 ? (const void*)&tiled2d_kernel<uint64_t, 2, 1, int64_t>
-                     : (const void*)&tiled2d_kernel<uint64_t, 2, 1, int32_t>;
+// 2-D kernel instantiations: (word, VW, MA, MB).  Tile TA x TB = 16*VW*MA x 16*VW*MB.
+template <typename W, int VW, int MA, int MB>
+static const void* t2d_fn(bool idx64) {
+    return idx64 ? (const void*)&tiled2d_kernel<W, VW, MA, MB, int64_t>
+                 : (const void*)&tiled2d_kernel<W, VW, MA, MB, int32_t>;
+}
+
+static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) {
+    if (esize == 4 && vec == 4) {
+        if (ta == 64 && tb == 64) return t2d_fn<uint32_t, 4, 1, 1>(idx64);
+        if (ta == 128 && tb == 64) return t2d_fn<uint32_t, 4, 2, 1>(idx64);
+        if (ta == 64 && tb == 128) return t2d_fn<uint32_t, 4, 1, 2>(idx64);
+        if (ta == 128 && tb == 128) return t2d_fn<uint32_t, 4, 2, 2>(idx64);
+    } else if (esize == 4 && vec == 2) {
+        if (ta == 32 && tb == 64) return t2d_fn<uint32_t, 2, 1, 2>(idx64);
+        if (ta == 64 && tb == 64) return t2d_fn<uint32_t, 2, 2, 2>(idx64);
+    } else if (esize == 8 && vec == 2) {
+        if (ta == 32 && tb == 32) return t2d_fn<uint64_t, 2, 1, 1>(idx64);
+        if (ta == 64 && tb == 32) return t2d_fn<uint64_t, 2, 2, 1>(idx64);
+        if (ta == 32 && tb == 64) return t2d_fn<uint64_t, 2, 1, 2>(idx64);
+        if (ta == 64 && tb == 64) return t2d_fn<uint64_t, 2, 2, 2>(idx64);
     }
     return nullptr;
 }
 
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     const void* fn = q.kernel == TT_KERNEL_TILE      ? pick_tile(q.esize, q.nreg, q.idx64)
-                     : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.idx64)
+                     : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
                                                      : nullptr;
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -373,7 +396,8 @@ int launch_plan(const Plan& plan, const void* in, void* out, void* stream_) {
             grid = kc.fb_grid;
             smem = kc.fb_smem;
         }
-        const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.idx64) : pick_tile(E, kc.nreg, kc.idx64);
+        const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64)
+                            : pick_tile(E, kc.nreg, kc.idx64);
         if (!fn) return (int)cudaErrorInvalidConfiguration;
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -439,22 +439,38 @@ static void choose_smem(TileParams& tp, int esize) {
 // Returns false if the problem is not of that class or the vector width
 // would be 1.  TA = 16*VW, TB = 16*VW*R with (VW, R) = (4,1) | (2,2) for 4-byte
 // and (2,1) for 8-byte words (kernels.cu instantiations).
+// Instantiated tiles (kernels.cu pick_tiled2d): 4-byte VW=4: {64,128}^2;
+// 4-byte VW=2: 32x64, 64x64; 8-byte VW=2: {32,64}^2.
+static bool tiled2d_tile_ok(int esize, int vec, int ta, int tb) {
+    if (esize == 4 && vec == 4) return (ta == 64 || ta == 128) && (tb == 64 || tb == 128);
+    if (esize == 4 && vec == 2) return (ta == 32 || ta == 64) && tb == 64;
+    if (esize == 8 && vec == 2) return (ta == 32 || ta == 64) && (tb == 32 || tb == 64);
+    return false;
+}
+
 static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta, int& tb,
-                          double& fill) {
+                          double& fill, int wantA, int wantB, int order) {
     if (pr.n < 2 || pr.p[0] == 0) return false;
     const int B = pr.p[0];
     const int64_t dA = pr.d[0], dB = pr.d[B];
-    int R = 1;
     vec = 0;
     if (pr.esize == 4) {
-        if (dA % 4 == 0 && dB % 4 == 0) { vec = 4; R = 1; }
-        else if (dA % 2 == 0 && dB % 2 == 0) { vec = 2; R = 2; }
+        if (dA % 4 == 0 && dB % 4 == 0) vec = 4;
+        else if (dA % 2 == 0 && dB % 2 == 0) vec = 2;
     } else if (dA % 2 == 0 && dB % 2 == 0) {
-        vec = 2; R = 1;
+        vec = 2;
     }
     if (vec == 0) return false;
-    ta = 16 * vec;
-    tb = 16 * vec * R;
+    // default tiles from the B200 calibration sweep (tools/sweep.py t2d,
+    // profiles/round1_sweep_t2d.md): 64 x 128 for 4-byte words with 16-byte
+    // vectors, 64 x 64 otherwise; two CTAs per SM, B-chunks fastest.
+    if (pr.esize == 4) { ta = 64; tb = vec == 4 ? 128 : 64; }
+    else { ta = 64; tb = 64; }
+    if (wantA || wantB) {
+        if (wantA) ta = wantA;
+        if (wantB) tb = wantB;
+        if (!tiled2d_tile_ok(pr.esize, vec, ta, tb)) return false;
+    }
     std::memset(&t, 0, sizeof(t));
     t.nSplit = 2;
     t.splitLane[0] = 0;
@@ -472,8 +488,21 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
         t.gC[g] = acc; t.gD[g] = ext; t.gSin[g] = sIn; t.gSout[g] = sOut;
         acc *= ext; ++g;
     };
-    add(nA, (int64_t)ta * pr.sin[0], (int64_t)ta * pr.sout[0]);
-    add(nB, (int64_t)tb * pr.sin[B], (int64_t)tb * pr.sout[B]);
+    // Tile order: consecutive tiles run concurrently on neighbouring CTAs, so
+    // the fastest grid dim decides which side's DRAM rows are streamed whole.
+    // B-chunks fastest keeps whole OUTPUT rows in flight (writes are the
+    // costlier side on B200, calibration sweep); A-fastest the input rows.
+    if (order == 1) {
+        add(nA, (int64_t)ta * pr.sin[0], (int64_t)ta * pr.sout[0]);
+        add(nB, (int64_t)tb * pr.sin[B], (int64_t)tb * pr.sout[B]);
+        t.splitLane[0] = 0;
+        t.splitLane[1] = 1;
+    } else {
+        add(nB, (int64_t)tb * pr.sin[B], (int64_t)tb * pr.sout[B]);
+        add(nA, (int64_t)ta * pr.sin[0], (int64_t)ta * pr.sout[0]);
+        t.splitLane[0] = 1;
+        t.splitLane[1] = 0;
+    }
     for (int i = 1; i < pr.n; ++i)
         if (i != B) add(pr.d[i], pr.sin[i], pr.sout[i]);
     t.h = g;
@@ -520,7 +549,11 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         return TT_UNSUPPORTED;
     int vec2d = 0, ta2d = 0, tb2d = 0;
     double fill2d = 0;
-    const bool can2d = build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d);
+    const bool force2d = forced == TT_KERNEL_TILED2D;
+    const bool can2d = build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d,
+                                     force2d && opts ? opts->run_in : 0,
+                                     force2d && opts ? opts->run_out : 0,
+                                     opts && opts->grid_order ? opts->grid_order : 2);
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
@@ -541,7 +574,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     }
     if (!best.ok) {
         // fall back to the smallest legal tile
-        for (int64_t t = 2; t <= 64 && !best.ok; t *= 2) {
+        for (int64_t t = 64; t >= 2 && !best.ok; t /= 2) {
             TileCand c = build_tile(pr, t, t, 12288, dev, forceThreads);
             if (c.ok) best = c;
         }
@@ -557,7 +590,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.vec = 1;
     kc.predicted_us = best.cost_us;
     kc.model_dram_eff = best.dram_eff;
-    OccQuery q{TT_KERNEL_TILE, E, kc.nreg, 1, kc.threads, kc.smem, kc.idx64};
+    OccQuery q{TT_KERNEL_TILE, E, kc.nreg, 1, kc.threads, kc.smem, kc.idx64, 0, 0};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
     kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
@@ -580,9 +613,12 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.tile1 = tb2d;
         kc.threads = 256;
         kc.smem = 2 * ta2d * tb2d * E;
-        OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64};
-        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q2, dev) : 0);
-        if (per2 <= 0) per2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
+        OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64, ta2d, tb2d};
+        int occ2 = occ ? occ(q2, dev) : 0;
+        if (occ2 <= 0) occ2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
+        // two CTAs per SM measured best (fewer concurrent tiles, whole DRAM
+        // rows); never more than fit, so the persistent grid is one wave
+        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(2, occ2);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
         const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
         kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;
@@ -635,6 +671,8 @@ std::string describe_json(const Plan& plan) {
         o << ",\"tiled2d\":{\"TA\":" << kc.tile0 << ",\"TB\":" << kc.tile1 << ",\"nTiles\":"
           << (long long)t.nTiles << ",\"tails\":";
         arr(o, t.splitTail, 2);
+        o << ",\"lanes\":";
+        arr(o, t.splitLane, 2);
         o << ",\"sInB\":" << (long long)t.sInB << ",\"sOutA\":" << (long long)t.sOutA
           << ",\"grid_c\":";
         arr(o, t.gC, t.h);

@@ -129,6 +129,7 @@ struct DeviceInfo {
 struct OccQuery {
     int kernel, esize, nreg, vec, threads, smem;
     bool idx64;
+    int ta, tb;  // TILED2D tile
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 

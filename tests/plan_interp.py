@@ -78,8 +78,9 @@ def interpret_tiled2d_plan(j, words):
         q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
         ib = sum(q[g] * gSi[g] for g in range(len(gC)))
         ob = sum(q[g] * gSo[g] for g in range(len(gC)))
-        limA = t["tails"][0] if q[0] == gD[0] - 1 else TA
-        limB = t["tails"][1] if q[1] == gD[1] - 1 else TB
+        la, lb = t["lanes"]
+        limA = t["tails"][0] if q[la] == gD[la] - 1 else TA
+        limB = t["tails"][1] if q[lb] == gD[lb] - 1 else TB
         a = np.arange(limA)[:, None]
         b = np.arange(limB)[None, :]
         dst = (ob + a * t["sOutA"] + b).ravel()

@@ -124,8 +124,18 @@ def test_forced_tiled2d(esize):
     shapes = [((64, 64), (1, 0)), ((132, 36), (1, 0)), ((6, 10, 7), (1, 2, 0)),
               ((34, 3, 98), (2, 1, 0)), ((8, 5, 12, 3), (2, 3, 0, 1)), ((70, 50), (1, 0)),
               ((1000, 998), (1, 0)), ((36, 7, 44, 3), (2, 0, 3, 1)), ((2, 4, 6), (2, 0, 1))]
+    tiles = [(64, 64), (128, 64), (64, 128), (128, 128), (32, 64)] if esize == 4 else \
+        [(32, 32), (64, 32), (32, 64), (64, 64)]
     for dims, perm in shapes:
         check(dims, perm, esize, kernel=tt.KERNEL_TILED2D)
+        for order in (1, 2):
+            for ta, tb in tiles:
+                try:
+                    tt.Plan(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb)
+                except tt.TTError:
+                    continue  # tile not instantiated for this vector width
+                check(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb,
+                      grid_order=order)
         # pointers misaligned for the vector width take the generic fallback
         words = wl.random_words(int(np.prod(dims)), esize, 8)
         got = run_gpu(dims, perm, words, offset=1, kernel=tt.KERNEL_TILED2D)

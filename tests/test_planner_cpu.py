@@ -120,12 +120,22 @@ def test_plan_interpreter_matches_oracle(dims, perm, esize):
     ((34, 3, 98), (2, 1, 0), 8), ((8, 5, 12, 3), (2, 3, 0, 1), 4), ((70, 50), (1, 0), 8),
 ])
 def test_tiled2d_geometry(dims, perm, esize):
-    j = tt.plan_offline(dims, perm, esize, kernel=tt.KERNEL_TILED2D)
-    assert j["kernel"] == "tiled2d"
     words = wl.random_words(int(np.prod(dims)), esize, 3)
-    fj = dict(j)
-    fj["dims"] = j["fused"]["dims"]
-    np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), orc.permute(dims, perm, words))
+    want = orc.permute(dims, perm, words)
+    tiles = [(64, 64), (128, 64), (64, 128), (128, 128)] if esize == 4 else \
+        [(32, 32), (64, 32), (32, 64), (64, 64)]
+    for order in (0, 1, 2):
+        for ta, tb in tiles:
+            try:
+                j = tt.plan_offline(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta,
+                                    run_out=tb, grid_order=order)
+            except tt.TTError:
+                assert esize == 4 and 2 in {dims[0] % 4, dims[perm[0]] % 4}  # VW=2 tiles only
+                continue
+            assert j["kernel"] == "tiled2d"
+            fj = dict(j)
+            fj["dims"] = j["fused"]["dims"]
+            np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), want)
 
 
 def test_tiled2d_rejects_odd_or_unchanged():
