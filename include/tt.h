@@ -93,6 +93,7 @@ typedef struct {
     int ctas_per_sm;     /* persistent CTAs per SM (grid = num_sms * this)         */
     int no_fusion;       /* 1 = skip dimension fusion / extent-1 removal (debug)   */
     int grid_order;      /* TILED2D tile order: 1 = A-chunks fastest, 2 = B-chunks fastest */
+    int no_widen;        /* 1 = never regroup elements of an unchanged fastest dim into wider words */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

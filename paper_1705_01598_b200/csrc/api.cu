@@ -58,6 +58,27 @@ tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* pe
     p->perm.assign(perm, perm + rank);
     const bool fuse = !(opts && opts->no_fusion);
     p->prob = normalize(rank, dims, perm, (int)elem_size, fuse);
+    // element widening (planner.cpp widen_factor) unless geometry is forced
+    const bool forcedGeometry = opts && (opts->kernel || opts->run_in || opts->run_out ||
+                                         opts->threads || opts->no_widen);
+    const int k = forcedGeometry ? 1 : widen_factor(p->prob);
+    if (k > 1) {
+        Plan* nar = new (std::nothrow) Plan();
+        if (nar == nullptr) { delete p; return TT_INTERNAL_ERROR; }
+        nar->device = p->device;
+        nar->stream = p->stream;
+        nar->rank = rank;
+        nar->dims = p->dims;
+        nar->perm = p->perm;
+        nar->prob = p->prob;
+        if (choose_plan(*nar, dev, opts, occ) == TT_SUCCESS) {
+            p->narrow = nar;
+            p->widen = k;
+            p->prob = widen_problem(p->prob, k);
+        } else {
+            delete nar;
+        }
+    }
     st = choose_plan(*p, dev, opts, occ);
     if (st != TT_SUCCESS) {
         delete p;
@@ -66,6 +87,8 @@ tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* pe
     *out = p;
     return TT_SUCCESS;
 }
+
+Plan::~Plan() { delete narrow; }
 
 void destroy_plan(Plan* p) {
     if (p == nullptr) return;
@@ -141,7 +164,7 @@ static tt_status_t check_exec(Plan* p, const void* in, void* out) {
     if (p == nullptr) return TT_INVALID_PLAN;
     if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
     const uintptr_t mis = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
-                          (uintptr_t)(p->prob.esize - 1);
+                          (uintptr_t)(p->prob.esize / p->widen - 1);
     if (mis) return TT_INVALID_PARAMETER;
     if (p->device < 0) return TT_INVALID_DEVICE;
     int d = -1;

@@ -51,30 +51,85 @@ __global__ void __launch_bounds__(1024) copy_kernel(const W* __restrict__ in, W*
 }
 
 // ---------------------------------------------------------------------------
+// shared memory by 32-bit shared-window byte address (no generic->shared
+// conversions in the hot loop)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void sts(uint32_t a, uint64_t v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v));
+}
+__device__ __forceinline__ void sts(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+template <typename W> __device__ __forceinline__ W lds(uint32_t a);
+template <> __device__ __forceinline__ uint32_t lds<uint32_t>(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ uint64_t lds<uint64_t>(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ uint4 lds<uint4>(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 ldg_(const uint4* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ldg_(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint64_t ldg_(const uint64_t* p) {
+    return __ldg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+// Hide a per-tile base pointer from the optimiser so that `base + offset`
+// stays one IMAD.WIDE.U32 per access instead of a re-associated 64-bit add.
+template <typename T>
+__device__ __forceinline__ T* opaque(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+
+// ---------------------------------------------------------------------------
 // generic staged tile
 // ---------------------------------------------------------------------------
 template <typename I>
 struct TileBase {
     I in, out;
-    uint32_t mask;   // slot-word bits that must be set for a slot to be valid
+    uint32_t need;   // bit 0: ragged last chunk of split dim A, bit 1: of split dim B
 };
+
+// n / d for n < 2^31 with the planner's magic (m, l): (umulhi(n, m) + n) >> l.
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t l) {
+    return (__umulhi(n, m) + n) >> l;
+}
 
 // Algorithm 1: lane i < h evaluates the i-th term of Eqs. (2)
 // and (3) for the tile index b = t -- mod(floor(t / c_i), d_i) * stride_i --
 // and an XOR butterfly sums the terms; every lane ends with both bases.  The
 // same decode order serves both sums (reading R3).  A lane holding
 // a split dim also reports whether this tile is that dim's ragged last chunk
-// (PackedSplit edge), gathered with one ballot.
+// (PackedSplit edge), gathered with one ballot.  32-bit indices use
+// multiply-shift division with per-lane magic numbers from the planner.
 template <typename I, typename P>
 __device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
     I vin = 0, vout = 0;
     bool ragged = false;
     if (lane < p.h) {
-        const I d = (I)p.gD[lane];
-        const I q = (t / (I)p.gC[lane]) % d;
+        I q;
+        if constexpr (sizeof(I) == 4) {
+            const uint32_t q1 = fast_div((uint32_t)t, p.gMC[lane], p.gLC[lane]);
+            const uint32_t q2 = fast_div(q1, p.gMD[lane], p.gLD[lane]);
+            q = (I)(q1 - q2 * (uint32_t)p.gD[lane]);
+        } else {
+            q = (t / (I)p.gC[lane]) % (I)p.gD[lane];
+        }
         vin = q * (I)p.gSin[lane];
         vout = q * (I)p.gSout[lane];
-        ragged = (q == d - 1) &&
+        ragged = (q == (I)p.gD[lane] - 1) &&
                  ((p.nSplit > 0 && lane == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) ||
                   (p.nSplit > 1 && lane == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]));
     }
@@ -84,55 +139,60 @@ __device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
         vout += __shfl_xor_sync(0xffffffffu, vout, o);
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, ragged);
-    uint32_t m = 0;
-    if (p.nSplit > 0) m |= ((bal >> p.splitLane[0]) & 1u) << 14;
-    if (p.nSplit > 1) m |= ((bal >> p.splitLane[1]) & 1u) << 15;
+    uint32_t need = 0;
+    if (p.nSplit > 0) need |= (bal >> p.splitLane[0]) & 1u;
+    if (p.nSplit > 1) need |= ((bal >> p.splitLane[1]) & 1u) << 1;
     TileBase<I> b;
     b.in = vin;
     b.out = vout;
-    b.mask = m;
+    b.need = need;
     return b;
 }
 
-// Slot word (one register per slot): bits 0-13 staging position of the load
-// element, bit 14/15 "load element lies inside the ragged last chunk of split
-// dim A/B", bits 16-29 staging position of the store element, bits 30/31 the
-// same flags for it.  A slot is valid in a tile iff (word & mask) == mask.
+// Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
+// (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
+// store element (Eq. 6 through the padded layout).  `flags` holds 4 bits per
+// slot: (load elem inside ragged A-chunk, ... B-chunk, store elem inside
+// ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
+// cover the tile's `need`.
 template <typename W, int NREG, typename I>
-__global__ void __launch_bounds__(512, (sizeof(I) == 8 ? 1 : 2))
+__global__ void __launch_bounds__(NREG >= 8 ? 256 : 512, (NREG >= 8 ? (sizeof(W) >= 8 ? 2 : 3) : (sizeof(I) == 8 ? 1 : 2)))
 tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    W* const sm = reinterpret_cast<W*>(smem_raw);
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
     const int tid = threadIdx.x;
     const int NT = blockDim.x;
     const int lane = tid & 31;
 
     // Per-thread loop-invariant minor positions (Eqs. 4-6; the
-    // register arrays of P:L155-159): slot r handles tile element k = tid + r*NT
-    // in input order (load) and k' = k in output order (store).
+    // register arrays of P:L155-159).
     I gin[NREG], gout[NREG];
-    uint32_t slot[NREG];
+    uint32_t sin_[NREG], sout[NREG];
+    uint32_t flags = 0;
     const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    const bool allSlots = p.V == NT * NREG;  // CTA-uniform
 #pragma unroll
     for (int r = 0; r < NREG; ++r) {
         gin[r] = 0;
         gout[r] = 0;
-        slot[r] = 0;
+        sin_[r] = 0;
+        sout[r] = 0;
         if (r < nmine) {
             const int k = tid + r * NT;
+            uint32_t f = 0;
             // Eq. (4): pMinorIn(k), tile-input order
             int rem = k;
             I off = 0;
-            uint32_t w = 0;
             for (int i = 0; i < p.a; ++i) {
                 const int c = rem % p.tExt[i];
                 rem /= p.tExt[i];
                 off += (I)c * (I)p.tSin[i];
-                if (p.nSplit > 0 && i == p.splitTile[0] && c < p.splitTail[0]) w |= 1u << 14;
-                if (p.nSplit > 1 && i == p.splitTile[1] && c < p.splitTail[1]) w |= 1u << 15;
+                if (p.nSplit > 0 && i == p.splitTile[0] && c < p.splitTail[0]) f |= 1u;
+                if (p.nSplit > 1 && i == p.splitTile[1] && c < p.splitTail[1]) f |= 2u;
             }
             gin[r] = off;
-            w |= (uint32_t)(k + (k / p.padEvery) * p.pad);
+            sin_[r] = (uint32_t)(k + (k / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
             // Eqs. (5), (6): pMinorOut(k') and pSh(k'), tile-output order
             rem = k;
             off = 0;
@@ -143,12 +203,12 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 rem /= p.tExt[t];
                 off += (I)c * (I)p.tSout[t];
                 sh += c * p.tCin[t];
-                if (p.nSplit > 0 && t == p.splitTile[0] && c < p.splitTail[0]) w |= 1u << 30;
-                if (p.nSplit > 1 && t == p.splitTile[1] && c < p.splitTail[1]) w |= 1u << 31;
+                if (p.nSplit > 0 && t == p.splitTile[0] && c < p.splitTail[0]) f |= 4u;
+                if (p.nSplit > 1 && t == p.splitTile[1] && c < p.splitTail[1]) f |= 8u;
             }
             gout[r] = off;
-            w |= (uint32_t)(sh + (sh / p.padEvery) * p.pad) << 16;
-            slot[r] = w;
+            sout[r] = (uint32_t)(sh + (sh / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
+            flags |= f << (4 * r);
         }
     }
 
@@ -158,37 +218,118 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     const I stride = (I)gridDim.x;
 
     W v[NREG];
+    auto load = [&](const TileBase<I>& tb) {
+        const W* __restrict__ src = opaque(in + tb.in);
+        if (tb.need == 0 && allSlots) {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r) v[r] = ldg_(src + gin[r]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(src + gin[r]);
+        }
+    };
     TileBase<I> cur = decode_tile<I>(p, t, lane);
-#pragma unroll
-    for (int r = 0; r < NREG; ++r)
-        if (r < nmine && (slot[r] & cur.mask) == cur.mask) v[r] = __ldg(in + (cur.in + gin[r]));
+    load(cur);
 
-    int buf = 0;
+    uint32_t sb = sm0;
     for (; t < nTiles; t += stride) {
-        W* const sb = sm + buf * p.sbuf;
         // stage the tile in input order
+        if (allSlots) {
 #pragma unroll
-        for (int r = 0; r < NREG; ++r)
-            if (r < nmine) sb[slot[r] & 0x3fffu] = v[r];
+            for (int r = 0; r < NREG; ++r) sts(sb + sin_[r], v[r]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine) sts(sb + sin_[r], v[r]);
+        }
         __syncthreads();
         // issue the next tile's global loads before writing this one
-        const I outBase = cur.out;
-        const uint32_t omask = cur.mask << 16;
+        const TileBase<I> now = cur;
         const I tn = t + stride;
         if (tn < nTiles) {
             cur = decode_tile<I>(p, tn, lane);
-#pragma unroll
-            for (int r = 0; r < NREG; ++r)
-                if (r < nmine && (slot[r] & cur.mask) == cur.mask) v[r] = __ldg(in + (cur.in + gin[r]));
+            load(cur);
         }
         // transposed read of shared memory (Eq. 6), coalesced writes (Eq. 5)
+        W* __restrict__ dst = opaque(out + now.out);
+        if (now.need == 0 && allSlots) {
 #pragma unroll
-        for (int r = 0; r < NREG; ++r)
-            if (r < nmine && (slot[r] & omask) == omask)
-                out[outBase + gout[r]] = sb[(slot[r] >> 16) & 0x3fffu];
-        buf ^= 1;
+            for (int r = 0; r < NREG; ++r) dst[gout[r]] = lds<W>(sb + sout[r]);
+        } else {
+            const uint32_t needOut = now.need << 2;
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
+                    dst[gout[r]] = lds<W>(sb + sout[r]);
+        }
         // Two buffers: the next iteration writes the other buffer, whose
         // readers (previous tile) all passed this iteration's barrier.
+        sb = (sb == sm0) ? sm0 + sbytes : sm0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// row copy: fastest dim unchanged with long rows (TiledCopy class, P:L141:
+// "no need for shared memory buffer since no transpose takes place")
+// ---------------------------------------------------------------------------
+template <typename I>
+__device__ __forceinline__ I warp_sum(I v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Output row r (r over output dims 1..n-1 in output order) is out[r*L, r*L+L)
+// and the contiguous input row at base(r) = sum_j x_j * S_in_j.  Each warp
+// copies a contiguous range of rows: the first base is decoded with
+// Algorithm 1 (lane j holds digit x_j), the next ones by a lane-parallel
+// odometer step (ballot finds the first digit that does not wrap).
+template <typename W, typename I>
+__global__ void __launch_bounds__(256)
+rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W* __restrict__ out) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const I nWarps = (I)(((uint64_t)gridDim.x * blockDim.x) >> 5);
+    const I warp = (I)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const I nRows = (I)p.nRows;
+    const I per = (nRows + nWarps - 1) / nWarps;
+    const I r0 = warp * per;
+    if (r0 >= nRows) return;
+    const I r1 = min(r0 + per, nRows);
+    const I L = (I)p.row;
+
+    I x = 0, d = 1, s = 0;
+    if (lane < p.h) {
+        d = (I)p.rD[lane];
+        s = (I)p.rSin[lane];
+        if constexpr (sizeof(I) == 4) {
+            const uint32_t q1 = fast_div((uint32_t)r0, p.gMC[lane], p.gLC[lane]);
+            x = (I)(q1 - fast_div(q1, p.gMD[lane], p.gLD[lane]) * (uint32_t)d);
+        } else {
+            x = (r0 / (I)p.rC[lane]) % d;
+        }
+    }
+    I base = warp_sum<I>(x * s);
+    for (I r = r0; r < r1; ++r) {
+        const W* __restrict__ src = opaque(in + base);
+        W* __restrict__ dst = opaque(out + r * L);
+        for (I c = lane; c < L; c += 32 * U) {
+            W t[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c + 32 * u < L) t[u] = ldg_(src + c + 32 * u);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c + 32 * u < L) dst[c + 32 * u] = t[u];
+        }
+        // odometer step to row r+1
+        const uint32_t wraps = __ballot_sync(0xffffffffu, lane < p.h && x == d - 1);
+        const int f = __ffs(~wraps) - 1;
+        I delta = 0;
+        if (lane < f) { delta = (I)0 - (d - 1) * s; x = 0; }
+        else if (lane == f) { delta = s; x += 1; }
+        base += warp_sum<I>(delta);
     }
 }
 
@@ -239,8 +380,8 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
     // v[mb][ma][k][j]: element (a = (ta + 16 ma)*VW + j, b = (tbg + 16 mb)*VW + k)
     W v[MB][MA][VW][VW];
     auto load = [&](const TileBase<I>& tb) {
-        const int limA = (tb.mask & (1u << 14)) ? p.splitTail[0] : TA;
-        const int limB = (tb.mask & (1u << 15)) ? p.splitTail[1] : TB;
+        const int limA = (tb.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (tb.need & 2u) ? p.splitTail[1] : TB;
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
             const int b0 = (tbg + 16 * mb) * VW;
@@ -286,8 +427,8 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
             cur = decode_tile<I>(p, tn, lane);
             load(cur);
         }
-        const int limA = (now.mask & (1u << 14)) ? p.splitTail[0] : TA;
-        const int limB = (now.mask & (1u << 15)) ? p.splitTail[1] : TB;
+        const int limA = (now.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (now.need & 2u) ? p.splitTail[1] : TB;
 #pragma unroll
         for (int u = 0; u < CHUNKS; ++u) {
             const int q = tid + 256 * u;
@@ -320,18 +461,38 @@ static const void* pick_tile(int esize, int nreg, bool idx64) {
         default: return nullptr;                    \
     }
     if (esize == 4) {
-        if (idx64) { TT_PICK(uint32_t, int64_t) } else { TT_PICK(uint32_t, int32_t) }
-    } else {
-        if (idx64) { TT_PICK(uint64_t, int64_t) } else { TT_PICK(uint64_t, int32_t) }
+        if (idx64) { TT_PICK(uint32_t, int64_t) } else { TT_PICK(uint32_t, uint32_t) }
+    } else if (esize == 8) {
+        if (idx64) { TT_PICK(uint64_t, int64_t) } else { TT_PICK(uint64_t, uint32_t) }
+    } else if (esize == 16) {  // widened words: at most 4 slots (register budget)
+        switch (nreg) {
+            case 1: return idx64 ? tile_fn<uint4, 1, int64_t>() : tile_fn<uint4, 1, uint32_t>();
+            case 2: return idx64 ? tile_fn<uint4, 2, int64_t>() : tile_fn<uint4, 2, uint32_t>();
+            case 4: return idx64 ? tile_fn<uint4, 4, int64_t>() : tile_fn<uint4, 4, uint32_t>();
+            default: return nullptr;
+        }
     }
+    return nullptr;
 #undef TT_PICK
+}
+
+static const void* pick_rowcopy(int esize, bool idx64) {
+    switch (esize) {
+        case 4: return idx64 ? (const void*)&rowcopy_kernel<uint32_t, int64_t>
+                             : (const void*)&rowcopy_kernel<uint32_t, uint32_t>;
+        case 8: return idx64 ? (const void*)&rowcopy_kernel<uint64_t, int64_t>
+                             : (const void*)&rowcopy_kernel<uint64_t, uint32_t>;
+        case 16: return idx64 ? (const void*)&rowcopy_kernel<uint4, int64_t>
+                              : (const void*)&rowcopy_kernel<uint4, uint32_t>;
+        default: return nullptr;
+    }
 }
 
 // 2-D kernel instantiations: (word, VW, MA, MB).  Tile TA x TB = 16*VW*MA x 16*VW*MB.
 template <typename W, int VW, int MA, int MB>
 static const void* t2d_fn(bool idx64) {
     return idx64 ? (const void*)&tiled2d_kernel<W, VW, MA, MB, int64_t>
-                 : (const void*)&tiled2d_kernel<W, VW, MA, MB, int32_t>;
+                 : (const void*)&tiled2d_kernel<W, VW, MA, MB, uint32_t>;
 }
 
 static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) {
@@ -355,6 +516,7 @@ static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) 
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     const void* fn = q.kernel == TT_KERNEL_TILE      ? pick_tile(q.esize, q.nreg, q.idx64)
                      : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
+                     : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -370,20 +532,28 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     return blocks;
 }
 
-int launch_plan(const Plan& plan, const void* in, void* out, void* stream_) {
+int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    // widened words need E*widen-aligned pointers; otherwise run the narrow plan
+    const Plan& plan = (plan0.widen > 1 && plan0.narrow &&
+                        ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
+                         (uintptr_t)(plan0.prob.esize - 1)) != 0)
+                           ? *plan0.narrow
+                           : plan0;
     const KernelChoice& kc = plan.kc;
     const int E = plan.prob.esize;
     if (kc.kernel == TT_KERNEL_COPY) {
-        const int64_t n = plan.prob.vol;
         const int vec16 = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
-        if (E == 4)
-            copy_kernel<uint32_t><<<kc.grid, kc.threads, 0, stream>>>(
-                static_cast<const uint32_t*>(in), static_cast<uint32_t*>(out), n, vec16);
-        else
-            copy_kernel<uint64_t><<<kc.grid, kc.threads, 0, stream>>>(
-                static_cast<const uint64_t*>(in), static_cast<uint64_t*>(out), n, vec16);
+        const int64_t n = plan.prob.vol * (E / 4);  // copy in 4-byte words
+        copy_kernel<uint32_t><<<kc.grid, kc.threads, 0, stream>>>(
+            static_cast<const uint32_t*>(in), static_cast<uint32_t*>(out), n, vec16);
         return (int)cudaGetLastError();
+    }
+    if (kc.kernel == TT_KERNEL_ROWCOPY) {
+        const void* fn = pick_rowcopy(E, kc.idx64);
+        if (!fn) return (int)cudaErrorInvalidConfiguration;
+        void* args[] = {(void*)&plan.row, (void*)&in, (void*)&out};
+        return (int)cudaLaunchKernel(fn, dim3(kc.grid), dim3(kc.threads), args, 0, stream);
     }
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
         bool t2 = kc.kernel == TT_KERNEL_TILED2D;

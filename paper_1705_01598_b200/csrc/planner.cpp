@@ -99,6 +99,25 @@ Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, boo
     return pr;
 }
 
+// Element widening: when the fastest dim is unchanged (perm[0] == 0) every
+// row of d0 elements is contiguous on both sides, so k consecutive elements
+// can move as one (E*k)-byte word when k divides d0 (bit-exact: the words are
+// opaque).  Returns k in {1, 2, 4} (E*k <= 16).
+int widen_factor(const Problem& pr) {
+    if (pr.n < 2 || pr.p[0] != 0) return 1;
+    const int kmax = 16 / pr.esize;
+    for (int k = kmax; k >= 2; k /= 2)
+        if (pr.d[0] % k == 0) return k;
+    return 1;
+}
+
+Problem widen_problem(const Problem& pr, int k) {
+    int64_t d[kMaxDims];
+    for (int i = 0; i < pr.n; ++i) d[i] = pr.d[i];
+    d[0] /= k;
+    return normalize(pr.n, d, pr.p, pr.esize * k, true);  // d[0] may have become 1
+}
+
 // --------------------------------------------------------------------------
 // a-4 model.  Constants are B200 measurements: the
 // sustained copy bandwidth of MEASURED_PEAKS.json and per-tile / per-slot
@@ -117,6 +136,24 @@ constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row 
 }  // namespace model
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Hacker's Delight unsigned division by invariant integers: l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1; the 33-bit sum umulhi(n, m) + n cannot
+// overflow for n < 2^31.
+void magic_u31(uint32_t d, uint32_t& m, uint32_t& l) {
+    if (d == 0) d = 1;
+    l = 0;
+    while ((uint64_t(1) << l) < d) ++l;
+    m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+}
+
+template <typename T>
+static void fill_magic(T& t) {
+    for (int g = 0; g < t.h; ++g) {
+        if (t.gC[g] < (int64_t(1) << 31)) magic_u31((uint32_t)t.gC[g], t.gMC[g], t.gLC[g]);
+        if (t.gD[g] < (int64_t(1) << 31)) magic_u31((uint32_t)t.gD[g], t.gMD[g], t.gLD[g]);
+    }
+}
 
 // Expected sectors touched by a run of `bytes` starting at an address that is
 // a multiple of `align` bytes (align a power of two).
@@ -319,6 +356,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         }
     }
     tp.nTiles = acc;
+    fill_magic(tp);
     for (int s = 0; s < tp.nSplit; ++s)
         if (tp.splitChunk[s] > 256) return c;  // kernel packs split coordinates in 8 bits
 
@@ -344,13 +382,14 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         int bestT = 0, bestR = 0;
         long bestWaste = 1L << 40;
         for (int R : {8, 4, 2, 1}) {
+            if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
             int T = (int)ceil_div(tp.V, R);
             T = (int)ceil_div(T, 32) * 32;
             if (forceThreads) {
                 if ((long)forceThreads * R < tp.V) continue;
                 T = forceThreads;
             }
-            if (T > 512) continue;
+            if (T > (R >= 8 ? 256 : 512)) continue;  // kernels.cu launch bounds
             if (T < 64 && R > 1) continue;
             long waste = (long)T * R - tp.V;
             // prefer 128..512 threads, then least waste
@@ -507,6 +546,7 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
         if (i != B) add(pr.d[i], pr.sin[i], pr.sout[i]);
     t.h = g;
     t.nTiles = acc;
+    fill_magic(t);
     fill = (double)pr.vol / ((double)acc * ta * tb);
     return true;
 }
@@ -545,6 +585,38 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         return TT_SUCCESS;
     }
     if (forced == TT_KERNEL_COPY) return TT_UNSUPPORTED;
+
+    // (ii) fastest dim unchanged with long rows: row copy, no staging
+    const bool rowClass = pr.n >= 2 && pr.p[0] == 0;
+    if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
+    if (rowClass && (forced == TT_KERNEL_ROWCOPY ||
+                     (forced == TT_KERNEL_AUTO && pr.d[0] * E >= 512 &&
+                      !(opts && (opts->run_in || opts->run_out))))) {
+        RowParams& r = plan.row;
+        std::memset(&r, 0, sizeof(r));
+        r.row = pr.d[0];
+        r.nRows = pr.vol / pr.d[0];
+        r.h = pr.n - 1;
+        int64_t acc = 1;
+        for (int j = 1; j < pr.n; ++j) {
+            const int i = pr.p[j];
+            r.rC[j - 1] = acc;
+            r.rD[j - 1] = pr.d[i];
+            r.rSin[j - 1] = pr.sin[i];
+            acc *= pr.d[i];
+            if (r.rC[j - 1] < (int64_t(1) << 31)) magic_u31((uint32_t)r.rC[j - 1], r.gMC[j - 1], r.gLC[j - 1]);
+            if (r.rD[j - 1] < (int64_t(1) << 31)) magic_u31((uint32_t)r.rD[j - 1], r.gMD[j - 1], r.gLD[j - 1]);
+        }
+        kc.kernel = TT_KERNEL_ROWCOPY;
+        kc.threads = opts && opts->threads ? opts->threads : 256;
+        const int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : 4;
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)dev.num_sms * perSm,
+                                                              ceil_div(r.nRows * 32, kc.threads)));
+        kc.predicted_us = 2.0 * pr.vol * E / model::kBwBytesPerUs + model::kLaunchUs;
+        kc.model_dram_eff = 1.0;
+        return TT_SUCCESS;
+    }
+    if (forced == TT_KERNEL_ROWCOPY) return TT_UNSUPPORTED;
     if (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE && forced != TT_KERNEL_TILED2D)
         return TT_UNSUPPORTED;
     int vec2d = 0, ta2d = 0, tb2d = 0;
@@ -557,7 +629,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
-    const int Vmax = (E == 4) ? 8192 : 4096;
+    const int Vmax = 2048;  // 256 threads x 8 slots or 512 x 4 (kernel launch bounds)
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
@@ -665,7 +737,19 @@ std::string describe_json(const Plan& plan) {
       << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
       << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
-      << ",\"model_dram_eff\":" << kc.model_dram_eff;
+      << ",\"model_dram_eff\":" << kc.model_dram_eff << ",\"widen\":" << plan.widen;
+    if (kc.kernel == TT_KERNEL_ROWCOPY) {
+        const RowParams& r = plan.row;
+        o << ",\"rowcopy\":{\"row\":" << (long long)r.row << ",\"nRows\":" << (long long)r.nRows
+          << ",\"row_c\":";
+        arr(o, r.rC, r.h);
+        o << ",\"row_d\":";
+        arr(o, r.rD, r.h);
+        o << ",\"row_sin\":";
+        arr(o, r.rSin, r.h);
+        o << "}";
+    }
+    if (plan.narrow) o << ",\"narrow\":" << describe_json(*plan.narrow);
     if (kc.kernel == TT_KERNEL_TILED2D) {
         const Tiled2DParams& t = plan.t2d;
         o << ",\"tiled2d\":{\"TA\":" << kc.tile0 << ",\"TB\":" << kc.tile1 << ",\"nTiles\":"

@@ -66,19 +66,21 @@ struct TileParams {
     int64_t gD[kMaxDims];
     int64_t gSin[kMaxDims];
     int64_t gSout[kMaxDims];
+    // 32-bit multiply-shift division magic for / gC and / gD (see fast_div)
+    uint32_t gMC[kMaxDims], gLC[kMaxDims], gMD[kMaxDims], gLD[kMaxDims];
 };
 
 // Row-copy (fastest dim unchanged, long rows; TiledCopy class P:L141): each
 // row of `row` contiguous elements is contiguous on both sides.  Rows are
 // enumerated in OUTPUT order over the remaining dims.
 struct RowParams {
-    int64_t row;        // elements per row (fused dim 0)
+    int64_t row;        // elements per row (fused dim 0); output row r starts at r*row
     int64_t nRows;
-    int32_t h;          // remaining dims
+    int32_t h;          // remaining dims (output dims 1..n-1, output order)
     int64_t rC[kMaxDims];     // cumulative row count in output order
     int64_t rD[kMaxDims];     // extent
     int64_t rSin[kMaxDims];   // input stride
-    int64_t rSout[kMaxDims];  // output stride
+    uint32_t gMC[kMaxDims], gLC[kMaxDims], gMD[kMaxDims], gLD[kMaxDims];  // fast_div magic
 };
 
 // Two-dimensional vectorised tiled transpose (Tiled class): the
@@ -99,6 +101,7 @@ struct Tiled2DParams {
     int64_t sInB;            // input stride of dim B (elements)
     int64_t sOutA;           // output stride of dim A (elements)
     int64_t gC[kMaxDims], gD[kMaxDims], gSin[kMaxDims], gSout[kMaxDims];
+    uint32_t gMC[kMaxDims], gLC[kMaxDims], gMD[kMaxDims], gLD[kMaxDims];
 };
 
 struct KernelChoice {
@@ -133,7 +136,7 @@ struct OccQuery {
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 
-struct ShardInfo;  // defined in dist.cpp
+struct ShardInfo;  // defined in dist.cu
 
 struct Plan {
     uint32_t magic = 0x54545054u;  // "TTPT"
@@ -148,11 +151,19 @@ struct Plan {
     RowParams row{};
     Tiled2DParams t2d{};
     ShardInfo* shard = nullptr;    // sharded plans only
+    int widen = 1;                 // words of the fused problem = widen original elements
+    Plan* narrow = nullptr;        // un-widened plan, for pointers not aligned to E*widen
+    ~Plan();
 };
 
 // planner.cpp ---------------------------------------------------------------
+// Magic (m, l) such that floor(n / d) == (umulhi(n, m) + n) >> l for all
+// 0 <= n < 2^31 and 1 <= d < 2^31.
+void magic_u31(uint32_t d, uint32_t& m, uint32_t& l);
 tt_status_t validate(int rank, const int64_t* dims, const int* perm, size_t elem_size);
 Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, bool fuse);
+int widen_factor(const Problem& pr);
+Problem widen_problem(const Problem& pr, int k);
 tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
                         OccupancyFn occ);
 std::string describe_json(const Plan& plan);

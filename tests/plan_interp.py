@@ -17,7 +17,7 @@ def interpret_tile_plan(j, words):
     tails = [se[s] - (-(-se[s] // sc[s]) - 1) * sc[s] for s in range(len(st))]
     gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
     vol = int(np.prod(j["dims"]))
-    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
+    out = np.zeros(vol, dtype=words.dtype)
     written = np.zeros(vol, dtype=np.int64)
     # per-slot tables
     gin, pin, cin_s = [], [], []
@@ -72,7 +72,7 @@ def interpret_tiled2d_plan(j, words):
     TA, TB = t["TA"], t["TB"]
     gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
     vol = int(np.prod(j["dims"]))
-    out = np.full(vol, 0xDEADBEEF, dtype=words.dtype)
+    out = np.zeros(vol, dtype=words.dtype)
     written = np.zeros(vol, dtype=np.int64)
     for tile in range(t["nTiles"]):
         q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
@@ -91,12 +91,35 @@ def interpret_tiled2d_plan(j, words):
 
 
 
+def interpret_rowcopy_plan(j, words):
+    """Replay the row-copy kernel: output row r = contiguous input row at
+    sum_j digit_j(r) * row_sin[j]."""
+    t = j["rowcopy"]
+    L, n = t["row"], t["nRows"]
+    out = np.zeros(L * n, dtype=words.dtype)
+    for r in range(n):
+        base = sum(((r // c) % d) * s for c, d, s in zip(t["row_c"], t["row_d"], t["row_sin"]))
+        out[r * L:(r + 1) * L] = words[base:base + L]
+    return out
+
+
 def interpret_plan(j, words):
-    """Output of a (non-sharded) plan description applied to ``words``."""
+    """Output of a (non-sharded) plan description applied to ``words``.
+    A widened plan (elem_size = widen x the caller's element) is replayed on
+    the same bytes viewed as wider opaque words."""
+    E = j["elem_size"]
+    orig = words.dtype
+    if words.dtype.itemsize != E:
+        words = np.ascontiguousarray(words).view(np.dtype(f"V{E}"))
     if j["kernel"] == "copy":
-        return np.array(words, copy=True)
-    fj = dict(j)
-    fj["dims"] = j["fused"]["dims"]
-    if j["kernel"] == "tiled2d":
-        return interpret_tiled2d_plan(fj, words)
-    return interpret_tile_plan(fj, words)
+        out = np.array(words, copy=True)
+    else:
+        fj = dict(j)
+        fj["dims"] = j["fused"]["dims"]
+        if j["kernel"] == "tiled2d":
+            out = interpret_tiled2d_plan(fj, words)
+        elif j["kernel"] == "rowcopy":
+            out = interpret_rowcopy_plan(fj, words)
+        else:
+            out = interpret_tile_plan(fj, words)
+    return out.view(orig)

@@ -142,6 +142,27 @@ def test_forced_tiled2d(esize):
         np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
 
 
+ROW_SHAPES = [((600, 7, 5), (0, 2, 1)), ((256, 3, 5, 2), (0, 3, 1, 2)), ((8, 7, 5), (0, 2, 1)),
+              ((6, 5, 7), (0, 2, 1)), ((1001, 3, 4), (0, 2, 1)), ((2, 300, 3, 17), (0, 3, 2, 1)),
+              ((128, 2, 2, 2, 2, 2), (0, 5, 3, 1, 4, 2)), ((4, 4), (0, 1))]
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+def test_rowcopy_and_widening(esize):
+    """Fastest dim unchanged: row copy and widened words (auto), forced row
+    copy without widening, and unaligned pointers taking the narrow plan."""
+    for dims, perm in ROW_SHAPES:
+        check(dims, perm, esize)
+        try:
+            check(dims, perm, esize, kernel=tt.KERNEL_ROWCOPY)
+        except tt.TTError:
+            assert dims == (4, 4)  # rank 1 after fusion: copy, not row copy
+        words = wl.random_words(int(np.prod(dims)), esize, 12)
+        for off in (1, 2):
+            got = run_gpu(dims, perm, words, offset=off)
+            np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)

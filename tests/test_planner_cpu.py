@@ -79,13 +79,20 @@ def test_offline_plan_cannot_execute():
 ])
 def test_normalisation(dims, perm, fdims, fperm):
     j = tt.plan_offline(dims, perm, 4)
-    assert tuple(j["fused"]["dims"]) == fdims
-    assert tuple(j["fused"]["perm"]) == fperm
-    assert j["kernel"] in (("copy",) if len(fdims) == 1 else ("tile", "tiled2d"))
+    jn = j.get("narrow") or j       # widened plans keep the unwidened one as "narrow"
+    assert tuple(jn["fused"]["dims"]) == fdims
+    assert tuple(jn["fused"]["perm"]) == fperm
+    assert j["kernel"] in (("copy",) if len(fdims) == 1 else ("tile", "tiled2d", "rowcopy"))
+    j2 = tt.plan_offline(dims, perm, 4, no_widen=True)
+    assert tuple(j2["fused"]["dims"]) == fdims and j2["widen"] == 1
 
 
 CASES = [
     ((7, 13, 5), (2, 0, 1)),
+    ((600, 7, 5), (0, 2, 1)),               # row copy
+    ((8, 7, 5), (0, 2, 1)),                 # widened short rows (tile)
+    ((256, 3, 5, 2), (0, 3, 1, 2)),         # widened row copy
+    ((6, 5, 7), (0, 2, 1)),                 # widen by 2 (4-byte)
     ((67, 45), (1, 0)),
     ((5, 3, 2, 4, 7, 6), (4, 0, 5, 2, 3, 1)),
     ((2, 3, 4, 3, 2, 2, 3, 2, 5, 4), tuple(range(9, -1, -1))),
@@ -103,8 +110,10 @@ def test_plan_interpreter_matches_oracle(dims, perm, esize):
     j = tt.plan_offline(dims, perm, esize)
     words = wl.random_words(int(np.prod(dims)), esize, 77)
     want = orc.permute(dims, perm, words)
-    if j["kernel"] == "copy":
-        np.testing.assert_array_equal(words, want)
+    np.testing.assert_array_equal(interpret_plan(j, words), want)
+    if j.get("narrow"):
+        np.testing.assert_array_equal(interpret_plan(j["narrow"], words), want)
+    if j["kernel"] in ("copy", "rowcopy") or j["widen"] > 1:
         return
     # the interpreter works on the fused problem the plan describes
     fj = dict(j)
