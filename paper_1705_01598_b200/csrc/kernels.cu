@@ -93,6 +93,25 @@ __device__ __forceinline__ T* opaque(T* p) {
     return p;
 }
 
+// base + off elements as one mad.wide.u32 (32-bit offsets stay 32-bit in
+// registers instead of being hoisted as 64-bit byte offsets).
+template <typename W>
+__device__ __forceinline__ const W* elem_addr(const W* base, uint32_t off) {
+    const W* r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(off), "n"((int)sizeof(W)), "l"(base));
+    return r;
+}
+template <typename W>
+__device__ __forceinline__ W* elem_addr(W* base, uint32_t off) {
+    W* r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(off), "n"((int)sizeof(W)), "l"(base));
+    return r;
+}
+template <typename W>
+__device__ __forceinline__ const W* elem_addr(const W* base, int64_t off) { return base + off; }
+template <typename W>
+__device__ __forceinline__ W* elem_addr(W* base, int64_t off) { return base + off; }
+
 // ---------------------------------------------------------------------------
 // generic staged tile
 // ---------------------------------------------------------------------------
@@ -156,7 +175,7 @@ __device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
 // ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
 // cover the tile's `need`.
 template <typename W, int NREG, typename I>
-__global__ void __launch_bounds__(NREG >= 8 ? 256 : 512, (NREG >= 8 ? (sizeof(W) >= 8 ? 2 : 3) : (sizeof(I) == 8 ? 1 : 2)))
+__global__ void __launch_bounds__(512, (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2))
 tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -168,7 +187,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     // Per-thread loop-invariant minor positions (Eqs. 4-6; the
     // register arrays of P:L155-159).
     I gin[NREG], gout[NREG];
-    uint32_t sin_[NREG], sout[NREG];
+    uint32_t spk[NREG];  // staging byte offsets: load element (low 16 bits), store element (high)
     uint32_t flags = 0;
     const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
     const bool allSlots = p.V == NT * NREG;  // CTA-uniform
@@ -176,8 +195,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     for (int r = 0; r < NREG; ++r) {
         gin[r] = 0;
         gout[r] = 0;
-        sin_[r] = 0;
-        sout[r] = 0;
+        spk[r] = 0;
         if (r < nmine) {
             const int k = tid + r * NT;
             uint32_t f = 0;
@@ -192,7 +210,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (p.nSplit > 1 && i == p.splitTile[1] && c < p.splitTail[1]) f |= 2u;
             }
             gin[r] = off;
-            sin_[r] = (uint32_t)(k + (k / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
+            spk[r] = (uint32_t)(k + (k / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
             // Eqs. (5), (6): pMinorOut(k') and pSh(k'), tile-output order
             rem = k;
             off = 0;
@@ -207,7 +225,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (p.nSplit > 1 && t == p.splitTile[1] && c < p.splitTail[1]) f |= 8u;
             }
             gout[r] = off;
-            sout[r] = (uint32_t)(sh + (sh / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
+            spk[r] |= ((uint32_t)(sh + (sh / p.padEvery) * p.pad) * (uint32_t)sizeof(W)) << 16;
             flags |= f << (4 * r);
         }
     }
@@ -222,11 +240,11 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         const W* __restrict__ src = opaque(in + tb.in);
         if (tb.need == 0 && allSlots) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) v[r] = ldg_(src + gin[r]);
+            for (int r = 0; r < NREG; ++r) v[r] = ldg_(elem_addr(src, gin[r]));
         } else {
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(src + gin[r]);
+                if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(elem_addr(src, gin[r]));
         }
     };
     TileBase<I> cur = decode_tile<I>(p, t, lane);
@@ -237,11 +255,11 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         // stage the tile in input order
         if (allSlots) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) sts(sb + sin_[r], v[r]);
+            for (int r = 0; r < NREG; ++r) sts(sb + (spk[r] & 0xffffu), v[r]);
         } else {
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine) sts(sb + sin_[r], v[r]);
+                if (r < nmine) sts(sb + (spk[r] & 0xffffu), v[r]);
         }
         __syncthreads();
         // issue the next tile's global loads before writing this one
@@ -255,13 +273,13 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         W* __restrict__ dst = opaque(out + now.out);
         if (now.need == 0 && allSlots) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) dst[gout[r]] = lds<W>(sb + sout[r]);
+            for (int r = 0; r < NREG; ++r) *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
         } else {
             const uint32_t needOut = now.need << 2;
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
                 if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
-                    dst[gout[r]] = lds<W>(sb + sout[r]);
+                    *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
         }
         // Two buffers: the next iteration writes the other buffer, whose
         // readers (previous tile) all passed this iteration's barrier.

@@ -133,6 +133,7 @@ constexpr double kTileInstr64 = 160.0;    // same with 64-bit index arithmetic
 constexpr double kSlotInstr = 11.0;       // per warp per slot: LDG, STS, LDS, STG, masks, address
 constexpr double kLaunchUs = 3.0;         // launch + tail
 constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row locality overhead
+constexpr double kInflightBytes = 32768;  // loads in flight per SM needed for full bandwidth
 }  // namespace model
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -389,7 +390,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
                 if ((long)forceThreads * R < tp.V) continue;
                 T = forceThreads;
             }
-            if (T > (R >= 8 ? 256 : 512)) continue;  // kernels.cu launch bounds
+            if (T > 512) continue;  // kernels.cu launch bounds
             if (T < 64 && R > 1) continue;
             long waste = (long)T * R - tp.V;
             // prefer 128..512 threads, then least waste
@@ -432,7 +433,13 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         c.dram_eff = usefulSec / modelSec;
         // slots of ragged tiles are partly idle but still issued
         const double bytes = (double)tp.nTiles * modelSec * model::kSector;
-        const double t_mem = bytes / model::kBwBytesPerUs;
+        // memory-level parallelism: bytes of loads in flight per SM (the
+        // B200 analogue of the paper's MWP/MLP terms)
+        const OccQuery oq{TT_KERNEL_TILE, pr.esize, c.nreg, 1, c.threads, c.smem,
+                          pr.vol >= (int64_t(1) << 31), 0, 0};
+        const double inflight = (double)estimate_occupancy(oq, dev) * c.threads * c.nreg * E;
+        const double mlp = std::min(1.0, inflight / model::kInflightBytes);
+        const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
         const double warps = c.threads / 32.0;
         const double perTile = warps * ((pr.vol >= (int64_t(1) << 31) ? model::kTileInstr64
                                                                       : model::kTileInstr) +
@@ -552,8 +559,15 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
 }
 
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
-    int regs = 40 + q.nreg * (q.esize == 8 ? 6 : 5) + (q.idx64 ? q.nreg * 2 : 0);
-    regs = (regs + 7) / 8 * 8;
+    // register counts of the tile kernels as compiled (ptxas -v, build/obj)
+    int regs;
+    if (q.kernel == TT_KERNEL_TILE) {
+        const int r8 = q.esize == 8 ? 96 : 64;
+        regs = q.nreg >= 8 ? r8 : q.nreg >= 4 ? 56 : q.nreg >= 2 ? 52 : 44;
+        if (q.idx64) regs += 16;
+    } else {
+        regs = 64;
+    }
     int byRegs = dev.regs_per_sm / std::max(1, regs * q.threads);
     int byThreads = dev.max_threads_per_sm / std::max(1, q.threads);
     int bySmem = q.smem > 0 ? dev.max_smem_per_sm / (q.smem + 1024) : 32;
@@ -629,7 +643,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
-    const int Vmax = 2048;  // 256 threads x 8 slots or 512 x 4 (kernel launch bounds)
+    // 512 threads x 8 slots, and staging byte offsets < 2^16 (16-bit packing)
+    const int Vmax = std::min(4096, 57344 / E);
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
@@ -728,7 +743,8 @@ std::string describe_json(const Plan& plan) {
     arr(o, plan.dims.data(), plan.rank);
     o << ",\"perm\":";
     arr(o, plan.perm.data(), plan.rank);
-    o << ",\"elem_size\":" << pr.esize << ",\"vol\":" << (long long)pr.vol;
+    o << ",\"elem_size\":" << pr.esize / plan.widen << ",\"word_size\":" << pr.esize
+      << ",\"vol\":" << (long long)pr.vol;
     o << ",\"fused\":{\"rank\":" << pr.n << ",\"dims\":";
     arr(o, pr.d, pr.n);
     o << ",\"perm\":";

@@ -107,7 +107,7 @@ def interpret_plan(j, words):
     """Output of a (non-sharded) plan description applied to ``words``.
     A widened plan (elem_size = widen x the caller's element) is replayed on
     the same bytes viewed as wider opaque words."""
-    E = j["elem_size"]
+    E = j["word_size"]
     orig = words.dtype
     if words.dtype.itemsize != E:
         words = np.ascontiguousarray(words).view(np.dtype(f"V{E}"))
