@@ -373,7 +373,7 @@ def run_ours(args):
                                 ("independent tensor per GPU" if world > 1 else "single GPU")),
                 "l2": "inputs larger than L2 (%.0f MB per tensor > 126 MB L2); no flush" % (local_vol * E / 1e6),
                 "plan": {k: desc_plan.get(k) for k in ("kernel", "threads", "grid", "smem", "nreg")},
-                "tile": {k: desc_plan.get("tile", {}).get(k) for k in ("ext", "V", "pad", "padEvery")},
+                "tile": {k: desc_plan.get("tile", {}).get(k) for k in ("ext", "V", "sm")},
             },
             "memcpy_gbs_per_gpu": round(memcpy_gbs, 2),
             "frac_of_memcpy": round(achieved / memcpy_gbs, 4),

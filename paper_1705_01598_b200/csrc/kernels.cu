@@ -126,47 +126,103 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t l)
     return (__umulhi(n, m) + n) >> l;
 }
 
-// Algorithm 1: lane i < h evaluates the i-th term of Eqs. (2)
-// and (3) for the tile index b = t -- mod(floor(t / c_i), d_i) * stride_i --
-// and an XOR butterfly sums the terms; every lane ends with both bases.  The
-// same decode order serves both sums (reading R3).  A lane holding
-// a split dim also reports whether this tile is that dim's ragged last chunk
-// (PackedSplit edge), gathered with one ballot.  32-bit indices use
-// multiply-shift division with per-lane magic numbers from the planner.
-template <typename I, typename P>
-__device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
-    I vin = 0, vout = 0;
-    bool ragged = false;
-    if (lane < p.h) {
-        I q;
-        if constexpr (sizeof(I) == 4) {
-            const uint32_t q1 = fast_div((uint32_t)t, p.gMC[lane], p.gLC[lane]);
-            const uint32_t q2 = fast_div(q1, p.gMD[lane], p.gLD[lane]);
-            q = (I)(q1 - q2 * (uint32_t)p.gD[lane]);
-        } else {
-            q = (t / (I)p.gC[lane]) % (I)p.gD[lane];
+// Warp-parallel walk over the tile grid (the "major" dims M̄_mk).
+// Lane i < h owns grid dim i: its extent, its input/output strides and its
+// digit of the current tile index, all in registers (indexing the kernel
+// parameters per lane would serialise the constant cache).
+//  * seek(t): Algorithm 1 -- every lane evaluates its term
+//    mod(floor(t / c_i), d_i) * stride_i (multiply-shift division for 32-bit
+//    indices) and an XOR butterfly sums the terms for Eq. (2) and Eq. (3) in
+//    ONE common order (R3).
+//  * next(): the tile t+1 from tile t without any division: a ballot finds the
+//    first digit that does not wrap; its lane's precomputed carry (its stride
+//    minus the wrapped lower digits' spans, an exclusive warp scan done once)
+//    is broadcast with one shuffle per side.
+// Split dims report their ragged last chunk (PackedSplit edge).
+template <typename I>
+struct GridWalker {
+    I d, x, sIn, sOut, cIn, cOut;
+    uint32_t mC, lC, mD, lD;
+    I cC;
+    uint32_t splitBit;  // 1 / 2 if this lane is split dim A / B with a ragged tail
+    int h, lane;
+
+    template <typename P>
+    __device__ __forceinline__ GridWalker(const P& p, int lane_) : lane(lane_) {
+        h = p.h;
+        d = 1; sIn = 0; sOut = 0; x = 0; cC = 1;
+        mC = 1; lC = 0; mD = 1; lD = 0;
+        splitBit = 0;
+        if (lane < h) {
+            d = (I)p.gD[lane];
+            sIn = (I)p.gSin[lane];
+            sOut = (I)p.gSout[lane];
+            cC = (I)p.gC[lane];
+            mC = p.gMC[lane]; lC = p.gLC[lane]; mD = p.gMD[lane]; lD = p.gLD[lane];
+            if (p.nSplit > 0 && lane == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) splitBit |= 1u;
+            if (p.nSplit > 1 && lane == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]) splitBit |= 2u;
         }
-        vin = q * (I)p.gSin[lane];
-        vout = q * (I)p.gSout[lane];
-        ragged = (q == (I)p.gD[lane] - 1) &&
-                 ((p.nSplit > 0 && lane == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) ||
-                  (p.nSplit > 1 && lane == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]));
-    }
+        // exclusive scan of the wrapped spans (d_i - 1) * stride_i over lanes
+        I spanIn = (lane < h) ? (d - 1) * sIn : (I)0;
+        I spanOut = (lane < h) ? (d - 1) * sOut : (I)0;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        vin += __shfl_xor_sync(0xffffffffu, vin, o);
-        vout += __shfl_xor_sync(0xffffffffu, vout, o);
+        for (int o = 1; o < 32; o <<= 1) {
+            const I ui = __shfl_up_sync(0xffffffffu, spanIn, o);
+            const I uo = __shfl_up_sync(0xffffffffu, spanOut, o);
+            if (lane >= o) { spanIn += ui; spanOut += uo; }
+        }
+        const I exIn = __shfl_up_sync(0xffffffffu, spanIn, 1);
+        const I exOut = __shfl_up_sync(0xffffffffu, spanOut, 1);
+        cIn = sIn - (lane > 0 ? exIn : (I)0);
+        cOut = sOut - (lane > 0 ? exOut : (I)0);
     }
-    const uint32_t bal = __ballot_sync(0xffffffffu, ragged);
-    uint32_t need = 0;
-    if (p.nSplit > 0) need |= (bal >> p.splitLane[0]) & 1u;
-    if (p.nSplit > 1) need |= ((bal >> p.splitLane[1]) & 1u) << 1;
-    TileBase<I> b;
-    b.in = vin;
-    b.out = vout;
-    b.need = need;
-    return b;
-}
+
+    __device__ __forceinline__ uint32_t need() const {
+        const bool last = lane < h && x == d - 1;
+        const uint32_t a = __ballot_sync(0xffffffffu, last && (splitBit & 1u));
+        const uint32_t b = __ballot_sync(0xffffffffu, last && (splitBit & 2u));
+        return (a ? 1u : 0u) | (b ? 2u : 0u);
+    }
+
+    __device__ __forceinline__ TileBase<I> seek(I t) {
+        if (lane < h) {
+            if constexpr (sizeof(I) == 4) {
+                const uint32_t q1 = fast_div((uint32_t)t, mC, lC);
+                x = (I)(q1 - fast_div(q1, mD, lD) * (uint32_t)d);
+            } else {
+                x = (t / cC) % d;
+            }
+        }
+        I vin = x * sIn, vout = x * sOut;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            vin += __shfl_xor_sync(0xffffffffu, vin, o);
+            vout += __shfl_xor_sync(0xffffffffu, vout, o);
+        }
+        TileBase<I> b;
+        b.in = vin;
+        b.out = vout;
+        b.need = need();
+        return b;
+    }
+
+    __device__ __forceinline__ TileBase<I> next(const TileBase<I>& cur) {
+        const uint32_t wraps = __ballot_sync(0xffffffffu, lane < h && x == d - 1);
+        const int f = __ffs(~wraps) - 1;  // first digit that does not wrap (< h inside the grid)
+        TileBase<I> b;
+        b.in = cur.in + __shfl_sync(0xffffffffu, cIn, f);
+        b.out = cur.out + __shfl_sync(0xffffffffu, cOut, f);
+        if (lane < f) x = 0;
+        else if (lane == f) x += 1;
+        b.need = need();
+        return b;
+    }
+};
+
+// Stateless Algorithm-1 decode (used by the 2-D kernel's interleaved tile
+// order); per-lane grid values come from the walker's registers.
+template <typename I>
+__device__ __forceinline__ TileBase<I> decode_tile(GridWalker<I>& g, I t) { return g.seek(t); }
 
 // Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
 // (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
@@ -202,15 +258,17 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             // Eq. (4): pMinorIn(k), tile-input order
             int rem = k;
             I off = 0;
+            int sp = 0;
             for (int i = 0; i < p.a; ++i) {
                 const int c = rem % p.tExt[i];
                 rem /= p.tExt[i];
                 off += (I)c * (I)p.tSin[i];
+                sp += c * p.tSm[i];
                 if (p.nSplit > 0 && i == p.splitTile[0] && c < p.splitTail[0]) f |= 1u;
                 if (p.nSplit > 1 && i == p.splitTile[1] && c < p.splitTail[1]) f |= 2u;
             }
             gin[r] = off;
-            spk[r] = (uint32_t)(k + (k / p.padEvery) * p.pad) * (uint32_t)sizeof(W);
+            spk[r] = (uint32_t)sp * (uint32_t)sizeof(W);
             // Eqs. (5), (6): pMinorOut(k') and pSh(k'), tile-output order
             rem = k;
             off = 0;
@@ -220,20 +278,23 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 const int c = rem % p.tExt[t];
                 rem /= p.tExt[t];
                 off += (I)c * (I)p.tSout[t];
-                sh += c * p.tCin[t];
+                sh += c * p.tSm[t];
                 if (p.nSplit > 0 && t == p.splitTile[0] && c < p.splitTail[0]) f |= 4u;
                 if (p.nSplit > 1 && t == p.splitTile[1] && c < p.splitTail[1]) f |= 8u;
             }
             gout[r] = off;
-            spk[r] |= ((uint32_t)(sh + (sh / p.padEvery) * p.pad) * (uint32_t)sizeof(W)) << 16;
+            spk[r] |= ((uint32_t)sh * (uint32_t)sizeof(W)) << 16;
             flags |= f << (4 * r);
         }
     }
 
+    // contiguous tile range per CTA, walked with the odometer
     const I nTiles = (I)p.nTiles;
-    I t = (I)blockIdx.x;
-    if (t >= nTiles) return;
-    const I stride = (I)gridDim.x;
+    const I G = (I)gridDim.x;
+    const I t0 = (I)(((uint64_t)nTiles * blockIdx.x) / G);
+    const I t1 = (I)(((uint64_t)nTiles * (blockIdx.x + 1)) / G);
+    if (t0 >= t1) return;
+    GridWalker<I> walk(p, lane);
 
     W v[NREG];
     auto load = [&](const TileBase<I>& tb) {
@@ -247,11 +308,11 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(elem_addr(src, gin[r]));
         }
     };
-    TileBase<I> cur = decode_tile<I>(p, t, lane);
+    TileBase<I> cur = walk.seek(t0);
     load(cur);
 
     uint32_t sb = sm0;
-    for (; t < nTiles; t += stride) {
+    for (I t = t0; t < t1; ++t) {
         // stage the tile in input order
         if (allSlots) {
 #pragma unroll
@@ -264,9 +325,8 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         __syncthreads();
         // issue the next tile's global loads before writing this one
         const TileBase<I> now = cur;
-        const I tn = t + stride;
-        if (tn < nTiles) {
-            cur = decode_tile<I>(p, tn, lane);
+        if (t + 1 < t1) {
+            cur = walk.next(cur);
             load(cur);
         }
         // transposed read of shared memory (Eq. 6), coalesced writes (Eq. 5)
@@ -417,7 +477,8 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
         }
     };
 
-    TileBase<I> cur = decode_tile<I>(p, t, lane);
+    GridWalker<I> walk(p, lane);
+    TileBase<I> cur = walk.seek(t);
     load(cur);
     int buf = 0;
     for (; t < nTiles; t += stride) {
@@ -442,7 +503,7 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
         const TileBase<I> now = cur;
         const I tn = t + stride;
         if (tn < nTiles) {
-            cur = decode_tile<I>(p, tn, lane);
+            cur = walk.seek(tn);
             load(cur);
         }
         const int limA = (now.need & 1u) ? p.splitTail[0] : TA;

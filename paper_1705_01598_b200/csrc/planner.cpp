@@ -133,7 +133,7 @@ constexpr double kTileInstr64 = 160.0;    // same with 64-bit index arithmetic
 constexpr double kSlotInstr = 11.0;       // per warp per slot: LDG, STS, LDS, STG, masks, address
 constexpr double kLaunchUs = 3.0;         // launch + tail
 constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row locality overhead
-constexpr double kInflightBytes = 32768;  // loads in flight per SM needed for full bandwidth
+constexpr double kInflightBytes = 49152;  // loads in flight per SM needed for full bandwidth
 }  // namespace model
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -221,34 +221,35 @@ static int warp_wavefronts(const int* pos, int nlanes, int esize) {
     return total;
 }
 
-// Exact bank-conflict cost of a smem layout over the whole tile (the paper's
-// TPR_shmem "calculated at runtime using the element positions given by
-// Equation (6)"), both the staging store (input order) and the
-// transposed read (output order).
-static long smem_cost(const TileParams& tp, int esize, int padEvery, int pad) {
+// Bank-conflict cost of a staging layout (the paper's TPR_shmem "calculated
+// at runtime using the element positions given by Equation (6)"),
+// for both the staging store (input order) and the transposed read (output
+// order), on a sample of warps (cf. the 10 samples of P:L244).  Element
+// (c_i) sits at sum_i c_i * sm[i].
+static long smem_cost(const TileParams& tp, int esize, const int32_t* sm) {
     const int V = tp.V;
     const int nw = (V + 31) / 32;
-    const int step = std::max(1, nw / 8);  // sample ~8 warps (cf. P:L244's 10 samples)
+    const int step = std::max(1, nw / 8);
     long cost = 0;
     int pos[32];
-    // staging store: consecutive k
-    for (int w = 0; w * 32 < V; w += step) {
-        int nl = std::min(32, V - w * 32);
-        for (int l = 0; l < nl; ++l) { int k = w * 32 + l; pos[l] = k + (k / padEvery) * pad; }
-        cost += warp_wavefronts(pos, nl, esize);
-    }
-    // transposed read: consecutive k' in output order -> pSh (Eq. 6)
-    for (int w = 0; w * 32 < V; w += step) {
-        int nl = std::min(32, V - w * 32);
+    for (int w = 0; w < nw; w += step) {
+        const int nl = std::min(32, V - w * 32);
+        // staging store: consecutive k in input order
         for (int l = 0; l < nl; ++l) {
-            int kk = w * 32 + l, sh = 0;
+            int kk = w * 32 + l, sp = 0;
+            for (int i = 0; i < tp.a; ++i) { sp += (kk % tp.tExt[i]) * sm[i]; kk /= tp.tExt[i]; }
+            pos[l] = sp;
+        }
+        cost += warp_wavefronts(pos, nl, esize);
+        // transposed read: consecutive k' in output order
+        for (int l = 0; l < nl; ++l) {
+            int kk = w * 32 + l, sp = 0;
             for (int jj = 0; jj < tp.a; ++jj) {
-                int t = tp.tOutOrder[jj];
-                int c = kk % tp.tExt[t];
+                const int t = tp.tOutOrder[jj];
+                sp += (kk % tp.tExt[t]) * sm[t];
                 kk /= tp.tExt[t];
-                sh += c * tp.tCin[t];
             }
-            pos[l] = sh + (sh / padEvery) * pad;
+            pos[l] = sp;
         }
         cost += warp_wavefronts(pos, nl, esize);
     }
@@ -404,7 +405,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
 
     // smem footprint with the worst-case padding (layout chosen for the winner)
     {
-        int64_t words = tp.V + tp.V / 8 + 8;
+        int64_t words = tp.V + tp.V / 4 + 64;  // choose_smem's padding cap
         c.smem = (int)(2 * ((words + 3) / 4 * 4) * pr.esize);
         if (c.smem > dev.max_smem_per_block) return c;
     }
@@ -452,33 +453,49 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
     return c;
 }
 
-// Shared-memory layout: pick (padEvery, pad) with the fewest modelled
-// wavefronts (the L x (L+1) padding of P:L123 generalised), then footprint.
+// Shared-memory layout: per-dimension padded strides sm[i] = sm[i-1]*ext[i-1]
+// + pad[i] (the L x (L+1) padding of P:L123 generalised to every level of
+// the tile), chosen by coordinate descent on the conflict model, then by
+// footprint.  Footprint is capped so the 16-bit staging offsets fit.
 static void choose_smem(TileParams& tp, int esize) {
-    const int ideal = esize == 4 ? 1 : 2;
+    const int a = tp.a;
+    int32_t pad[kMaxDims] = {};
+    int32_t sm[kMaxDims];
+    auto strides = [&](const int32_t* pd, int32_t* out) -> int64_t {
+        int64_t acc = 1;
+        for (int i = 0; i < a; ++i) {
+            acc += (i > 0 ? pd[i] : 0);
+            out[i] = (int32_t)acc;
+            acc *= tp.tExt[i];
+        }
+        // footprint: last element + 1
+        int64_t last = 0;
+        for (int i = 0; i < a; ++i) last += (int64_t)(tp.tExt[i] - 1) * out[i];
+        return last + 1;
+    };
+    const int64_t limit = std::min<int64_t>((65536 / esize) - 8, tp.V + tp.V / 4 + 64);
+    strides(pad, sm);
+    long best = smem_cost(tp, esize, sm);
+    const int ideal_per_warp = esize == 4 ? 2 : esize == 8 ? 4 : 8;  // store + read
     const int nw = (tp.V + 31) / 32;
-    const int sampled = (nw + std::max(1, nw / 8) - 1) / std::max(1, nw / 8);
-    long best = smem_cost(tp, esize, 1 << 30, 0);
-    int bestEvery = 1 << 30, bestPad = 0;
-    if (best > (long)2 * sampled * ideal) {
-        std::vector<int> everies;
-        for (int t = 1; t < tp.a; ++t)
-            if (tp.tCin[t] >= 2 && tp.tCin[t] < tp.V) everies.push_back(tp.tCin[t]);
-        everies.push_back(32);
-        for (int ev : everies) {
-            for (int pad : {1, 2, 4}) {
-                if ((int64_t)(tp.V / ev) * pad > tp.V / 8) continue;  // footprint bound of build_tile
-                long cst = smem_cost(tp, esize, ev, pad);
-                if (cst < best || (cst == best && ev > bestEvery)) {
-                    best = cst; bestEvery = ev; bestPad = pad;
-                }
+    const long ideal = (long)((nw + std::max(1, nw / 8) - 1) / std::max(1, nw / 8)) * ideal_per_warp;
+    for (int pass = 0; pass < 2 && best > ideal; ++pass) {
+        for (int i = 1; i < a && best > ideal; ++i) {
+            int32_t keep = pad[i];
+            int32_t bestPad = keep;
+            for (int c = 0; c < 32; ++c) {
+                pad[i] = c;
+                const int64_t foot = strides(pad, sm);
+                if (foot > limit) continue;
+                const long cst = smem_cost(tp, esize, sm);
+                if (cst < best) { best = cst; bestPad = c; }
             }
+            pad[i] = bestPad;
         }
     }
-    tp.padEvery = bestEvery;
-    tp.pad = bestPad;
-    int64_t words = tp.V + (bestPad ? (int64_t)((tp.V - 1) / bestEvery) * bestPad : 0) + 1;
-    tp.sbuf = (int32_t)((words + 3) / 4 * 4);
+    const int64_t foot = strides(pad, sm);
+    for (int i = 0; i < a; ++i) tp.tSm[i] = sm[i];
+    tp.sbuf = (int32_t)((foot + 3) / 4 * 4);
 }
 
 // Vectorised 2-D tiled kernel (TT_KERNEL_TILED2D): A = input dim 0, B = p[0].
@@ -788,11 +805,13 @@ std::string describe_json(const Plan& plan) {
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
         const TileParams& t = plan.tile;
         o << ",\"tile\":{\"V\":" << t.V << ",\"sbuf\":" << t.sbuf << ",\"nTiles\":"
-          << (long long)t.nTiles << ",\"padEvery\":" << t.padEvery << ",\"pad\":" << t.pad
+          << (long long)t.nTiles
           << ",\"ext\":";
         arr(o, t.tExt, t.a);
         o << ",\"cin\":";
         arr(o, t.tCin, t.a);
+        o << ",\"sm\":";
+        arr(o, t.tSm, t.a);
         o << ",\"cout\":";
         arr(o, t.tCout, t.a);
         o << ",\"out_order\":";

@@ -33,9 +33,10 @@ struct Problem {
 // A tile is the sub-volume M_mk (the union of the first input dims M_m and
 // the first output dims M_k), with at most one split dim per side
 // (PackedSplit).  Tile dims are listed in input order; the kernel
-// reads a tile with input-order index k (Eq. 4), stages it in shared memory
-// at position pos(k) = k + (k / padEvery) * pad, and writes it with
-// output-order index k' (Eqs. 5, 6).  The remaining dims (and the chunk
+// reads a tile with input-order index k (Eq. 4), stages element (c_i) at
+// shared position sum_i c_i * tSm[i] (Eq. 6 with padded strides tSm instead
+// of the dense c(q_i, M_mk^I), chosen by the planner's bank-conflict model),
+// and writes it with output-order index k' (Eq. 5).  The remaining dims (and the chunk
 // index of split dims) are the "major" grid dims M̄_mk decoded per tile with
 // the warp-parallel Algorithm 1 in ONE common order for both the
 // read and the write base (reading R3).
@@ -46,8 +47,6 @@ struct TileParams {
     int32_t sbuf;       // elements per shared-memory buffer incl. padding
     int32_t a;          // number of tile dims
     int32_t h;          // number of grid dims (<= 32, one warp lane each)
-    int32_t padEvery;   // smem layout: pos(k) = k + (k / padEvery) * pad
-    int32_t pad;
     int32_t nSplit;     // number of split tile dims (0..2)
     int32_t splitLane[2];   // grid lane carrying the split dim's chunk index
     int32_t splitChunk[2];  // tile extent of the split dim
@@ -57,6 +56,7 @@ struct TileParams {
     // tile dims (tile-input order, i.e. ascending input dimension)
     int32_t tExt[kMaxDims];       // tile extent
     int32_t tCin[kMaxDims];       // c(q_i, M_mk^I): cumulative volume, tile-input order
+    int32_t tSm[kMaxDims];        // staging (shared memory) stride, elements: tCin + padding
     int32_t tCout[kMaxDims];      // c(q_i, M_mk^O): cumulative volume, tile-output order
     int32_t tOutOrder[kMaxDims];  // tile dims in output order (indices into the above)
     int64_t tSin[kMaxDims];       // c(q_i, I): global input stride

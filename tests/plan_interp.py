@@ -12,7 +12,7 @@ def interpret_tile_plan(j, words):
     V, a = t["V"], len(t["ext"])
     ext, cin, order = t["ext"], t["cin"], t["out_order"]
     sin, sout = t["sin"], t["sout"]
-    pe, pad = t["padEvery"], t["pad"]
+    sm = t["sm"]
     st, sl, sc, se = t["split_tile"], t["split_lane"], t["split_chunk"], t["split_ext"]
     tails = [se[s] - (-(-se[s] // sc[s]) - 1) * sc[s] for s in range(len(st))]
     gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
@@ -31,7 +31,11 @@ def interpret_tile_plan(j, words):
                 if st[s] == i:
                     cs[s] = c
         gin.append(off)
-        pin.append(k + (k // pe) * pad)
+        rem, sp = k, 0
+        for i in range(a):
+            sp += (rem % ext[i]) * sm[i]
+            rem //= ext[i]
+        pin.append(sp)
         cin_s.append(cs)
     assert len(set(pin)) == V and max(pin) < t["sbuf"]
     gout, psh, cout_s = [], [], []
@@ -41,12 +45,12 @@ def interpret_tile_plan(j, words):
             c = rem % ext[ti]
             rem //= ext[ti]
             off += c * sout[ti]
-            sh += c * cin[ti]
+            sh += c * sm[ti]
             for s in range(len(st)):
                 if st[s] == ti:
                     cs[s] = c
         gout.append(off)
-        psh.append(sh + (sh // pe) * pad)
+        psh.append(sh)
         cout_s.append(cs)
     for tile in range(t["nTiles"]):
         q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
