@@ -121,10 +121,53 @@ def sweep_cps(n):
         torch.cuda.empty_cache()
 
 
+def calib_cases():
+    cs = wl.s2_ttc()[2::5]
+    s3 = [c for c in wl.s3_random(per_cell=1, set2_random=0)]
+    cs += [c for c in s3 if c.rank >= 4][::5]
+    cs += [c for c in wl.s3_random(per_cell=0, set2_random=2) if c.tags[0] == "SET2"][::2]
+    return cs
+
+
+def sweep_calib():
+    """Forced generic-tile geometries (run targets x threads) per case, for
+    fitting the planner's model."""
+    for c in calib_cases():
+        j0 = tt.plan_offline(c.dims, c.perm, c.esize)
+        if j0["kernel"] != "tile":
+            continue
+        x, ref, p0 = setup(c)
+        print(json.dumps({"case": c.name, "dims": c.dims, "perm": c.perm, "esize": c.esize,
+                          "memcpy_gbs": memcpy_gbs(x), "auto": measure(c, x, ref)}), flush=True)
+        E = c.esize
+        seen = set()
+        for rb_in in (64, 128, 256, 512, 1024):
+            for rb_out in (64, 128, 256, 512, 1024):
+                for thr in (0, 128, 256, 512):
+                    try:
+                        j = tt.plan_offline(c.dims, c.perm, E, kernel=tt.KERNEL_TILE,
+                                            run_in=max(2, rb_in // E), run_out=max(2, rb_out // E),
+                                            threads=thr)
+                    except tt.TTError:
+                        continue
+                    key = (tuple(j["tile"]["ext"]), j["threads"], j["nreg"])
+                    if key in seen:
+                        continue
+                    seen.add(key)
+                    r = measure(c, x, ref, kernel=tt.KERNEL_TILE, run_in=max(2, rb_in // E),
+                                run_out=max(2, rb_out // E), threads=thr)
+                    print(json.dumps({"case": c.name, "rin": rb_in, "rout": rb_out, "thr": thr,
+                                      "nreg": j["nreg"], **r}), flush=True)
+        del x, ref
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "t2d":
         sweep_t2d()
+    elif mode == "calib":
+        sweep_calib()
     elif mode == "cps":
         sweep_cps(int(sys.argv[2]) if len(sys.argv) > 2 else 8)
     else:
