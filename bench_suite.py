@@ -80,14 +80,17 @@ def verify(case, x, y, mode):
     return bool(ok)
 
 
-def run_case(case, reps, vmode, memcpy_cache, opts):
+def run_case(case, reps, vmode, memcpy_cache, opts, measured=False):
     td = torch.int32 if case.esize == 4 else torch.int64
     g = torch.Generator(device="cuda")
     g.manual_seed(case.seed & 0x7FFFFFFFFFFFFFFF)
     x = torch.randint(-2**31, 2**31 - 1, (case.vol,), dtype=td, device="cuda", generator=g)
     y = torch.empty_like(x)
     t0 = time.perf_counter()
-    plan = tt.Plan(case.dims, case.perm, case.esize, **opts)
+    if measured:
+        plan = tt.Plan(case.dims, case.perm, case.esize, measure=(x, y))
+    else:
+        plan = tt.Plan(case.dims, case.perm, case.esize, **opts)
     plan_us = (time.perf_counter() - t0) * 1e6
     ms, mn, mx = event_ms(lambda: plan.execute(x, y), reps)
     torch.cuda.synchronize()
@@ -107,14 +110,16 @@ def run_case(case, reps, vmode, memcpy_cache, opts):
             "gbs": round(gbs, 1), "memcpy_gbs": round(2 * case.nbytes / mc / 1e6, 1),
             "frac_memcpy": round(mc / ms, 4), "plan_us": round(plan_us, 1),
             "pred_us": round(d["predicted_us"], 1), "verified": ok,
-            "tile": d.get("tile", {}).get("ext"), "threads": d["threads"], "grid": d["grid"]}
+            "tile": d.get("tile", {}).get("ext"), "threads": d["threads"], "grid": d["grid"],
+            "plan": "measured" if measured else "heuristic", "measured": d.get("measured")}
 
 
 def summarize(rows):
     out = {}
     by_suite = {}
     for r in rows:
-        by_suite.setdefault(r["case"].split("_")[0], []).append(r)
+        key = r["case"].split("_")[0] + ("@measured" if r["case"].endswith("@measured") else "")
+        by_suite.setdefault(key, []).append(r)
     for s, rs in by_suite.items():
         f = sorted(r["frac_memcpy"] for r in rs)
         g = sorted(r["gbs"] for r in rs)
@@ -140,6 +145,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--plan", default="heuristic", choices=["heuristic", "measured", "both"])
     a = ap.parse_args()
     cases = cases_for(a.suite.split(","), a.per_cell)
     if a.limit:
@@ -151,13 +157,17 @@ def main():
         opts["ctas_per_sm"] = a.ctas_per_sm
     rows, cache = [], {}
     f = open(a.out, "w") if a.out else None
+    modes = {"heuristic": [False], "measured": [True], "both": [False, True]}[a.plan]
     for c in cases:
-        r = run_case(c, a.reps, a.verify, cache, opts)
-        rows.append(r)
-        line = json.dumps(r)
-        print(line, flush=True)
-        if f:
-            f.write(line + "\n")
+        for m in modes:
+            r = run_case(c, a.reps, a.verify, cache, opts, measured=m)
+            if m:
+                r["case"] = r["case"] + "@measured"
+            rows.append(r)
+            line = json.dumps(r)
+            print(line, flush=True)
+            if f:
+                f.write(line + "\n")
         torch.cuda.empty_cache()
     summ = summarize(rows)
     print(json.dumps({"summary": summ}), flush=True)

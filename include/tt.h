@@ -125,6 +125,19 @@ tt_status_t tt_plan_ex(tt_plan_t* plan, int rank, const int64_t* dims, const int
                        size_t elem_size, tt_stream_t stream, const tt_plan_options_t* opts);
 
 /*
+ * tt_plan_measure -- measurement-based plan selection ("measure the
+ * runtime of tensor transpose execution for each plan and pick the fastest
+ * one").  Builds the heuristic plan and up to max_candidates-1 alternatives
+ * (kernel family, tile geometry, grid size; 0 = all), runs each on the device
+ * buffers in/out (out is overwritten; in is only read) on `stream`, times
+ * them with CUDA events and keeps the fastest.  Synchronises `stream`.
+ * tt_plan_describe reports "measured": {candidates, best_ms, heuristic_ms}.
+ */
+tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, tt_stream_t stream, const void* in, void* out,
+                            int max_candidates);
+
+/*
  * tt_plan_offline -- plan for a DESCRIBED device without touching the CUDA
  * runtime (works on a machine with no GPU).  The plan can be described but
  * tt_execute on it returns TT_INVALID_DEVICE.  props may be NULL (B200 values).

@@ -66,6 +66,8 @@ def _load():
                        ctypes.POINTER(PlanOptions)],
         "tt_plan_offline": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t,
                             ctypes.POINTER(DeviceProps), ctypes.POINTER(PlanOptions)],
+        "tt_plan_measure": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, vp, vp, vp,
+                            ctypes.c_int],
         "tt_execute": [vp, vp, vp],
         "tt_execute_host": [vp, vp, vp, vp, vp],
         "tt_destroy": [vp],
@@ -135,16 +137,26 @@ class Plan:
     """plan -> execute -> destroy.  ``dims`` stride-1 first,
     ``perm[j]`` = input dim of output dim j, ``elem_size`` 4 or 8."""
 
-    def __init__(self, dims, perm, elem_size: int, stream=None, **opts):
+    def __init__(self, dims, perm, elem_size: int, stream=None, measure=None,
+                 max_candidates: int = 0, **opts):
+        """``measure=(inp, out)``: measurement-based selection on those device
+        buffers (tt_plan_measure) instead of the heuristic."""
         n, d, p = _arrays(dims, perm)
         self.dims, self.perm, self.elem_size = tuple(dims), tuple(perm), int(elem_size)
         self.vol = 1
         for x in self.dims:
             self.vol *= int(x)
         h = ctypes.c_void_p()
-        o = _options(**opts)
-        _check(lib.tt_plan_ex(ctypes.byref(h), n, d, p, self.elem_size,
-                              _stream_handle(stream), ctypes.byref(o)), "tt_plan")
+        if measure is not None:
+            if opts:
+                raise ValueError("measured planning takes no planner overrides")
+            _check(lib.tt_plan_measure(ctypes.byref(h), n, d, p, self.elem_size,
+                                       _stream_handle(stream), _ptr(measure[0]), _ptr(measure[1]),
+                                       int(max_candidates)), "tt_plan_measure")
+        else:
+            o = _options(**opts)
+            _check(lib.tt_plan_ex(ctypes.byref(h), n, d, p, self.elem_size,
+                                  _stream_handle(stream), ctypes.byref(o)), "tt_plan")
         self._h = h
 
     @property

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "tt_internal.h"
 
@@ -45,6 +46,12 @@ tt_status_t query_device(DeviceInfo& dev) {
 tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
                         size_t elem_size, void* stream, const DeviceInfo& dev,
                         const tt_plan_options_t* opts, OccupancyFn occ) {
+    return create_plan_w(out, rank, dims, perm, elem_size, stream, dev, opts, occ, false);
+}
+
+tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* perm,
+                          size_t elem_size, void* stream, const DeviceInfo& dev,
+                          const tt_plan_options_t* opts, OccupancyFn occ, bool widenForced) {
     if (out == nullptr) return TT_INVALID_PARAMETER;
     *out = nullptr;
     tt_status_t st = validate(rank, dims, perm, elem_size);
@@ -59,8 +66,9 @@ tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* pe
     const bool fuse = !(opts && opts->no_fusion);
     p->prob = normalize(rank, dims, perm, (int)elem_size, fuse);
     // element widening (planner.cpp widen_factor) unless geometry is forced
-    const bool forcedGeometry = opts && (opts->kernel || opts->run_in || opts->run_out ||
-                                         opts->threads || opts->no_widen);
+    const bool forcedGeometry = opts && (opts->no_widen ||
+                                         (!widenForced && (opts->kernel || opts->run_in ||
+                                                           opts->run_out || opts->threads)));
     const int k = forcedGeometry ? 1 : widen_factor(p->prob);
     if (k > 1) {
         Plan* nar = new (std::nothrow) Plan();
@@ -143,6 +151,101 @@ tt_status_t tt_plan_ex(tt_plan_t* plan, int rank, const int64_t* dims, const int
 tt_status_t tt_plan(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
                     size_t elem_size, tt_stream_t stream) {
     return tt_plan_ex(plan, rank, dims, perm, elem_size, stream, nullptr);
+}
+
+// Measurement-based plan selection ("measure the runtime of tensor
+// transpose execution for each plan and pick the fastest one"): the
+// heuristic plan plus alternative kernels / tile geometries / grid sizes are
+// each run on (in, out) and timed with CUDA events on the plan's stream.
+tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, tt_stream_t stream, const void* in, void* out,
+                            int max_candidates) {
+    if (plan == nullptr) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    tt_status_t st = validate(rank, dims, perm, elem_size);
+    if (st != TT_SUCCESS) return st;
+    if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
+    DeviceInfo dev;
+    st = query_device(dev);
+    if (st != TT_SUCCESS) return st;
+    Plan* heur = nullptr;
+    st = create_plan(&heur, rank, dims, perm, elem_size, stream, dev, nullptr, &cuda_occupancy);
+    if (st != TT_SUCCESS) return st;
+
+    // candidate options (elements of the widened problem when it widens)
+    std::vector<tt_plan_options_t> vars;
+    auto opt = [](int kernel, int a, int b, int threads, int cps, int order) {
+        tt_plan_options_t o;
+        std::memset(&o, 0, sizeof(o));
+        o.kernel = kernel; o.run_in = a; o.run_out = b; o.threads = threads;
+        o.ctas_per_sm = cps; o.grid_order = order;
+        return o;
+    };
+    const Problem& hp = heur->prob;
+    const int W = hp.esize;
+    if (hp.n >= 2 && hp.p[0] != 0) {
+        const int tiles4[4][2] = {{64, 128}, {128, 64}, {128, 128}, {64, 64}};
+        const int tiles8[4][2] = {{64, 64}, {64, 32}, {32, 64}, {32, 32}};
+        for (int t = 0; t < 4; ++t)
+            for (int cps : {1, 2, 3})
+                vars.push_back(W == 4 ? opt(TT_KERNEL_TILED2D, tiles4[t][0], tiles4[t][1], 0, cps, 2)
+                                      : opt(TT_KERNEL_TILED2D, tiles8[t][0], tiles8[t][1], 0, cps, 2));
+    }
+    if (hp.n >= 2 && hp.p[0] == 0)
+        for (int cps : {2, 4, 8}) vars.push_back(opt(TT_KERNEL_ROWCOPY, 0, 0, 0, cps, 0));
+    if (hp.n >= 2)
+        for (int bi : {128, 256, 512, 1024})
+            for (int bo : {128, 256, 512, 1024})
+                vars.push_back(opt(TT_KERNEL_TILE, std::max(2, bi / W), std::max(2, bo / W), 0, 0, 0));
+
+    std::vector<Plan*> cands{heur};
+    std::vector<std::string> keys{describe_json(*heur)};
+    for (const auto& o : vars) {
+        if (max_candidates > 0 && (int)cands.size() >= max_candidates) break;
+        Plan* c = nullptr;
+        if (create_plan_w(&c, rank, dims, perm, elem_size, stream, dev, &o, &cuda_occupancy, true) !=
+            TT_SUCCESS)
+            continue;
+        std::string k = describe_json(*c);
+        bool dup = false;
+        for (const auto& kk : keys) dup |= kk == k;
+        if (dup) { destroy_plan(c); continue; }
+        cands.push_back(c);
+        keys.push_back(k);
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        cudaGetLastError();
+        for (Plan* c : cands) destroy_plan(c);
+        return TT_CUDA_ERROR;
+    }
+    int best = 0;
+    float bestMs = 1e30f, heurMs = 0.f;
+    for (size_t i = 0; i < cands.size(); ++i) {
+        if (launch_plan(*cands[i], in, out, stream) != 0) { cudaGetLastError(); continue; }
+        cudaEventRecord(e0, s);
+        const int reps = 3;
+        for (int r = 0; r < reps; ++r) launch_plan(*cands[i], in, out, stream);
+        cudaEventRecord(e1, s);
+        if (cudaEventSynchronize(e1) != cudaSuccess) { cudaGetLastError(); continue; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= reps;
+        if (i == 0) heurMs = ms;
+        if (ms < bestMs) { bestMs = ms; best = (int)i; }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (size_t i = 0; i < cands.size(); ++i)
+        if ((int)i != best) destroy_plan(cands[i]);
+    Plan* p = cands[best];
+    p->measured = true;
+    p->measured_ms = bestMs;
+    p->heuristic_ms = heurMs;
+    p->n_candidates = (int)cands.size();
+    *plan = reinterpret_cast<tt_plan_t>(p);
+    return TT_SUCCESS;
 }
 
 tt_status_t tt_plan_offline(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,

@@ -783,6 +783,9 @@ std::string describe_json(const Plan& plan) {
         o << "}";
     }
     if (plan.narrow) o << ",\"narrow\":" << describe_json(*plan.narrow);
+    if (plan.measured)
+        o << ",\"measured\":{\"candidates\":" << plan.n_candidates << ",\"best_ms\":"
+          << plan.measured_ms << ",\"heuristic_ms\":" << plan.heuristic_ms << "}";
     if (kc.kernel == TT_KERNEL_TILED2D) {
         const Tiled2DParams& t = plan.t2d;
         o << ",\"tiled2d\":{\"TA\":" << kc.tile0 << ",\"TB\":" << kc.tile1 << ",\"nTiles\":"

@@ -151,6 +151,9 @@ struct Plan {
     RowParams row{};
     Tiled2DParams t2d{};
     ShardInfo* shard = nullptr;    // sharded plans only
+    bool measured = false;         // chosen by tt_plan_measure
+    float measured_ms = 0.f, heuristic_ms = 0.f;
+    int n_candidates = 0;
     int widen = 1;                 // words of the fused problem = widen original elements
     Plan* narrow = nullptr;        // un-widened plan, for pointers not aligned to E*widen
     ~Plan();
@@ -175,6 +178,9 @@ tt_status_t query_device(DeviceInfo& dev);
 tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
                         size_t elem_size, void* stream, const DeviceInfo& dev,
                         const tt_plan_options_t* opts, OccupancyFn occ);
+tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* perm,
+                          size_t elem_size, void* stream, const DeviceInfo& dev,
+                          const tt_plan_options_t* opts, OccupancyFn occ, bool widenForced);
 void destroy_plan(Plan* p);
 
 // dist.cu -------------------------------------------------------------------

@@ -288,3 +288,21 @@ def test_permute_torch_matches_torch_semantics():
     for axes in [(3, 2, 1, 0), (0, 2, 1, 3), (1, 3, 0, 2)]:
         y = tt.permute_torch(x, axes)
         assert torch.equal(y, x.permute(*axes).contiguous())
+
+
+def test_measured_planning():
+    """tt_plan_measure: every candidate it may keep is a valid plan; the kept
+    one is bit-exact and reports its measurement."""
+    for dims, perm, esize in [((130, 70), (1, 0), 4), ((37, 29, 11, 4), (2, 0, 3, 1), 8),
+                              ((600, 7, 5), (0, 2, 1), 4), ((5, 3, 2, 4, 7, 6), (4, 0, 5, 2, 3, 1), 4)]:
+        words = wl.random_words(int(np.prod(dims)), esize, 2)
+        x = to_dev(words)
+        y = torch.empty_like(x)
+        plan = tt.Plan(dims, perm, esize, measure=(x, y))
+        d = plan.describe()
+        assert d["measured"]["candidates"] >= 2 and d["measured"]["best_ms"] > 0
+        y.fill_(0)
+        plan.execute(x, y)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y.cpu().numpy().view(words.dtype), orc.permute(dims, perm, words))
+        plan.destroy()
