@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "tt_internal.h"
 
@@ -231,7 +232,7 @@ __device__ __forceinline__ TileBase<I> decode_tile(GridWalker<I>& g, I t) { retu
 // ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
 // cover the tile's `need`.
 template <typename W, int NREG, typename I>
-__global__ void __launch_bounds__(512, (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2))
+__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, (NREG >= 16 ? 2 : (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
 tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -244,7 +245,8 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     // register arrays of P:L155-159).
     I gin[NREG], gout[NREG];
     uint32_t spk[NREG];  // staging byte offsets: load element (low 16 bits), store element (high)
-    uint32_t flags = 0;
+    typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
+    FlagT flags = 0;
     const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
     const bool allSlots = p.V == NT * NREG;  // CTA-uniform
 #pragma unroll
@@ -284,7 +286,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             }
             gout[r] = off;
             spk[r] |= ((uint32_t)sh * (uint32_t)sizeof(W)) << 16;
-            flags |= f << (4 * r);
+            flags |= (FlagT)f << (4 * r);
         }
     }
 
@@ -537,6 +539,7 @@ static const void* pick_tile(int esize, int nreg, bool idx64) {
         case 2: return tile_fn<W, 2, I>();          \
         case 4: return tile_fn<W, 4, I>();          \
         case 8: return tile_fn<W, 8, I>();          \
+        case 16: return tile_fn<W, 16, I>();        \
         default: return nullptr;                    \
     }
     if (esize == 4) {

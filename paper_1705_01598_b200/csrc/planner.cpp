@@ -379,30 +379,6 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         c.runOut = std::min<int64_t>(r, tp.V);
     }
 
-    // threads x slots: NT*NREG >= V, NREG in {1,2,4,8}, NT multiple of 32
-    {
-        int bestT = 0, bestR = 0;
-        long bestWaste = 1L << 40;
-        for (int R : {8, 4, 2, 1}) {
-            if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
-            int T = (int)ceil_div(tp.V, R);
-            T = (int)ceil_div(T, 32) * 32;
-            if (forceThreads) {
-                if ((long)forceThreads * R < tp.V) continue;
-                T = forceThreads;
-            }
-            if (T > 512) continue;  // kernels.cu launch bounds
-            if (T < 64 && R > 1) continue;
-            long waste = (long)T * R - tp.V;
-            // prefer 128..512 threads, then least waste
-            long pen = waste + ((T < 128 || T > 512) ? tp.V : 0);
-            if (pen < bestWaste) { bestWaste = pen; bestT = T; bestR = R; }
-        }
-        if (bestT == 0) return c;
-        c.threads = bestT;
-        c.nreg = bestR;
-    }
-
     // smem footprint with the worst-case padding (layout chosen for the winner)
     {
         int64_t words = tp.V + tp.V / 4 + 64;  // choose_smem's padding cap
@@ -410,7 +386,8 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         if (c.smem > dev.max_smem_per_block) return c;
     }
 
-    // model: DRAM sectors of full tiles + slot issue + per-tile overhead
+    // model: DRAM sectors of full tiles + slot issue + per-tile overhead,
+    // minimised over the launch shape (threads x slots, NT*NREG >= V)
     {
         const double E = pr.esize;
         int64_t aIn = 256;  // allocations are at least 256-byte aligned
@@ -434,20 +411,39 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         c.dram_eff = usefulSec / modelSec;
         // slots of ragged tiles are partly idle but still issued
         const double bytes = (double)tp.nTiles * modelSec * model::kSector;
-        // memory-level parallelism: bytes of loads in flight per SM (the
-        // B200 analogue of the paper's MWP/MLP terms)
-        const OccQuery oq{TT_KERNEL_TILE, pr.esize, c.nreg, 1, c.threads, c.smem,
-                          pr.vol >= (int64_t(1) << 31), 0, 0};
-        const double inflight = (double)estimate_occupancy(oq, dev) * c.threads * c.nreg * E;
-        const double mlp = std::min(1.0, inflight / model::kInflightBytes);
-        const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
-        const double warps = c.threads / 32.0;
-        const double perTile = warps * ((pr.vol >= (int64_t(1) << 31) ? model::kTileInstr64
-                                                                      : model::kTileInstr) +
-                                        c.nreg * model::kSlotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
-        const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
-                               std::max(1, dev.num_sms) / model::kClockMHz;
-        c.cost_us = std::max(t_mem, t_issue) + 0.25 * std::min(t_mem, t_issue) + model::kLaunchUs;
+        const bool idx64 = pr.vol >= (int64_t(1) << 31);
+        for (int R : {16, 8, 4, 2, 1}) {
+            if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
+            // 16 slots: 256-thread CTAs, 32-bit indices only (kernels.cu launch bounds)
+            if (R == 16 && idx64) continue;
+            int T = (int)ceil_div(tp.V, R);
+            T = (int)ceil_div(T, 32) * 32;
+            if (forceThreads) {
+                if ((long)forceThreads * R < tp.V) continue;
+                T = forceThreads;
+            }
+            if (T > (R >= 16 ? 256 : 512)) continue;  // kernels.cu launch bounds
+            if (T < 64 && R > 1) continue;
+            // memory-level parallelism: bytes of loads in flight per SM (the
+            // B200 analogue of the paper's MWP/MLP terms)
+            const OccQuery oq{TT_KERNEL_TILE, pr.esize, R, 1, T, c.smem, idx64, 0, 0};
+            const double inflight = (double)estimate_occupancy(oq, dev) * T * R * E;
+            const double mlp = std::min(1.0, inflight / model::kInflightBytes);
+            const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
+            const double warps = T / 32.0;
+            const double perTile = warps * ((idx64 ? model::kTileInstr64 : model::kTileInstr) +
+                                            R * model::kSlotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
+            const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
+                                   std::max(1, dev.num_sms) / model::kClockMHz;
+            const double cost =
+                std::max(t_mem, t_issue) + 0.25 * std::min(t_mem, t_issue) + model::kLaunchUs;
+            if (c.threads == 0 || cost < c.cost_us) {
+                c.cost_us = cost;
+                c.threads = T;
+                c.nreg = R;
+            }
+        }
+        if (c.threads == 0) return c;
     }
     c.ok = true;
     return c;
@@ -580,7 +576,7 @@ int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     int regs;
     if (q.kernel == TT_KERNEL_TILE) {
         const int r8 = q.esize == 8 ? 96 : 64;
-        regs = q.nreg >= 8 ? r8 : q.nreg >= 4 ? 56 : q.nreg >= 2 ? 52 : 44;
+        regs = q.nreg >= 16 ? 128 : q.nreg >= 8 ? r8 : q.nreg >= 4 ? 56 : q.nreg >= 2 ? 52 : 44;
         if (q.idx64) regs += 16;
     } else {
         regs = 64;
