@@ -525,6 +525,84 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
 }
 
 // ---------------------------------------------------------------------------
+// scalar 2-D tiled transpose: the Tiled class when the two
+// fastest dims do not allow vectors (odd extents).  256 threads = 32 lanes
+// along A x 8 along B; each thread moves MA x MB elements of a TA = 32*MA by
+// TB = 8*MB tile through shared memory rows of TB+1 elements -- the paper's
+// L x (L+1) padding, conflict-free for both the staging store
+// (lanes along A) and the transposed read (lanes along B).
+// ---------------------------------------------------------------------------
+template <typename W, int MA, int MB, typename I>
+__global__ void __launch_bounds__(256)
+tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in, W* __restrict__ out) {
+    constexpr int TA = 32 * MA;
+    constexpr int TB = 8 * MB;
+    constexpr int RS = TB + 1;                       // padded row stride (elements)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    constexpr uint32_t BUF = (uint32_t)(TA * RS * sizeof(W));
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int wid = tid >> 5;                        // 8 warps
+
+    const I nTiles = (I)p.nTiles;
+    I t = (I)blockIdx.x;
+    if (t >= nTiles) return;
+    const I stride = (I)gridDim.x;
+    const I sInB = (I)p.sInB;
+    const I sOutA = (I)p.sOutA;
+
+    W v[MB][MA];  // element (a = lane + 32 ma, b = wid + 8 mb)
+    auto load = [&](const TileBase<I>& tb) {
+        const int limA = (tb.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (tb.need & 2u) ? p.splitTail[1] : TB;
+        const W* __restrict__ src = opaque(in + tb.in);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int b = wid + 8 * mb;
+#pragma unroll
+            for (int ma = 0; ma < MA; ++ma) {
+                const int a = lane + 32 * ma;
+                if (a < limA && b < limB) v[mb][ma] = ldg_(src + ((I)b * sInB + a));
+            }
+        }
+    };
+    GridWalker<I> walk(p, lane);
+    TileBase<I> cur = walk.seek(t);
+    load(cur);
+    uint32_t sb = sm0;
+    for (; t < nTiles; t += stride) {
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int ma = 0; ma < MA; ++ma)
+                sts(sb + (uint32_t)(((lane + 32 * ma) * RS + wid + 8 * mb) * sizeof(W)), v[mb][ma]);
+        __syncthreads();
+        const TileBase<I> now = cur;
+        const I tn = t + stride;
+        if (tn < nTiles) {
+            cur = walk.seek(tn);
+            load(cur);
+        }
+        const int limA = (now.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (now.need & 2u) ? p.splitTail[1] : TB;
+        W* __restrict__ dst = opaque(out + now.out);
+        // output row a = wid + 8 j, elements b = lane + 32 u
+#pragma unroll
+        for (int j = 0; j < TA / 8; ++j) {
+            const int a = wid + 8 * j;
+#pragma unroll
+            for (int u = 0; u < TB / 32; ++u) {
+                const int b = lane + 32 * u;
+                if (a < limA && b < limB)
+                    dst[(I)a * sOutA + b] = lds<W>(sb + (uint32_t)((a * RS + b) * sizeof(W)));
+            }
+        }
+        sb = (sb == sm0) ? sm0 + BUF : sm0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
 template <typename W, int NREG, typename I>
@@ -577,7 +655,22 @@ static const void* t2d_fn(bool idx64) {
                  : (const void*)&tiled2d_kernel<W, VW, MA, MB, uint32_t>;
 }
 
+template <typename W, int MA, int MB>
+static const void* t2ds_fn(bool idx64) {
+    return idx64 ? (const void*)&tiled2d_s_kernel<W, MA, MB, int64_t>
+                 : (const void*)&tiled2d_s_kernel<W, MA, MB, uint32_t>;
+}
+
 static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) {
+    if (vec == 1) {  // scalar 2-D kernel: TA = 32*MA, TB = 8*MB
+        if (esize == 4 && ta == 64 && tb == 64) return t2ds_fn<uint32_t, 2, 8>(idx64);
+        if (esize == 4 && ta == 128 && tb == 64) return t2ds_fn<uint32_t, 4, 8>(idx64);
+        if (esize == 4 && ta == 64 && tb == 128) return t2ds_fn<uint32_t, 2, 16>(idx64);
+        if (esize == 8 && ta == 64 && tb == 64) return t2ds_fn<uint64_t, 2, 8>(idx64);
+        if (esize == 8 && ta == 32 && tb == 64) return t2ds_fn<uint64_t, 1, 8>(idx64);
+        if (esize == 8 && ta == 64 && tb == 32) return t2ds_fn<uint64_t, 2, 4>(idx64);
+        return nullptr;
+    }
     if (esize == 4 && vec == 4) {
         if (ta == 64 && tb == 64) return t2d_fn<uint32_t, 4, 1, 1>(idx64);
         if (ta == 128 && tb == 64) return t2d_fn<uint32_t, 4, 2, 1>(idx64);

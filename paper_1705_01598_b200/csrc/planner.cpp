@@ -501,6 +501,10 @@ static void choose_smem(TileParams& tp, int esize) {
 // Instantiated tiles (kernels.cu pick_tiled2d): 4-byte VW=4: {64,128}^2;
 // 4-byte VW=2: 32x64, 64x64; 8-byte VW=2: {32,64}^2.
 static bool tiled2d_tile_ok(int esize, int vec, int ta, int tb) {
+    if (vec == 1) {  // scalar kernel instantiations
+        if (esize == 4) return (ta == 64 && tb == 64) || (ta == 128 && tb == 64) || (ta == 64 && tb == 128);
+        return (ta == 64 && tb == 64) || (ta == 32 && tb == 64) || (ta == 64 && tb == 32);
+    }
     if (esize == 4 && vec == 4) return (ta == 64 || ta == 128) && (tb == 64 || tb == 128);
     if (esize == 4 && vec == 2) return (ta == 32 || ta == 64) && tb == 64;
     if (esize == 8 && vec == 2) return (ta == 32 || ta == 64) && (tb == 32 || tb == 64);
@@ -519,12 +523,13 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     } else if (dA % 2 == 0 && dB % 2 == 0) {
         vec = 2;
     }
-    if (vec == 0) return false;
+    if (vec == 0) vec = 1;  // scalar 2-D kernel (padded staging)
     // default tiles from the B200 calibration sweep (tools/sweep.py t2d,
     // profiles/round1_sweep_t2d.md): 64 x 128 for 4-byte words with 16-byte
     // vectors, 64 x 64 otherwise; two CTAs per SM, B-chunks fastest.
     if (pr.esize == 4) { ta = 64; tb = vec == 4 ? 128 : 64; }
     else { ta = 64; tb = 64; }
+    if (vec == 1) { ta = 64; tb = 64; }
     if (wantA || wantB) {
         if (wantA) ta = wantA;
         if (wantB) tb = wantB;
@@ -712,13 +717,13 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.tile0 = ta2d;
         kc.tile1 = tb2d;
         kc.threads = 256;
-        kc.smem = 2 * ta2d * tb2d * E;
+        kc.smem = vec2d == 1 ? 2 * ta2d * (tb2d + 1) * E : 2 * ta2d * tb2d * E;
         OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64, ta2d, tb2d};
         int occ2 = occ ? occ(q2, dev) : 0;
         if (occ2 <= 0) occ2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
         // two CTAs per SM measured best (fewer concurrent tiles, whole DRAM
         // rows); never more than fit, so the persistent grid is one wave
-        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(2, occ2);
+        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(vec2d == 1 ? 4 : 2, occ2);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
         const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
         kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;

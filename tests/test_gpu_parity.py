@@ -123,7 +123,10 @@ def test_forced_tiled2d(esize):
     """The vectorised 2-D kernel on full, ragged and batched tiles."""
     shapes = [((64, 64), (1, 0)), ((132, 36), (1, 0)), ((6, 10, 7), (1, 2, 0)),
               ((34, 3, 98), (2, 1, 0)), ((8, 5, 12, 3), (2, 3, 0, 1)), ((70, 50), (1, 0)),
-              ((1000, 998), (1, 0)), ((36, 7, 44, 3), (2, 0, 3, 1)), ((2, 4, 6), (2, 0, 1))]
+              ((1000, 998), (1, 0)), ((36, 7, 44, 3), (2, 0, 3, 1)), ((2, 4, 6), (2, 0, 1)),
+              # odd extents: scalar 2-D kernel with padded staging
+              ((67, 45), (1, 0)), ((13, 3, 67), (2, 1, 0)), ((1001, 999), (1, 0)),
+              ((129, 5, 65), (2, 0, 1))]
     tiles = [(64, 64), (128, 64), (64, 128), (128, 128), (32, 64)] if esize == 4 else \
         [(32, 32), (64, 32), (32, 64), (64, 64)]
     for dims, perm in shapes:

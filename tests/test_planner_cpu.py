@@ -147,13 +147,23 @@ def test_tiled2d_geometry(dims, perm, esize):
             np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), want)
 
 
-def test_tiled2d_rejects_odd_or_unchanged():
-    with pytest.raises(tt.TTError):
-        tt.plan_offline((13, 64), (1, 0), 4, kernel=tt.KERNEL_TILED2D)
-    with pytest.raises(tt.TTError):
+def test_tiled2d_vector_width_and_rejections():
+    # odd extents take the scalar 2-D kernel (vec 1), even ones vectors
+    assert tt.plan_offline((13, 64), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 1
+    assert tt.plan_offline((64, 63), (1, 0), 8, kernel=tt.KERNEL_TILED2D)["vec"] == 1
+    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 2
+    assert tt.plan_offline((64, 60), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 4
+    with pytest.raises(tt.TTError):   # fastest dim unchanged: not the Tiled class
         tt.plan_offline((64, 8, 8), (0, 2, 1), 4, kernel=tt.KERNEL_TILED2D)
-    with pytest.raises(tt.TTError):
-        tt.plan_offline((64, 63), (1, 0), 8, kernel=tt.KERNEL_TILED2D)
+    with pytest.raises(tt.TTError):   # tile not instantiated for the scalar kernel
+        tt.plan_offline((13, 64), (1, 0), 4, kernel=tt.KERNEL_TILED2D, run_in=32, run_out=32)
+    for dims, e in [((13, 67), 4), ((65, 63), 8), ((129, 3, 67), 4)]:
+        perm = (1, 0) if len(dims) == 2 else (2, 1, 0)
+        j = tt.plan_offline(dims, perm, e, kernel=tt.KERNEL_TILED2D)
+        words = wl.random_words(int(np.prod(dims)), e, 4)
+        fj = dict(j)
+        fj["dims"] = j["fused"]["dims"]
+        np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), orc.permute(dims, perm, words))
 
 
 @pytest.mark.parametrize("run", [(2, 2), (4, 16), (16, 4), (64, 64), (3, 5)])
