@@ -220,10 +220,45 @@ struct GridWalker {
     }
 };
 
-// Stateless Algorithm-1 decode (used by the 2-D kernel's interleaved tile
-// order); per-lane grid values come from the walker's registers.
-template <typename I>
-__device__ __forceinline__ TileBase<I> decode_tile(GridWalker<I>& g, I t) { return g.seek(t); }
+// Stateless Algorithm-1 decode for the 2-D kernels' interleaved tile order:
+// each lane reads its grid dim's values from the parameter block per tile.
+// (Keeping them in registers, as the walker does, measured 3.5 % slower on
+// S1: it raises the 2-D kernels' register count and delays their loads;
+// A/B in one process, tools/ab_lib.py.)
+template <typename I, typename P>
+__device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
+    I vin = 0, vout = 0;
+    bool ragged = false;
+    if (lane < p.h) {
+        I q;
+        if constexpr (sizeof(I) == 4) {
+            const uint32_t q1 = fast_div((uint32_t)t, p.gMC[lane], p.gLC[lane]);
+            const uint32_t q2 = fast_div(q1, p.gMD[lane], p.gLD[lane]);
+            q = (I)(q1 - q2 * (uint32_t)p.gD[lane]);
+        } else {
+            q = (t / (I)p.gC[lane]) % (I)p.gD[lane];
+        }
+        vin = q * (I)p.gSin[lane];
+        vout = q * (I)p.gSout[lane];
+        ragged = (q == (I)p.gD[lane] - 1) &&
+                 ((p.nSplit > 0 && lane == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) ||
+                  (p.nSplit > 1 && lane == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        vin += __shfl_xor_sync(0xffffffffu, vin, o);
+        vout += __shfl_xor_sync(0xffffffffu, vout, o);
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, ragged);
+    uint32_t need = 0;
+    if (p.nSplit > 0) need |= (bal >> p.splitLane[0]) & 1u;
+    if (p.nSplit > 1) need |= ((bal >> p.splitLane[1]) & 1u) << 1;
+    TileBase<I> b;
+    b.in = vin;
+    b.out = vout;
+    b.need = need;
+    return b;
+}
 
 // Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
 // (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
@@ -479,8 +514,7 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
         }
     };
 
-    GridWalker<I> walk(p, lane);
-    TileBase<I> cur = walk.seek(t);
+    TileBase<I> cur = decode_tile<I>(p, t, lane);
     load(cur);
     int buf = 0;
     for (; t < nTiles; t += stride) {
@@ -505,7 +539,7 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
         const TileBase<I> now = cur;
         const I tn = t + stride;
         if (tn < nTiles) {
-            cur = walk.seek(tn);
+            cur = decode_tile<I>(p, tn, lane);
             load(cur);
         }
         const int limA = (now.need & 1u) ? p.splitTail[0] : TA;
@@ -567,8 +601,7 @@ tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ 
             }
         }
     };
-    GridWalker<I> walk(p, lane);
-    TileBase<I> cur = walk.seek(t);
+    TileBase<I> cur = decode_tile<I>(p, t, lane);
     load(cur);
     uint32_t sb = sm0;
     for (; t < nTiles; t += stride) {
@@ -581,7 +614,7 @@ tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ 
         const TileBase<I> now = cur;
         const I tn = t + stride;
         if (tn < nTiles) {
-            cur = walk.seek(tn);
+            cur = decode_tile<I>(p, tn, lane);
             load(cur);
         }
         const int limA = (now.need & 1u) ? p.splitTail[0] : TA;
