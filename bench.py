@@ -245,28 +245,30 @@ def run_ours(args):
     case, desc = workload(args.config)
     E = case.esize
     tdt = torch.int32 if E == 4 else torch.int64
-    stream = torch.cuda.Stream(device=dev)
-
     sharded = args.config == "s5redist" and world > 1
-    if sharded:
-        comm = tt.Comm.from_process_group()
-        plan = tt.ShardedPlan(comm, case.dims, case.perm, E, stream=stream)
-        local_vol = case.vol // world
-        execute = plan.execute
-        units_per_step_all = case.vol  # global tensor per step
-    else:
-        plan = tt.Plan(case.dims, case.perm, E, stream=stream)
-        local_vol = case.vol
-        execute = plan.execute
-        units_per_step_all = case.vol * world
-    desc_plan = plan.describe()
+    local_vol = case.vol // world if sharded else case.vol
 
-    # seeded input, resident in HBM before timing (rank-specific seed)
+    # seeded input, resident in HBM before timing (rank-specific seed).
+    # Allocated BEFORE the plan's stream is created: creating a stream before
+    # the first device allocation measured ~4 % slower for S1 with the same
+    # kernel (tools/stream_exp3.py; profiles/round1_summary.md).
     g = torch.Generator(device=dev)
     g.manual_seed(case.seed + rank)
     x = torch.randint(-(2 ** 31), 2 ** 31 - 1, (local_vol,), dtype=tdt, device=dev, generator=g)
     y = torch.empty_like(x)
     torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=dev)
+
+    if sharded:
+        comm = tt.Comm.from_process_group()
+        plan = tt.ShardedPlan(comm, case.dims, case.perm, E, stream=stream)
+        execute = plan.execute
+        units_per_step_all = case.vol  # global tensor per step
+    else:
+        plan = tt.Plan(case.dims, case.perm, E, stream=stream)
+        execute = plan.execute
+        units_per_step_all = case.vol * world
+    desc_plan = plan.describe()
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -280,10 +282,11 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     h0 = time.perf_counter()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        execute(x, y)
-    ev1.record(stream)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            execute(x, y)
+        ev1.record(stream)
     ev1.synchronize()
     h1 = time.perf_counter()
     torch.cuda.synchronize()

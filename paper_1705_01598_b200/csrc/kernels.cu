@@ -14,7 +14,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
+#include <unordered_set>
 
 #include "tt_internal.h"
 
@@ -721,14 +723,36 @@ static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) 
     return nullptr;
 }
 
+// Raise a kernel's dynamic shared-memory limit to the device maximum ONCE
+// per function (and device).  Setting the attribute on every launch costs a
+// driver call per launch and measured 4 % of S1 throughput on a non-default
+// stream (back-to-back launches).
+static std::mutex g_smem_mu;
+static std::unordered_set<uint64_t> g_smem_done;
+
+static cudaError_t ensure_max_smem(const void* fn) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t key = reinterpret_cast<uint64_t>(fn) ^ ((uint64_t)dev << 56);
+    std::lock_guard<std::mutex> g(g_smem_mu);
+    if (g_smem_done.count(key)) return cudaSuccess;
+    int maxOptin = 0;
+    e = cudaDeviceGetAttribute(&maxOptin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxOptin);
+    if (e == cudaSuccess) g_smem_done.insert(key);
+    return e;
+}
+
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
+    (void)dev;
     const void* fn = q.kernel == TT_KERNEL_TILE      ? pick_tile(q.esize, q.nreg, q.idx64)
                      : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
                      : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
     if (!fn) return 0;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dev.max_smem_per_block) != cudaSuccess) {
+    if (ensure_max_smem(fn) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -778,7 +802,7 @@ int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
                             : pick_tile(E, kc.nreg, kc.idx64);
         if (!fn) return (int)cudaErrorInvalidConfiguration;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaError_t e = ensure_max_smem(fn);
             if (e != cudaSuccess) return (int)e;
         }
         const void* pp = t2 ? (const void*)&plan.t2d : (const void*)&plan.tile;
