@@ -8,6 +8,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <algorithm>
 
 #include "tt_internal.h"
 
@@ -96,7 +97,130 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     return TT_SUCCESS;
 }
 
-Plan::~Plan() { delete narrow; }
+// ---------------------------------------------------------------------------
+// Pipelined host path of tt_execute_host: the output is cut into chunks
+// along its OUTERMOST dim (input dim t = perm[n-1]); output chunk q is a
+// contiguous block, and its input is the slab x_t in chunk q -- a strided 2-D
+// region of the host input (width c*S_in[t], pitch d_t*S_in[t]).  Chunk q's
+// H2D (one cudaMemcpy2DAsync), its permutation (a plan of the chunk problem)
+// and its D2H run on three streams linked by events, so the two PCIe
+// directions and the kernels overlap.
+// ---------------------------------------------------------------------------
+struct HostPipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;   // 3 per chunk: in-ready, out-ready, +1 start/end
+    int nchunks = 0;
+    int64_t chunk = 0, tail = 0;
+    Plan* full = nullptr;
+    Plan* last = nullptr;
+    int device = -1;
+    ~HostPipe() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
+        destroy_plan(full);
+        if (last != full) destroy_plan(last);
+    }
+};
+
+static tt_status_t build_pipe(Plan& p) {
+    const int n = p.rank;
+    const int t = p.perm[n - 1];
+    const int64_t dt = p.dims[t];
+    if (dt < 2) return TT_UNSUPPORTED;
+    const int nch = (int)std::min<int64_t>(dt, 8);
+    HostPipe* hp = new (std::nothrow) HostPipe();
+    if (!hp) return TT_INTERNAL_ERROR;
+    hp->device = p.device;
+    hp->chunk = (dt + nch - 1) / nch;
+    hp->nchunks = (int)((dt + hp->chunk - 1) / hp->chunk);
+    hp->tail = dt - (int64_t)(hp->nchunks - 1) * hp->chunk;
+    DeviceInfo dev;
+    if (query_device(dev) != TT_SUCCESS) { delete hp; return TT_CUDA_ERROR; }
+    const int esize = p.prob.esize / p.widen;
+    std::vector<int64_t> cd(p.dims);
+    cd[t] = hp->chunk;
+    if (create_plan(&hp->full, n, cd.data(), p.perm.data(), esize, p.stream, dev, nullptr,
+                    &cuda_occupancy) != TT_SUCCESS) { delete hp; return TT_UNSUPPORTED; }
+    if (hp->tail != hp->chunk) {
+        cd[t] = hp->tail;
+        if (create_plan(&hp->last, n, cd.data(), p.perm.data(), esize, p.stream, dev, nullptr,
+                        &cuda_occupancy) != TT_SUCCESS) { delete hp; return TT_UNSUPPORTED; }
+    } else {
+        hp->last = hp->full;
+    }
+    if (cudaStreamCreateWithFlags(&hp->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&hp->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete hp;
+        return TT_CUDA_ERROR;
+    }
+    hp->ev.assign(2 * hp->nchunks + 2, nullptr);
+    for (auto& e : hp->ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            delete hp;
+            return TT_CUDA_ERROR;
+        }
+    p.pipe = hp;
+    return TT_SUCCESS;
+}
+
+tt_status_t execute_host_pipelined(Plan& p, const void* host_in, void* host_out, void* dev_in,
+                                   void* dev_out) {
+    if (p.pipe == nullptr) {
+        tt_status_t st = build_pipe(p);
+        if (st != TT_SUCCESS) return st;
+    }
+    HostPipe* hp = p.pipe;
+    const int n = p.rank;
+    const int t = p.perm[n - 1];
+    const size_t E = (size_t)(p.prob.esize / p.widen);
+    int64_t sIn = 1;  // input stride of dim t
+    for (int i = 0; i < t; ++i) sIn *= p.dims[i];
+    int64_t vol = 1;
+    for (int i = 0; i < n; ++i) vol *= p.dims[i];
+    const int64_t dt = p.dims[t];
+    const int64_t rows = vol / (dt * sIn);  // product of the dims after t
+    const int64_t outBlock = vol / dt;      // output elements per unit of x_t
+    cudaStream_t main = static_cast<cudaStream_t>(p.stream);
+    cudaEvent_t start = hp->ev[2 * hp->nchunks], done = hp->ev[2 * hp->nchunks + 1];
+    bool ok = cudaEventRecord(start, main) == cudaSuccess &&
+              cudaStreamWaitEvent(hp->h2d, start, 0) == cudaSuccess &&
+              cudaStreamWaitEvent(hp->d2h, start, 0) == cudaSuccess;
+    for (int q = 0; ok && q < hp->nchunks; ++q) {
+        const int64_t c = (q == hp->nchunks - 1) ? hp->tail : hp->chunk;
+        const int64_t x0 = (int64_t)q * hp->chunk;
+        char* dIn = static_cast<char*>(dev_in) + (size_t)(x0 * sIn * rows) * E;
+        const char* hIn = static_cast<const char*>(host_in) + (size_t)(x0 * sIn) * E;
+        ok = cudaMemcpy2DAsync(dIn, (size_t)(c * sIn) * E, hIn, (size_t)(dt * sIn) * E,
+                               (size_t)(c * sIn) * E, (size_t)rows, cudaMemcpyHostToDevice,
+                               hp->h2d) == cudaSuccess &&
+             cudaEventRecord(hp->ev[2 * q], hp->h2d) == cudaSuccess &&
+             cudaStreamWaitEvent(main, hp->ev[2 * q], 0) == cudaSuccess;
+        if (!ok) break;
+        char* dOut = static_cast<char*>(dev_out) + (size_t)(x0 * outBlock) * E;
+        Plan* cp = (q == hp->nchunks - 1) ? hp->last : hp->full;
+        ok = launch_plan(*cp, dIn, dOut, p.stream) == 0 &&
+             cudaEventRecord(hp->ev[2 * q + 1], main) == cudaSuccess &&
+             cudaStreamWaitEvent(hp->d2h, hp->ev[2 * q + 1], 0) == cudaSuccess &&
+             cudaMemcpyAsync(static_cast<char*>(host_out) + (size_t)(x0 * outBlock) * E, dOut,
+                             (size_t)(c * outBlock) * E, cudaMemcpyDeviceToHost, hp->d2h) == cudaSuccess;
+    }
+    ok = ok && cudaEventRecord(done, hp->d2h) == cudaSuccess &&
+         cudaStreamWaitEvent(main, done, 0) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    return TT_SUCCESS;
+}
+
+Plan::~Plan() {
+    delete narrow;
+    delete pipe;
+}
 
 void destroy_plan(Plan* p) {
     if (p == nullptr) return;
@@ -295,6 +419,10 @@ tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out,
     if (p->shard) return TT_INVALID_PLAN;
     const size_t bytes = (size_t)p->prob.vol * (size_t)p->prob.esize;
     cudaStream_t s = static_cast<cudaStream_t>(p->stream);
+    if (bytes >= kPipeMinBytes) {
+        st = execute_host_pipelined(*p, host_in, host_out, dev_in, dev_out);
+        if (st != TT_UNSUPPORTED) return st;
+    }
     if (cudaMemcpyAsync(dev_in, host_in, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         cudaGetLastError();
         return TT_CUDA_ERROR;

@@ -137,6 +137,7 @@ struct OccQuery {
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 
 struct ShardInfo;  // defined in dist.cu
+struct HostPipe;   // defined in api.cu (pipelined tt_execute_host)
 
 struct Plan {
     uint32_t magic = 0x54545054u;  // "TTPT"
@@ -156,6 +157,7 @@ struct Plan {
     int n_candidates = 0;
     int widen = 1;                 // words of the fused problem = widen original elements
     Plan* narrow = nullptr;        // un-widened plan, for pointers not aligned to E*widen
+    HostPipe* pipe = nullptr;      // lazily built by tt_execute_host
     ~Plan();
 };
 
@@ -182,6 +184,9 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
                           size_t elem_size, void* stream, const DeviceInfo& dev,
                           const tt_plan_options_t* opts, OccupancyFn occ, bool widenForced);
 void destroy_plan(Plan* p);
+constexpr size_t kPipeMinBytes = size_t(64) << 20;  // pipeline tt_execute_host above this
+tt_status_t execute_host_pipelined(Plan& p, const void* host_in, void* host_out, void* dev_in,
+                                   void* dev_out);
 
 // dist.cu -------------------------------------------------------------------
 void destroy_shard(ShardInfo* s);
