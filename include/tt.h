@@ -159,8 +159,15 @@ tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out);
 /*
  * tt_execute_host -- end-to-end form: copy host_in (vol*elem_size bytes,
  * preferably pinned) to the device buffer dev_in, permute into dev_out, copy
- * dev_out back to host_out, all enqueued on the plan's stream.  Does not
- * synchronise; the caller synchronises the stream before reading host_out.
+ * dev_out back to host_out, ordered after prior work on the plan's stream
+ * and before later work on it.  Does not synchronise; the caller synchronises
+ * the stream before reading host_out.  Above 64 MB the transfer is pipelined:
+ * the output is cut into chunks along its outermost dimension, each chunk's
+ * input slab is one strided 2-D H2D copy, and chunk H2D / permute / D2H run on
+ * three streams so both PCIe directions and the kernels overlap (dev_in is
+ * used as chunk staging).  A plan's pipeline (two streams, events, chunk
+ * plans) is built on first use and freed by tt_destroy; tt_execute_host must
+ * not run concurrently with itself on one plan.
  */
 tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out,
                             void* dev_in, void* dev_out);
