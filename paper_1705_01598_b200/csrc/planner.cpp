@@ -181,6 +181,8 @@ struct TileCand {
     int threads = 0, nreg = 0;
     double cost_us = 1e30;
     double dram_eff = 0;
+    double secIn = 0, secOut = 0;    // modelled sectors per full tile (read / write)
+    double inflight = 0;             // modelled load bytes in flight per SM
     int smem = 0;
     bool ok = false;
 };
@@ -409,6 +411,8 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
                           ((double)tp.V / c.runIn + (double)tp.V / c.runOut) * model::kRunBytes /
                               model::kSector;
         c.dram_eff = usefulSec / modelSec;
+        c.secIn = secIn;
+        c.secOut = secOut;
         // slots of ragged tiles are partly idle but still issued
         const double bytes = (double)tp.nTiles * modelSec * model::kSector;
         const bool idx64 = pr.vol >= (int64_t(1) << 31);
@@ -441,6 +445,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
                 c.cost_us = cost;
                 c.threads = T;
                 c.nreg = R;
+                c.inflight = inflight;
             }
         }
         if (c.threads == 0) return c;
@@ -695,6 +700,11 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.vec = 1;
     kc.predicted_us = best.cost_us;
     kc.model_dram_eff = best.dram_eff;
+    kc.m_runIn = best.runIn;
+    kc.m_runOut = best.runOut;
+    kc.m_secIn = best.secIn;
+    kc.m_secOut = best.secOut;
+    kc.m_inflight = best.inflight;
     OccQuery q{TT_KERNEL_TILE, E, kc.nreg, 1, kc.threads, kc.smem, kc.idx64, 0, 0};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
@@ -772,6 +782,10 @@ std::string describe_json(const Plan& plan) {
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
       << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
       << ",\"model_dram_eff\":" << kc.model_dram_eff << ",\"widen\":" << plan.widen;
+    if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D)
+        o << ",\"model\":{\"run_in\":" << kc.m_runIn << ",\"run_out\":" << kc.m_runOut
+          << ",\"sec_in\":" << kc.m_secIn << ",\"sec_out\":" << kc.m_secOut
+          << ",\"inflight\":" << kc.m_inflight << "}";
     if (kc.kernel == TT_KERNEL_ROWCOPY) {
         const RowParams& r = plan.row;
         o << ",\"rowcopy\":{\"row\":" << (long long)r.row << ",\"nRows\":" << (long long)r.nRows

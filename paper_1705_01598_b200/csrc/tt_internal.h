@@ -116,6 +116,9 @@ struct KernelChoice {
     int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
+    // model features of the generic tile (describe "model"; calibration)
+    long long m_runIn = 0, m_runOut = 0;
+    double m_secIn = 0, m_secOut = 0, m_inflight = 0;
 };
 
 struct DeviceInfo {

@@ -58,6 +58,8 @@ def measure(case, x, ref, **opts):
     return {"ok": ok, "ms": round(ms, 5), "gbs": round(2 * case.nbytes / ms / 1e6, 1),
             "kernel": d["kernel"], "grid": d["grid"], "threads": d["threads"],
             "ext": d.get("tile", {}).get("ext"), "V": d.get("tile", {}).get("V"),
+            "nTiles": d.get("tile", {}).get("nTiles"), "nreg": d.get("nreg"),
+            "model": d.get("model"), "word": d.get("word_size"),
             "pred_us": d["predicted_us"]}
 
 
@@ -143,7 +145,7 @@ def sweep_calib():
         seen = set()
         for rb_in in (64, 128, 256, 512, 1024):
             for rb_out in (64, 128, 256, 512, 1024):
-                for thr in (0, 128, 256, 512):
+                for thr in (0, 64, 128, 256, 512):
                     try:
                         j = tt.plan_offline(c.dims, c.perm, E, kernel=tt.KERNEL_TILE,
                                             run_in=max(2, rb_in // E), run_out=max(2, rb_out // E),
