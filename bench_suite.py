@@ -144,6 +144,7 @@ def main():
     ap.add_argument("--limit", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--plan", default="heuristic", choices=["heuristic", "measured", "both"])
     a = ap.parse_args()
@@ -155,6 +156,8 @@ def main():
         opts["kernel"] = a.kernel
     if a.ctas_per_sm:
         opts["ctas_per_sm"] = a.ctas_per_sm
+    if a.stages:
+        opts["stages"] = a.stages
     rows, cache = [], {}
     f = open(a.out, "w") if a.out else None
     modes = {"heuristic": [False], "measured": [True], "both": [False, True]}[a.plan]

@@ -94,6 +94,7 @@ typedef struct {
     int no_fusion;       /* 1 = skip dimension fusion / extent-1 removal (debug)   */
     int grid_order;      /* TILED2D tile order: 1 = A-chunks fastest, 2 = B-chunks fastest */
     int no_widen;        /* 1 = never regroup elements of an unchanged fastest dim into wider words */
+    int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

@@ -44,7 +44,7 @@ class PlanOptions(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int), ("run_in", ctypes.c_int), ("run_out", ctypes.c_int),
                 ("threads", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
                 ("no_fusion", ctypes.c_int), ("grid_order", ctypes.c_int),
-                ("no_widen", ctypes.c_int)]
+                ("no_widen", ctypes.c_int), ("stages", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -112,9 +112,9 @@ def _arrays(dims, perm):
 
 
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
-             grid_order=0, no_widen=False):
+             grid_order=0, no_widen=False, stages=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
-                       1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0)
+                       1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages))
 
 
 def _ptr(x) -> int:

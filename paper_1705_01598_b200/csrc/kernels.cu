@@ -262,30 +262,13 @@ __device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
     return b;
 }
 
-// Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
-// (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
-// store element (Eq. 6 through the padded layout).  `flags` holds 4 bits per
-// slot: (load elem inside ragged A-chunk, ... B-chunk, store elem inside
-// ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
-// cover the tile's `need`.
-template <typename W, int NREG, typename I>
-__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, (NREG >= 16 ? 2 : (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
-tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
-    const int tid = threadIdx.x;
-    const int NT = blockDim.x;
-    const int lane = tid & 31;
-
-    // Per-thread loop-invariant minor positions (Eqs. 4-6, P:L105-117; the
-    // register arrays of P:L155-159).
-    I gin[NREG], gout[NREG];
-    uint32_t spk[NREG];  // staging byte offsets: load element (low 16 bits), store element (high)
-    typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
-    FlagT flags = 0;
-    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
-    const bool allSlots = p.V == NT * NREG;  // CTA-uniform
+// Per slot r (tile element k = tid + r*NT): Eq. (4) global input offset,
+// Eq. (5) global output offset, staging byte offsets of the load element and
+// of the store element (Eq. (6) with padded strides), ragged-chunk flags.
+template <typename W, int NREG, typename I, typename FlagT>
+__device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT, int nmine,
+                                            I (&gin)[NREG], I (&gout)[NREG], uint32_t (&spk)[NREG],
+                                            FlagT& flags) {
 #pragma unroll
     for (int r = 0; r < NREG; ++r) {
         gin[r] = 0;
@@ -326,6 +309,34 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             flags |= (FlagT)f << (4 * r);
         }
     }
+
+}
+
+// Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
+// (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
+// store element (Eq. 6 through the padded layout).  `flags` holds 4 bits per
+// slot: (load elem inside ragged A-chunk, ... B-chunk, store elem inside
+// ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
+// cover the tile's `need`.
+template <typename W, int NREG, typename I>
+__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, (NREG >= 16 ? 2 : (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
+tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
+    const int tid = threadIdx.x;
+    const int NT = blockDim.x;
+    const int lane = tid & 31;
+
+    // Per-thread loop-invariant minor positions (Eqs. 4-6, P:L105-117; the
+    // register arrays of P:L155-159).
+    I gin[NREG], gout[NREG];
+    uint32_t spk[NREG];  // staging byte offsets: load element (low 16 bits), store element (high)
+    typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
+    FlagT flags = 0;
+    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    const bool allSlots = p.V == NT * NREG;  // CTA-uniform
+    build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
 
     // contiguous tile range per CTA, walked with the odometer
     const I nTiles = (I)p.nTiles;
@@ -384,6 +395,109 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         // readers (previous tile) all passed this iteration's barrier.
         sb = (sb == sm0) ? sm0 + sbytes : sm0;
     }
+}
+
+// ---------------------------------------------------------------------------
+// generic staged tile, asynchronous-copy pipeline: the loads go straight from
+// global to the staging buffer with cp.async (LDGSTS), no data registers, so
+// S-1 tiles are in flight per CTA (S stages of shared memory) instead of one.
+// Same slot tables, walker and staging layout as tile_kernel.
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void cp_async(uint32_t saddr, const void* g) {
+    if constexpr (N == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr), "l"(g), "n"(N));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <typename W, int NREG, typename I, int S>
+__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, 2)
+tile_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
+    const int tid = threadIdx.x;
+    const int NT = blockDim.x;
+    const int lane = tid & 31;
+
+    I gin[NREG], gout[NREG];
+    uint32_t spk[NREG];
+    typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
+    FlagT flags = 0;
+    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    const bool allSlots = p.V == NT * NREG;
+    build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
+
+    const I nTiles = (I)p.nTiles;
+    const I G = (I)gridDim.x;
+    const I t0 = (I)(((uint64_t)nTiles * blockIdx.x) / G);
+    const I t1 = (I)(((uint64_t)nTiles * (blockIdx.x + 1)) / G);
+    if (t0 >= t1) return;
+    GridWalker<I> walk(p, lane);
+
+    auto issue = [&](const TileBase<I>& tb, uint32_t stage) {
+        const W* __restrict__ src = opaque(in + tb.in);
+        if (tb.need == 0 && allSlots) {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                cp_async<sizeof(W)>(stage + (spk[r] & 0xffffu), elem_addr(src, gin[r]));
+        } else {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need)
+                    cp_async<sizeof(W)>(stage + (spk[r] & 0xffffu), elem_addr(src, gin[r]));
+        }
+    };
+
+    // prologue: tiles t0 .. t0+S-2 in flight
+    TileBase<I> q[S - 1];  // q[0] = the tile written next
+    TileBase<I> cur = walk.seek(t0);
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        if (t0 + j < t1) {
+            if (j > 0) cur = walk.next(cur);
+            q[j] = cur;
+            issue(cur, sm0 + (uint32_t)j * sbytes);
+        }
+        cp_async_commit();
+    }
+    int stage = 0;  // stage of tile t
+    for (I t = t0; t < t1; ++t) {
+        cp_async_wait<S - 2>();  // this thread's copies for tile t have landed
+        __syncthreads();         // ... and everyone's; the stage read last iteration is free
+        TileBase<I> nw;
+        const bool more = t + (S - 1) < t1;
+        if (more) {
+            cur = walk.next(cur);
+            nw = cur;
+            const int ns = (stage + S - 1) % S;
+            issue(cur, sm0 + (uint32_t)ns * sbytes);
+        }
+        cp_async_commit();
+        // transposed read of the staged tile (Eq. 6), coalesced writes (Eq. 5)
+        const TileBase<I> now = q[0];
+        const uint32_t sb = sm0 + (uint32_t)stage * sbytes;
+        W* __restrict__ dst = opaque(out + now.out);
+        if (now.need == 0 && allSlots) {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r) *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+        } else {
+            const uint32_t needOut = now.need << 2;
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
+                    *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < S - 1; ++j) q[j] = q[j + 1];
+        if (more) q[S - 2] = nw;
+        stage = (stage + 1 == S) ? 0 : stage + 1;
+    }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -671,6 +785,25 @@ static const void* pick_tile(int esize, int nreg, bool idx64) {
 #undef TT_PICK
 }
 
+// asynchronous-copy tile: 3 stages, 32-bit indices, 4/8/16-byte words
+static const void* pick_tile_async(int esize, int nreg, bool idx64) {
+    if (idx64) return nullptr;
+#define TT_PICKA(W)                                                                  \
+    switch (nreg) {                                                                  \
+        case 1: return (const void*)&tile_async_kernel<W, 1, uint32_t, 3>;           \
+        case 2: return (const void*)&tile_async_kernel<W, 2, uint32_t, 3>;           \
+        case 4: return (const void*)&tile_async_kernel<W, 4, uint32_t, 3>;           \
+        case 8: return (const void*)&tile_async_kernel<W, 8, uint32_t, 3>;           \
+        case 16: return (const void*)&tile_async_kernel<W, 16, uint32_t, 3>;         \
+        default: return nullptr;                                                     \
+    }
+    if (esize == 4) { TT_PICKA(uint32_t) }
+    if (esize == 8) { TT_PICKA(uint64_t) }
+    if (esize == 16 && nreg <= 4) { TT_PICKA(uint4) }
+    return nullptr;
+#undef TT_PICKA
+}
+
 static const void* pick_rowcopy(int esize, bool idx64) {
     switch (esize) {
         case 4: return idx64 ? (const void*)&rowcopy_kernel<uint32_t, int64_t>
@@ -747,7 +880,8 @@ static cudaError_t ensure_max_smem(const void* fn) {
 
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
-    const void* fn = q.kernel == TT_KERNEL_TILE      ? pick_tile(q.esize, q.nreg, q.idx64)
+    const void* fn = q.kernel == TT_KERNEL_TILE      ? (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
+                                                                   : pick_tile(q.esize, q.nreg, q.idx64))
                      : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
                      : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
@@ -799,7 +933,8 @@ int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
             smem = kc.fb_smem;
         }
         const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64)
-                            : pick_tile(E, kc.nreg, kc.idx64);
+                            : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
+                                              : pick_tile(E, kc.nreg, kc.idx64));
         if (!fn) return (int)cudaErrorInvalidConfiguration;
         if (smem > 48 * 1024) {
             cudaError_t e = ensure_max_smem(fn);

@@ -696,7 +696,11 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.kernel = TT_KERNEL_TILE;
     kc.threads = best.threads;
     kc.nreg = best.nreg;
-    kc.smem = 2 * plan.tile.sbuf * E;
+    // staging pipeline: register double buffer (default) or a cp.async ring
+    // of 3 stages (32-bit indices only)
+    kc.stages = (opts && opts->stages >= 3 && !kc.idx64) ? 3 : 0;
+    kc.smem = (kc.stages ? kc.stages : 2) * plan.tile.sbuf * E;
+    if (kc.smem > dev.max_smem_per_block) { kc.stages = 0; kc.smem = 2 * plan.tile.sbuf * E; }
     kc.vec = 1;
     kc.predicted_us = best.cost_us;
     kc.model_dram_eff = best.dram_eff;
@@ -705,7 +709,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.m_secIn = best.secIn;
     kc.m_secOut = best.secOut;
     kc.m_inflight = best.inflight;
-    OccQuery q{TT_KERNEL_TILE, E, kc.nreg, 1, kc.threads, kc.smem, kc.idx64, 0, 0};
+    OccQuery q{TT_KERNEL_TILE, E, kc.nreg, kc.stages ? kc.stages : 1, kc.threads, kc.smem,
+               kc.idx64, 0, 0};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
     kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
@@ -777,7 +782,8 @@ std::string describe_json(const Plan& plan) {
     arr(o, pr.d, pr.n);
     o << ",\"perm\":";
     arr(o, pr.p, pr.n);
-    o << "},\"kernel\":\"" << kernel_name(kc.kernel) << "\",\"threads\":" << kc.threads
+    o << "},\"kernel\":\"" << kernel_name(kc.kernel) << "\",\"stages\":" << kc.stages
+      << ",\"threads\":" << kc.threads
       << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
       << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us

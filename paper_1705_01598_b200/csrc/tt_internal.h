@@ -114,6 +114,7 @@ struct KernelChoice {
     bool idx64 = false;
     int tile0 = 0, tile1 = 0;      // TILED2D tile
     int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
+    int stages = 0;                // generic tile: 0 = register double buffer, >= 3 = cp.async ring
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
     // model features of the generic tile (describe "model"; calibration)

@@ -166,6 +166,20 @@ def test_rowcopy_and_widening(esize):
             np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+def test_async_stages(esize):
+    """The cp.async 3-stage tile pipeline (stages=3) on generic, ragged,
+    forced-geometry and widened problems."""
+    for dims, perm in RANDOM_SHAPES[:11] + [((37, 29, 11), (2, 0, 1)), ((600, 7, 5), (0, 2, 1))]:
+        vol = int(np.prod(dims))
+        if vol > 2_000_000:
+            dims = wl.scaled(wl.Case("x", dims, perm, esize, 3), 1_000_000).dims
+        check(dims, perm, esize, stages=3)
+        check(dims, perm, esize, stages=3, kernel=tt.KERNEL_TILE, run_in=8, run_out=5)
+    for threads in (64, 256):
+        check((97, 89, 3), (1, 2, 0), esize, stages=3, kernel=tt.KERNEL_TILE, threads=threads)
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)
