@@ -145,6 +145,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--grid-order", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--plan", default="heuristic", choices=["heuristic", "measured", "both"])
     a = ap.parse_args()
@@ -158,6 +159,8 @@ def main():
         opts["ctas_per_sm"] = a.ctas_per_sm
     if a.stages:
         opts["stages"] = a.stages
+    if a.grid_order:
+        opts["grid_order"] = a.grid_order
     rows, cache = [], {}
     f = open(a.out, "w") if a.out else None
     modes = {"heuristic": [False], "measured": [True], "both": [False, True]}[a.plan]

@@ -338,11 +338,15 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     const bool allSlots = p.V == NT * NREG;  // CTA-uniform
     build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
 
-    // contiguous tile range per CTA, walked with the odometer
+    // Tile schedule: a contiguous range per CTA walked with the odometer, or
+    // (p.interleave) tiles blockIdx.x + k*gridDim.x so that concurrently
+    // running CTAs work on neighbouring tiles, each found with Algorithm 1.
     const I nTiles = (I)p.nTiles;
     const I G = (I)gridDim.x;
-    const I t0 = (I)(((uint64_t)nTiles * blockIdx.x) / G);
-    const I t1 = (I)(((uint64_t)nTiles * (blockIdx.x + 1)) / G);
+    const bool il = p.interleave != 0;
+    const I t0 = il ? (I)blockIdx.x : (I)(((uint64_t)nTiles * blockIdx.x) / G);
+    const I t1 = il ? nTiles : (I)(((uint64_t)nTiles * (blockIdx.x + 1)) / G);
+    const I step = il ? G : (I)1;
     if (t0 >= t1) return;
     GridWalker<I> walk(p, lane);
 
@@ -362,7 +366,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     load(cur);
 
     uint32_t sb = sm0;
-    for (I t = t0; t < t1; ++t) {
+    for (I t = t0; t < t1; t += step) {
         // stage the tile in input order
         if (allSlots) {
 #pragma unroll
@@ -375,8 +379,8 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         __syncthreads();
         // issue the next tile's global loads before writing this one
         const TileBase<I> now = cur;
-        if (t + 1 < t1) {
-            cur = walk.next(cur);
+        if (t + step < t1) {
+            cur = il ? walk.seek(t + step) : walk.next(cur);
             load(cur);
         }
         // transposed read of shared memory (Eq. 6), coalesced writes (Eq. 5)

@@ -48,6 +48,7 @@ struct TileParams {
     int32_t a;          // number of tile dims
     int32_t h;          // number of grid dims (<= 32, one warp lane each)
     int32_t nSplit;     // number of split tile dims (0..2)
+    int32_t interleave; // 1: CTA b runs tiles b, b+G, ...; 0: a contiguous range per CTA
     int32_t splitLane[2];   // grid lane carrying the split dim's chunk index
     int32_t splitChunk[2];  // tile extent of the split dim
     int32_t splitTile[2];   // tile-dim index of the split dim
