@@ -93,7 +93,7 @@ typedef struct {
     int ctas_per_sm;     /* persistent CTAs per SM (grid = num_sms * this)         */
     int no_fusion;       /* 1 = skip dimension fusion / extent-1 removal (debug)   */
     int grid_order;      /* TILED2D tile order: 1 = A-chunks fastest, 2 = B-chunks fastest;
-                            TILE: 1 = interleaved tiles over CTAs, 2 = contiguous ranges */
+                            TILE: 1/0 = interleaved tiles over CTAs, 2 = contiguous ranges */
     int no_widen;        /* 1 = never regroup elements of an unchanged fastest dim into wider words */
     int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner */
 } tt_plan_options_t;

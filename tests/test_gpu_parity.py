@@ -176,7 +176,7 @@ def test_async_stages(esize):
             dims = wl.scaled(wl.Case("x", dims, perm, esize, 3), 1_000_000).dims
         check(dims, perm, esize, stages=3)
         check(dims, perm, esize, stages=3, kernel=tt.KERNEL_TILE, run_in=8, run_out=5)
-        check(dims, perm, esize, kernel=tt.KERNEL_TILE, grid_order=1)  # interleaved tiles
+        check(dims, perm, esize, kernel=tt.KERNEL_TILE, grid_order=2)  # contiguous tile ranges
     for threads in (64, 256):
         check((97, 89, 3), (1, 2, 0), esize, stages=3, kernel=tt.KERNEL_TILE, threads=threads)
 

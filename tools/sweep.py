@@ -108,6 +108,27 @@ def sweep_tile(n):
         torch.cuda.empty_cache()
 
 
+def sweep_t2ds():
+    """Scalar 2-D kernel (odd extents): tiles x CTAs/SM x order."""
+    cases = [wl.Case("o4", (12953, 12953), (1, 0), 4, 3), wl.Case("o8", (9159, 9161), (1, 0), 8, 4),
+             wl.Case("o8b", (119, 119, 119, 119), (3, 2, 1, 0), 8, 5)]
+    for c in cases:
+        x, ref, p0 = setup(c)
+        print(json.dumps({"case": c.name, "memcpy_gbs": memcpy_gbs(x), "auto": measure(c, x, ref)}), flush=True)
+        tiles = [(64, 64), (128, 64), (64, 128)] if c.esize == 4 else [(64, 64), (32, 64), (64, 32)]
+        for order in (1, 2):
+            for ta, tb in tiles:
+                for cps in (1, 2, 3, 4, 6):
+                    r = measure(c, x, ref, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb,
+                                ctas_per_sm=cps, grid_order=order)
+                    print(json.dumps({"case": c.name, "order": order, "ta": ta, "tb": tb, "cps": cps,
+                                      "gbs": r.get("gbs"), "ok": r.get("ok")}), flush=True)
+        r = measure(c, x, ref, kernel=tt.KERNEL_TILE)
+        print(json.dumps({"case": c.name, "generic": r.get("gbs")}), flush=True)
+        del x, ref
+        torch.cuda.empty_cache()
+
+
 def sweep_cps(n):
     """Auto tile geometry at different persistent-grid sizes (CTAs per SM)."""
     cases = wl.s2_ttc()[::max(1, 57 // n)][:n] + \
@@ -168,6 +189,8 @@ if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "t2d":
         sweep_t2d()
+    elif mode == "t2ds":
+        sweep_t2ds()
     elif mode == "calib":
         sweep_calib()
     elif mode == "cps":
