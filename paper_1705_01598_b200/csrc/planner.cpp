@@ -534,7 +534,7 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     // vectors, 64 x 64 otherwise; two CTAs per SM, B-chunks fastest.
     if (pr.esize == 4) { ta = 64; tb = vec == 4 ? 128 : 64; }
     else { ta = 64; tb = 64; }
-    if (vec == 1) { ta = 64; tb = 64; }
+    if (vec == 1) { ta = pr.esize == 4 ? 64 : 32; tb = 64; }  // sweep_t2ds: 3 CTAs/SM
     if (wantA || wantB) {
         if (wantA) ta = wantA;
         if (wantB) tb = wantB;
@@ -741,7 +741,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         if (occ2 <= 0) occ2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
         // two CTAs per SM measured best (fewer concurrent tiles, whole DRAM
         // rows); never more than fit, so the persistent grid is one wave
-        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(vec2d == 1 ? 4 : 2, occ2);
+        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(vec2d == 1 ? 3 : 2, occ2);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
         const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
         kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;
