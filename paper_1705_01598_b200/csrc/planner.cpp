@@ -414,7 +414,9 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         c.secIn = secIn;
         c.secOut = secOut;
         // slots of ragged tiles are partly idle but still issued
-        const double bytes = (double)tp.nTiles * modelSec * model::kSector;
+        // DRAM bytes scale with the elements actually moved (ragged tiles move
+        // fewer), issue cost with the tiles launched (ragged slots still issue)
+        const double bytes = (double)pr.vol / tp.V * modelSec * model::kSector;
         const bool idx64 = pr.vol >= (int64_t(1) << 31);
         for (int R : {16, 8, 4, 2, 1}) {
             if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
