@@ -134,6 +134,7 @@ constexpr double kSlotInstr = 11.0;       // per warp per slot: LDG, STS, LDS, S
 constexpr double kLaunchUs = 3.0;         // launch + tail
 constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row locality overhead
 constexpr double kInflightBytes = 49152;  // loads in flight per SM needed for full bandwidth
+constexpr double kTileLatUs = 1.5;        // per tile iteration of one CTA: load latency + barrier
 }  // namespace model
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -441,8 +442,13 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
                                             R * model::kSlotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
             const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
                                    std::max(1, dev.num_sms) / model::kClockMHz;
-            const double cost =
-                std::max(t_mem, t_issue) + 0.25 * std::min(t_mem, t_issue) + model::kLaunchUs;
+            // latency floor: every tile iteration of a CTA waits for its loads
+            // and a barrier however few of its slots are valid (ragged tiles)
+            const int occ = estimate_occupancy(oq, dev);
+            const double t_lat = std::ceil((double)tp.nTiles / ((double)dev.num_sms * occ)) *
+                                 model::kTileLatUs;
+            const double top = std::max(std::max(t_mem, t_issue), t_lat);
+            const double cost = top + 0.25 * (t_mem + t_issue + t_lat - top) + model::kLaunchUs;
             if (c.threads == 0 || cost < c.cost_us) {
                 c.cost_us = cost;
                 c.threads = T;
