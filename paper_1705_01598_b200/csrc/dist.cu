@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <sstream>
@@ -109,7 +110,10 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
     const int P = nranks;
     const int t = perm[n - 1];
     if (gd[n - 1] % P != 0) return TT_UNSUPPORTED;
-    const bool redist = (t != n - 1) && P > 1;
+    // TT_SHARD_FORCE_REDIST=1 (tests): take the pack / all-to-all / unpack path
+    // even with one rank, so the NCCL path runs on a single-GPU box
+    const char* force = std::getenv("TT_SHARD_FORCE_REDIST");
+    const bool redist = (t != n - 1) && (P > 1 || (force && force[0] == '1'));
     if (redist && gd[t] % P != 0) return TT_UNSUPPORTED;
 
     ShardInfo* s = new (std::nothrow) ShardInfo();

@@ -77,3 +77,26 @@ def test_single_rank_nccl():
         np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), orc.permute(gdims, perm, words))
         sp.destroy()
     comm.destroy()
+
+
+def test_single_rank_nccl_redistribution_path(monkeypatch):
+    """pack -> ncclAlltoAll -> unpack with one rank (forced), so the NCCL
+    exchange and the staging buffers run on a single-GPU box."""
+    _dev()
+    monkeypatch.setenv("TT_SHARD_FORCE_REDIST", "1")
+    comm = tt.Comm(tt.unique_id(), 1, 0)
+    for perm, esize in [((3, 2, 1, 0), 8), ((2, 3, 0, 1), 4), ((0, 3, 1, 2), 8)]:
+        gdims = (16, 24, 8, 40)
+        words = wl.random_words(int(np.prod(gdims)), esize, 7)
+        x = torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
+        y = torch.empty_like(x)
+        sp = tt.ShardedPlan(comm, gdims, perm, esize)
+        d = sp.describe()
+        assert d["mode"] == "redistribute" and d["launches"] == 2
+        sp.execute(x, y)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y.cpu().numpy().view(words.dtype), orc.permute(gdims, perm, words))
+        pack_ms, a2a_ms, unpack_ms = sp.timings()
+        assert pack_ms > 0 and unpack_ms > 0 and a2a_ms >= 0
+        sp.destroy()
+    comm.destroy()
