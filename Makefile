@@ -29,7 +29,7 @@ $(LIB): $(OBJS) $(CSRC)/exports.map
 	mv $@.tmp $@
 
 oracle/liboracle.so: oracle/tt_oracle.c
-	gcc -O2 -std=c99 -shared -fPIC -Wall -Wextra -o $@ $<
+	gcc -O2 -std=c99 -ffp-contract=off -shared -fPIC -Wall -Wextra -o $@ $<
 
 clean:
 	rm -rf $(BUILD) $(LIB) oracle/liboracle.so

@@ -80,12 +80,48 @@ def verify(case, x, y, mode):
     return bool(ok)
 
 
+def verify_scaled(case, x, y0, y1, alpha, beta):
+    """Sampled check of out = alpha*perm(in) + beta*out: the oracle gives
+    in[src(q)] one position at a time; numpy's float ops (pinned equal to the
+    oracle's scaled form in tests/test_accumulate.py) finish the sample."""
+    from oracle import oracle as orc
+    wt, ft = (np.uint32, np.float32) if case.esize == 4 else (np.uint64, np.float64)
+    words = x.cpu().numpy().view(wt)
+    rng = np.random.default_rng(case.seed & 0xFFFFFFFF)
+    pos = rng.integers(0, case.vol, 1 << 16)
+    src = orc.permute_sample(case.dims, case.perm, words, pos).view(ft)
+    before = y0.cpu().numpy().view(ft)[pos]
+    want = (ft(alpha) * src + ft(beta) * before).astype(ft).view(wt)
+    got = y1.cpu().numpy().view(wt)[pos]
+    ok_nan = np.isnan(want.view(ft)) == np.isnan(got.view(ft))
+    fin = ~np.isnan(want.view(ft))
+    return bool(ok_nan.all() and np.array_equal(want[fin], got[fin]))
+
+
 def run_case(case, reps, vmode, memcpy_cache, opts, measured=False):
     td = torch.int32 if case.esize == 4 else torch.int64
     g = torch.Generator(device="cuda")
     g.manual_seed(case.seed & 0x7FFFFFFFFFFFFFFF)
     x = torch.randint(-2**31, 2**31 - 1, (case.vol,), dtype=td, device="cuda", generator=g)
     y = torch.empty_like(x)
+    if opts.get("accumulate"):
+        ft = torch.float32 if case.esize == 4 else torch.float64
+        x.view(ft).uniform_(-1.0, 1.0, generator=g)
+        y.view(ft).uniform_(-1.0, 1.0, generator=g)
+        plan = tt.Plan(case.dims, case.perm, case.esize, **opts)
+        y0 = y.clone()
+        plan.execute_scaled(x, y, 1.5, 0.5)
+        torch.cuda.synchronize()
+        ok = verify_scaled(case, x, y0, y, 1.5, 0.5) if vmode != "none" else None
+        ms, mn, mx = event_ms(lambda: plan.execute_scaled(x, y, 1.5, 0.5), reps)
+        d = plan.describe()
+        plan.destroy()
+        gbs = 3 * case.nbytes / ms / 1e6      # P:L303: read in, read out, write out
+        return {"case": case.name, "rank": case.rank, "esize": case.esize, "dims": list(case.dims),
+                "perm": list(case.perm), "kernel": "tile+acc", "ms": round(ms, 5),
+                "gbs": round(gbs, 1), "gibs": round(3 * case.nbytes / ms / 1e3 / 2**30 * 1e3, 1),
+                "frac_memcpy": None, "verified": ok, "tile": d.get("tile", {}).get("ext"),
+                "threads": d["threads"], "grid": d["grid"], "plan": "accumulate"}
     t0 = time.perf_counter()
     if measured:
         plan = tt.Plan(case.dims, case.perm, case.esize, measure=(x, y))
@@ -121,6 +157,12 @@ def summarize(rows):
         key = r["case"].split("_")[0] + ("@measured" if r["case"].endswith("@measured") else "")
         by_suite.setdefault(key, []).append(r)
     for s, rs in by_suite.items():
+        if rs[0]["frac_memcpy"] is None:  # accumulate form: GB/s and GiB/s only
+            g = sorted(r["gbs"] for r in rs)
+            out[s] = {"n": len(rs), "worst_gbs": g[0], "median_gbs": statistics.median(g),
+                      "best_gbs": g[-1], "median_gibs": statistics.median(r["gibs"] for r in rs),
+                      "all_verified": all(r["verified"] in (True, None) for r in rs)}
+            continue
         f = sorted(r["frac_memcpy"] for r in rs)
         g = sorted(r["gbs"] for r in rs)
         per_rank = {}
@@ -146,6 +188,8 @@ def main():
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--grid-order", type=int, default=0)
+    ap.add_argument("--accumulate", action="store_true",
+                    help="TTC-style accumulate form, bandwidth 3*vol*E/D (P:L303)")
     ap.add_argument("--out", default="")
     ap.add_argument("--plan", default="heuristic", choices=["heuristic", "measured", "both"])
     a = ap.parse_args()
@@ -161,6 +205,8 @@ def main():
         opts["stages"] = a.stages
     if a.grid_order:
         opts["grid_order"] = a.grid_order
+    if a.accumulate:
+        opts["accumulate"] = True
     rows, cache = [], {}
     f = open(a.out, "w") if a.out else None
     modes = {"heuristic": [False], "measured": [True], "both": [False, True]}[a.plan]

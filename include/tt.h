@@ -96,6 +96,7 @@ typedef struct {
                             TILE: 1/0 = interleaved tiles over CTAs, 2 = contiguous ranges */
     int no_widen;        /* 1 = never regroup elements of an unchanged fastest dim into wider words */
     int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner */
+    int accumulate;      /* 1 = accumulate plan for tt_execute_scaled (generic tile, 32-bit indices) */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */
@@ -173,6 +174,18 @@ tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out);
  */
 tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out,
                             void* dev_in, void* dev_out);
+
+/*
+ * tt_execute_scaled -- accumulate form (SURVEY f-3, the TTC
+ * comparison "read input, read output, accumulate, write output"):
+ *     out = alpha * permute(in) + beta * out
+ * elementwise in the element's float type (4 bytes: float, 8: double), with
+ * alpha and beta converted to it, round-to-nearest multiplies and add, no
+ * fused multiply-add; beta == 0 does not read out.  The plan must have been
+ * created with tt_plan_options_t.accumulate = 1 (else TT_INVALID_PLAN).
+ * Bandwidth convention for this form: 3 * vol * E / time.
+ */
+tt_status_t tt_execute_scaled(tt_plan_t plan, const void* in, void* out, double alpha, double beta);
 
 /* tt_destroy -- free the plan (and a sharded plan's staging buffers).
  * tt_destroy(NULL) returns TT_INVALID_PLAN. */

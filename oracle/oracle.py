@@ -43,7 +43,8 @@ def build(force: bool = False) -> str:
     ):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-Wall", "-Wextra", "-o", tmp, _SRC]
+            ["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-shared", "-fPIC", "-Wall", "-Wextra",
+             "-o", tmp, _SRC]
         )
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
@@ -67,6 +68,10 @@ def _load():
                                                   ctypes.c_void_p, i64p, ctypes.c_int64,
                                                   ctypes.c_void_p]
             lib.oracle_permute_sample.restype = ctypes.c_int
+            lib.oracle_permute_scaled.argtypes = [ctypes.c_int, i64p, i32p, ctypes.c_int,
+                                                  ctypes.c_void_p, ctypes.c_void_p,
+                                                  ctypes.c_double, ctypes.c_double]
+            lib.oracle_permute_scaled.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -151,6 +156,21 @@ def permute_sample(dims, perm, words, positions) -> np.ndarray:
     if rc != 0:
         raise ValueError("oracle rejected the arguments or a position")
     return vals
+
+
+def permute_scaled(dims, perm, words, out_words, alpha: float, beta: float) -> np.ndarray:
+    """out = alpha * permute(words) + beta * out_words (float for 4-byte words,
+    double for 8-byte; separate RN multiplies and add; beta == 0 ignores
+    out_words).  Returns the new output words."""
+    dims, perm, words, esize, vol, d, p = _args(dims, perm, words)
+    out = np.array(out_words, dtype=words.dtype, copy=True)
+    if out.size != vol:
+        raise ValueError("output size mismatch")
+    rc = _load().oracle_permute_scaled(len(dims), d, p, esize, words.ctypes.data, out.ctypes.data,
+                                       float(alpha), float(beta))
+    if rc != 0:
+        raise ValueError("oracle rejected the arguments")
+    return out
 
 
 # ---------------------------------------------------------------------------

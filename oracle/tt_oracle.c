@@ -142,3 +142,47 @@ int oracle_permute_sample(int rank, const int64_t* dims, const int* perm, int es
     }
     return ORACLE_OK;
 }
+
+/*
+ * Accumulate form (SURVEY f-3; Section 3.3: the TTC
+ * comparison kernels "read input, read output, accumulate, write output"):
+ *     out[q] = alpha * in[src(q)] + beta * out[q]
+ * in float (esize 4) or double (esize 8) with alpha, beta converted to that
+ * type; each multiply and the add rounded separately (this file is compiled
+ * with -ffp-contract=off, no FMA); beta == 0 does not read out (BLAS
+ * convention, reading R21).  src(q) by the P:L52 division decode.
+ */
+int oracle_permute_scaled(int rank, const int64_t* dims, const int* perm, int esize,
+                          const void* in, void* out, double alpha, double beta) {
+    if (check_args(rank, dims, perm, esize) != ORACLE_OK) return ORACLE_BAD_ARG;
+    int64_t cin[ORACLE_MAX_RANK], cout[ORACLE_MAX_RANK], e[ORACLE_MAX_RANK];
+    int64_t vol = 1;
+    for (int i = 0; i < rank; ++i) { cin[i] = vol; vol *= dims[i]; }
+    int64_t acc = 1;
+    for (int j = 0; j < rank; ++j) { e[j] = dims[perm[j]]; cout[j] = acc; acc *= e[j]; }
+    for (int64_t q = 0; q < vol; ++q) {
+        int64_t src = 0;
+        for (int j = 0; j < rank; ++j) src += ((q / cout[j]) % e[j]) * cin[perm[j]];
+        if (esize == 4) {
+            const float a = (float)alpha, b = (float)beta;
+            float x, y, r;
+            memcpy(&x, (const uint32_t*)in + src, 4);
+            r = a * x;
+            if (beta != 0.0) {
+                memcpy(&y, (uint32_t*)out + q, 4);
+                r = r + b * y;
+            }
+            memcpy((uint32_t*)out + q, &r, 4);
+        } else {
+            double x, y, r;
+            memcpy(&x, (const uint64_t*)in + src, 8);
+            r = alpha * x;
+            if (beta != 0.0) {
+                memcpy(&y, (uint64_t*)out + q, 8);
+                r = r + beta * y;
+            }
+            memcpy((uint64_t*)out + q, &r, 8);
+        }
+    }
+    return ORACLE_OK;
+}

@@ -44,7 +44,8 @@ class PlanOptions(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int), ("run_in", ctypes.c_int), ("run_out", ctypes.c_int),
                 ("threads", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
                 ("no_fusion", ctypes.c_int), ("grid_order", ctypes.c_int),
-                ("no_widen", ctypes.c_int), ("stages", ctypes.c_int)]
+                ("no_widen", ctypes.c_int), ("stages", ctypes.c_int),
+                ("accumulate", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -69,6 +70,7 @@ def _load():
         "tt_plan_measure": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, vp, vp, vp,
                             ctypes.c_int],
         "tt_execute": [vp, vp, vp],
+        "tt_execute_scaled": [vp, vp, vp, ctypes.c_double, ctypes.c_double],
         "tt_execute_host": [vp, vp, vp, vp, vp],
         "tt_destroy": [vp],
         "tt_plan_describe": [vp, ctypes.c_char_p, ctypes.c_size_t],
@@ -112,9 +114,10 @@ def _arrays(dims, perm):
 
 
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
-             grid_order=0, no_widen=False, stages=0):
+             grid_order=0, no_widen=False, stages=0, accumulate=False):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
-                       1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages))
+                       1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
+                       1 if accumulate else 0)
 
 
 def _ptr(x) -> int:
@@ -174,6 +177,11 @@ class Plan:
         _check(lib.tt_execute(self._h, _ptr(inp), _ptr(out)), "tt_execute")
 
     __call__ = execute
+
+    def execute_scaled(self, inp, out, alpha: float, beta: float) -> None:
+        """out = alpha * permute(inp) + beta * out (plan made with accumulate=True)."""
+        _check(lib.tt_execute_scaled(self._h, _ptr(inp), _ptr(out), float(alpha), float(beta)),
+               "tt_execute_scaled")
 
     def execute_host(self, host_in, host_out, dev_in, dev_out) -> None:
         """Enqueue H2D(host_in -> dev_in), permute, D2H(dev_out -> host_out)."""

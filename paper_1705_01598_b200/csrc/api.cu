@@ -67,7 +67,7 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     const bool fuse = !(opts && opts->no_fusion);
     p->prob = normalize(rank, dims, perm, (int)elem_size, fuse);
     // element widening (planner.cpp widen_factor) unless geometry is forced
-    const bool forcedGeometry = opts && (opts->no_widen ||
+    const bool forcedGeometry = opts && (opts->no_widen || opts->accumulate ||
                                          (!widenForced && (opts->kernel || opts->run_in ||
                                                            opts->run_out || opts->threads)));
     const int k = forcedGeometry ? 1 : widen_factor(p->prob);
@@ -405,7 +405,17 @@ tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out) {
     tt_status_t st = check_exec(p, in, out);
     if (st != TT_SUCCESS) return st;
     if (p->shard) return TT_INVALID_PLAN;  // sharded plans use tt_execute_sharded
+    if (p->kc.acc) return TT_INVALID_PLAN;  // accumulate plans use tt_execute_scaled
     int e = launch_plan(*p, in, out, p->stream);
+    return e == 0 ? TT_SUCCESS : TT_CUDA_ERROR;
+}
+
+tt_status_t tt_execute_scaled(tt_plan_t plan, const void* in, void* out, double alpha, double beta) {
+    Plan* p = as_plan(plan);
+    tt_status_t st = check_exec(p, in, out);
+    if (st != TT_SUCCESS) return st;
+    if (p->shard || !p->kc.acc) return TT_INVALID_PLAN;
+    int e = launch_plan_scaled(*p, in, out, p->stream, alpha, beta);
     return e == 0 ? TT_SUCCESS : TT_CUDA_ERROR;
 }
 

@@ -312,13 +312,54 @@ __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT
 
 }
 
+// Output store of the staged element: plain (out = v) or, for accumulate
+// plans (f-3; "read input, read output, accumulate, write output"),
+// out = alpha*v + beta*out in the element's float type with round-to-nearest
+// multiplies and add and no FMA contraction (bit-exact against the oracle's
+// separate operations); beta == 0 does not read out (BLAS convention).
+template <typename W> struct FloatOf;
+template <> struct FloatOf<uint32_t> {
+    typedef float T;
+    static __device__ __forceinline__ float from(uint32_t w) { return __uint_as_float(w); }
+    static __device__ __forceinline__ uint32_t to(float f) { return __float_as_uint(f); }
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+template <> struct FloatOf<uint64_t> {
+    typedef double T;
+    static __device__ __forceinline__ double from(uint64_t w) { return __longlong_as_double((long long)w); }
+    static __device__ __forceinline__ uint64_t to(double f) { return (uint64_t)__double_as_longlong(f); }
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+template <> struct FloatOf<uint4> {  // never instantiated with ACC (no widening for accumulate)
+    typedef float T;
+    static __device__ __forceinline__ float from(uint4) { return 0.f; }
+    static __device__ __forceinline__ uint4 to(float) { return make_uint4(0, 0, 0, 0); }
+    static __device__ __forceinline__ float mul(float a, float) { return a; }
+    static __device__ __forceinline__ float add(float a, float) { return a; }
+};
+
+template <typename W, int ACC>
+__device__ __forceinline__ void put_out(W* dst, W v, const TileParams& p) {
+    if constexpr (ACC == 0) {
+        *dst = v;
+    } else {
+        typedef FloatOf<W> F;
+        const typename F::T alpha = (typename F::T)p.alpha, beta = (typename F::T)p.beta;
+        typename F::T r = F::mul(alpha, F::from(v));
+        if (!p.betaZero) r = F::add(r, F::mul(beta, F::from(*dst)));
+        *dst = F::to(r);
+    }
+}
+
 // Per slot r (tile element k = tid + r*NT): gin/gout = global minor offsets
 // (Eqs. 4, 5), sin/sout = staging byte offsets of the load element and of the
 // store element (Eq. 6 through the padded layout).  `flags` holds 4 bits per
 // slot: (load elem inside ragged A-chunk, ... B-chunk, store elem inside
 // ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
 // cover the tile's `need`.
-template <typename W, int NREG, typename I>
+template <typename W, int NREG, typename I, int ACC = 0>
 __global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, (NREG >= 16 ? 2 : (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
 tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -387,13 +428,14 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         W* __restrict__ dst = opaque(out + now.out);
         if (now.need == 0 && allSlots) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+            for (int r = 0; r < NREG; ++r)
+                put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)), p);
         } else {
             const uint32_t needOut = now.need << 2;
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
                 if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
-                    *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+                    put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)), p);
         }
         // Two buffers: the next iteration writes the other buffer, whose
         // readers (previous tile) all passed this iteration's barrier.
@@ -763,6 +805,23 @@ static const void* tile_fn() {
     return reinterpret_cast<const void*>(&tile_kernel<W, NREG, I>);
 }
 
+// accumulate variant (f-3): 4/8-byte words, 32-bit indices
+static const void* pick_tile_acc(int esize, int nreg) {
+#define TT_PICKACC(W)                                                               \
+    switch (nreg) {                                                                 \
+        case 1: return (const void*)&tile_kernel<W, 1, uint32_t, 1>;               \
+        case 2: return (const void*)&tile_kernel<W, 2, uint32_t, 1>;               \
+        case 4: return (const void*)&tile_kernel<W, 4, uint32_t, 1>;               \
+        case 8: return (const void*)&tile_kernel<W, 8, uint32_t, 1>;               \
+        case 16: return (const void*)&tile_kernel<W, 16, uint32_t, 1>;             \
+        default: return nullptr;                                                    \
+    }
+    if (esize == 4) { TT_PICKACC(uint32_t) }
+    if (esize == 8) { TT_PICKACC(uint64_t) }
+    return nullptr;
+#undef TT_PICKACC
+}
+
 static const void* pick_tile(int esize, int nreg, bool idx64) {
 #define TT_PICK(W, I)                               \
     switch (nreg) {                                 \
@@ -884,8 +943,10 @@ static cudaError_t ensure_max_smem(const void* fn) {
 
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
-    const void* fn = q.kernel == TT_KERNEL_TILE      ? (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
-                                                                   : pick_tile(q.esize, q.nreg, q.idx64))
+    const void* fn = q.kernel == TT_KERNEL_TILE
+                         ? (q.acc ? pick_tile_acc(q.esize, q.nreg)
+                                      : (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
+                                                    : pick_tile(q.esize, q.nreg, q.idx64)))
                      : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
                      : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
@@ -903,6 +964,11 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
 }
 
 int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
+    return launch_plan_scaled(plan0, in, out, stream_, 1.0, 0.0);
+}
+
+int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* stream_, double alpha,
+                       double beta) {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     // widened words need E*widen-aligned pointers; otherwise run the narrow plan
     const Plan& plan = (plan0.widen > 1 && plan0.narrow &&
@@ -937,14 +1003,23 @@ int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
             smem = kc.fb_smem;
         }
         const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64)
-                            : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
-                                              : pick_tile(E, kc.nreg, kc.idx64));
+                            : kc.acc ? pick_tile_acc(E, kc.nreg)
+                                     : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
+                                                       : pick_tile(E, kc.nreg, kc.idx64));
         if (!fn) return (int)cudaErrorInvalidConfiguration;
         if (smem > 48 * 1024) {
             cudaError_t e = ensure_max_smem(fn);
             if (e != cudaSuccess) return (int)e;
         }
+        TileParams scaled;
         const void* pp = t2 ? (const void*)&plan.t2d : (const void*)&plan.tile;
+        if (kc.acc) {
+            scaled = plan.tile;
+            scaled.alpha = alpha;
+            scaled.beta = beta;
+            scaled.betaZero = beta == 0.0;
+            pp = &scaled;
+        }
         void* args[] = {const_cast<void*>(pp), (void*)&in, (void*)&out};
         return (int)cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, stream);
     }

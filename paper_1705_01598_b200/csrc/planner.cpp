@@ -616,9 +616,13 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const int E = pr.esize;
 
     kc.idx64 = pr.vol >= (int64_t(1) << 31);
+    const bool acc = opts && opts->accumulate;
+    if (acc && (kc.idx64 || E > 8 || (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE)))
+        return TT_UNSUPPORTED;
+    kc.acc = acc ? 1 : 0;
 
     // (i) rank 1 after fusion: copy (identity; "trivial" permutation)
-    if (pr.n == 1 && (forced == TT_KERNEL_AUTO || forced == TT_KERNEL_COPY)) {
+    if (!acc && pr.n == 1 && (forced == TT_KERNEL_AUTO || forced == TT_KERNEL_COPY)) {
         kc.kernel = TT_KERNEL_COPY;
         kc.threads = opts && opts->threads ? opts->threads : 512;
         kc.vec = 16 / E;
@@ -634,7 +638,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // (ii) fastest dim unchanged with long rows: row copy, no staging
     const bool rowClass = pr.n >= 2 && pr.p[0] == 0;
     if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
-    if (rowClass && (forced == TT_KERNEL_ROWCOPY ||
+    if (!acc && rowClass && (forced == TT_KERNEL_ROWCOPY ||
                      (forced == TT_KERNEL_AUTO && pr.d[0] * E >= 512 &&
                       !(opts && (opts->run_in || opts->run_out))))) {
         RowParams& r = plan.row;
@@ -667,7 +671,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     int vec2d = 0, ta2d = 0, tb2d = 0;
     double fill2d = 0;
     const bool force2d = forced == TT_KERNEL_TILED2D;
-    const bool can2d = build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d,
+    const bool can2d = !acc && build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d,
                                      force2d && opts ? opts->run_in : 0,
                                      force2d && opts ? opts->run_out : 0,
                                      opts && opts->grid_order ? opts->grid_order : 2);
@@ -706,7 +710,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.nreg = best.nreg;
     // staging pipeline: register double buffer (default) or a cp.async ring
     // of 3 stages (32-bit indices only)
-    kc.stages = (opts && opts->stages >= 3 && !kc.idx64) ? 3 : 0;
+    kc.stages = (opts && opts->stages >= 3 && !kc.idx64 && !acc) ? 3 : 0;
     // interleaved tiles (neighbouring tiles on concurrently running CTAs)
     // measured better than contiguous ranges on 72 of 84 suite cases
     plan.tile.interleave = (opts && opts->grid_order == 2) ? 0 : 1;
@@ -721,7 +725,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.m_secOut = best.secOut;
     kc.m_inflight = best.inflight;
     OccQuery q{TT_KERNEL_TILE, E, kc.nreg, kc.stages ? kc.stages : 1, kc.threads, kc.smem,
-               kc.idx64, 0, 0};
+               kc.idx64, 0, 0, kc.acc};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
     kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
@@ -793,7 +797,8 @@ std::string describe_json(const Plan& plan) {
     arr(o, pr.d, pr.n);
     o << ",\"perm\":";
     arr(o, pr.p, pr.n);
-    o << "},\"kernel\":\"" << kernel_name(kc.kernel) << "\",\"stages\":" << kc.stages
+    o << "},\"kernel\":\"" << kernel_name(kc.kernel) << "\",\"accumulate\":" << kc.acc
+      << ",\"stages\":" << kc.stages
       << ",\"threads\":" << kc.threads
       << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")

@@ -49,6 +49,8 @@ struct TileParams {
     int32_t h;          // number of grid dims (<= 32, one warp lane each)
     int32_t nSplit;     // number of split tile dims (0..2)
     int32_t interleave; // 1: CTA b runs tiles b, b+G, ...; 0: a contiguous range per CTA
+    int32_t betaZero;   // accumulate plans: beta == 0 (do not read out)
+    double alpha, beta; // accumulate plans: out = alpha*perm(in) + beta*out (set per launch)
     int32_t splitLane[2];   // grid lane carrying the split dim's chunk index
     int32_t splitChunk[2];  // tile extent of the split dim
     int32_t splitTile[2];   // tile-dim index of the split dim
@@ -116,6 +118,7 @@ struct KernelChoice {
     int tile0 = 0, tile1 = 0;      // TILED2D tile
     int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
     int stages = 0;                // generic tile: 0 = register double buffer, >= 3 = cp.async ring
+    int acc = 0;                   // accumulate plan (f-3): generic tile with alpha/beta
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
     // model features of the generic tile (describe "model"; calibration)
@@ -138,6 +141,7 @@ struct OccQuery {
     int kernel, esize, nreg, vec, threads, smem;
     bool idx64;
     int ta, tb;  // TILED2D tile
+    int acc;     // TILE accumulate variant
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 
@@ -201,5 +205,7 @@ std::string describe_shard_json(const Plan& plan);
 // kernels.cu ----------------------------------------------------------------
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev);
 int launch_plan(const Plan& plan, const void* in, void* out, void* stream);  // cudaError_t
+int launch_plan_scaled(const Plan& plan, const void* in, void* out, void* stream, double alpha,
+                       double beta);
 
 }  // namespace tt
