@@ -119,7 +119,7 @@ def run_case(case, reps, vmode, memcpy_cache, opts, measured=False):
         gbs = 3 * case.nbytes / ms / 1e6      # read in, read out, write out
         return {"case": case.name, "rank": case.rank, "esize": case.esize, "dims": list(case.dims),
                 "perm": list(case.perm), "kernel": "tile+acc", "ms": round(ms, 5),
-                "gbs": round(gbs, 1), "gibs": round(3 * case.nbytes / ms / 1e3 / 2**30 * 1e3, 1),
+                "gbs": round(gbs, 1), "gibs": round(3 * case.nbytes / (ms * 1e-3) / 2**30, 1),
                 "frac_memcpy": None, "verified": ok, "tile": d.get("tile", {}).get("ext"),
                 "threads": d["threads"], "grid": d["grid"], "plan": "accumulate"}
     t0 = time.perf_counter()

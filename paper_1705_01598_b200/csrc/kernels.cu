@@ -341,14 +341,14 @@ template <> struct FloatOf<uint4> {  // never instantiated with ACC (no widening
 };
 
 template <typename W, int ACC>
-__device__ __forceinline__ void put_out(W* dst, W v, const TileParams& p) {
+__device__ __forceinline__ void put_out(W* dst, W v, W old, const TileParams& p) {
     if constexpr (ACC == 0) {
         *dst = v;
     } else {
         typedef FloatOf<W> F;
         const typename F::T alpha = (typename F::T)p.alpha, beta = (typename F::T)p.beta;
         typename F::T r = F::mul(alpha, F::from(v));
-        if (!p.betaZero) r = F::add(r, F::mul(beta, F::from(*dst)));
+        if (!p.betaZero) r = F::add(r, F::mul(beta, F::from(old)));
         *dst = F::to(r);
     }
 }
@@ -403,8 +403,23 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(elem_addr(src, gin[r]));
         }
     };
+    // accumulate plans: the old output values of a tile, prefetched one
+    // iteration ahead (after the previous tile's writes) so the read of `out`
+    // is not exposed in the store phase
+    W ov[ACC ? NREG : 1];
+    auto load_out = [&](const TileBase<I>& tb) {
+        if constexpr (ACC != 0) {
+            if (p.betaZero) return;
+            const W* __restrict__ o = opaque(out + tb.out);
+            const uint32_t needOut = tb.need << 2;
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut) ov[r] = *elem_addr(o, gout[r]);
+        }
+    };
     TileBase<I> cur = walk.seek(t0);
     load(cur);
+    load_out(cur);
 
     uint32_t sb = sm0;
     for (I t = t0; t < t1; t += step) {
@@ -429,14 +444,17 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         if (now.need == 0 && allSlots) {
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)), p);
+                put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
+                                ov[ACC ? r : 0], p);
         } else {
             const uint32_t needOut = now.need << 2;
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
                 if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
-                    put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)), p);
+                    put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
+                                    ov[ACC ? r : 0], p);
         }
+        if (t + step < t1) load_out(cur);
         // Two buffers: the next iteration writes the other buffer, whose
         // readers (previous tile) all passed this iteration's barrier.
         sb = (sb == sm0) ? sm0 + sbytes : sm0;
