@@ -261,7 +261,7 @@ static long smem_cost(const TileParams& tp, int esize, const int32_t* sm) {
 
 // Build the tile of candidate run targets (Tin, Tout) in elements.
 static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
-                           const DeviceInfo& dev, int forceThreads) {
+                           const DeviceInfo& dev, int forceThreads, int maxR = 16) {
     TileCand c;
     const int n = pr.n;
     int64_t need[kMaxDims];
@@ -423,6 +423,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
             if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
             // 16 slots: 256-thread CTAs, 32-bit indices only (kernels.cu launch bounds)
             if (R == 16 && idx64) continue;
+            if (R > maxR) continue;
             int T = (int)ceil_div(tp.V, R);
             T = (int)ceil_div(T, 32) * 32;
             if (forceThreads) {
@@ -689,7 +690,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         for (int64_t to : targets) {
             int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
             int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads);
+            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16);
             if (!c.ok) continue;
             if (!best.ok || c.cost_us < best.cost_us) best = c;
         }
@@ -697,7 +698,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     if (!best.ok) {
         // fall back to the smallest legal tile
         for (int64_t t = 64; t >= 2 && !best.ok; t /= 2) {
-            TileCand c = build_tile(pr, t, t, 12288, dev, forceThreads);
+            TileCand c = build_tile(pr, t, t, 12288, dev, forceThreads, acc ? 8 : 16);
             if (c.ok) best = c;
         }
     }
