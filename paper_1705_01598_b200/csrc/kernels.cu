@@ -265,9 +265,7 @@ __device__ __forceinline__ TileBase<I> decode_tile(const P& p, I t, int lane) {
 // Per slot r (tile element k = tid + r*NT): Eq. (4) global input offset,
 // Eq. (5) global output offset, staging byte offsets of the load element and
 // of the store element (Eq. (6) with padded strides), ragged-chunk flags.
-// Slots past the tile volume (k >= V) alias element k mod V: they load, stage
-// and store exactly what that element's own slot does (same address, same
-// value), so every slot is valid and the hot loop carries no slot predicates.
+// Slots past the tile volume (k >= V) are idle (nmine).
 template <typename W, int NREG, typename I, typename FlagT>
 __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT, int nmine,
                                             I (&gin)[NREG], I (&gout)[NREG], uint32_t (&spk)[NREG],
@@ -278,7 +276,7 @@ __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT
         gout[r] = 0;
         spk[r] = 0;
         if (r < nmine) {
-            const int k = (tid + r * NT) % p.V;
+            const int k = tid + r * NT;
             uint32_t f = 0;
             // Eq. (4): pMinorIn(k), tile-input order
             int rem = k;
@@ -378,8 +376,8 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     uint32_t spk[NREG];  // staging byte offsets: load element (low 16 bits), store element (high)
     typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
     FlagT flags = 0;
-    constexpr int nmine = NREG;    // every slot valid (aliasing, build_slots)
-    constexpr bool allSlots = true;
+    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    const bool allSlots = p.V == NT * NREG;  // CTA-uniform
     build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
 
     // Tile schedule: a contiguous range per CTA walked with the odometer, or
@@ -400,6 +398,10 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         if (tb.need == 0 && allSlots) {
 #pragma unroll
             for (int r = 0; r < NREG; ++r) v[r] = ldg_(elem_addr(src, gin[r]));
+        } else if (tb.need == 0) {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine) v[r] = ldg_(elem_addr(src, gin[r]));
         } else {
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
@@ -449,6 +451,12 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             for (int r = 0; r < NREG; ++r)
                 put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
                                 ov[ACC ? r : 0], p);
+        } else if (now.need == 0) {
+#pragma unroll
+            for (int r = 0; r < NREG; ++r)
+                if (r < nmine)
+                    put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
+                                    ov[ACC ? r : 0], p);
         } else {
             const uint32_t needOut = now.need << 2;
 #pragma unroll
@@ -495,8 +503,8 @@ tile_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in
     uint32_t spk[NREG];
     typedef typename std::conditional<(NREG > 8), uint64_t, uint32_t>::type FlagT;
     FlagT flags = 0;
-    constexpr int nmine = NREG;
-    constexpr bool allSlots = true;
+    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    const bool allSlots = p.V == NT * NREG;
     build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
 
     const I nTiles = (I)p.nTiles;
