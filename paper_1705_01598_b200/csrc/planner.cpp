@@ -419,7 +419,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         // fewer), issue cost with the tiles launched (ragged slots still issue)
         const double bytes = (double)pr.vol / tp.V * modelSec * model::kSector;
         const bool idx64 = pr.vol >= (int64_t(1) << 31);
-        for (int R : {16, 8, 4, 2, 1}) {
+        for (int R : {8, 16, 4, 2, 1}) {  // ties: 8 slots (more warps, smaller code)
             if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
             // 16 slots: 256-thread CTAs, 32-bit indices only (kernels.cu launch bounds)
             if (R == 16 && idx64) continue;
