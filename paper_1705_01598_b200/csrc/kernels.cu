@@ -83,6 +83,35 @@ template <> __device__ __forceinline__ uint4 lds<uint4>(uint32_t a) {
     return v;
 }
 __device__ __forceinline__ uint4 ldg_(const uint4* p) { return __ldg(p); }
+// Global stores through explicit st.global: pointers built by elem_addr (a
+// mad.wide in inline PTX) are generic to the compiler, which would otherwise
+// emit generic ST instead of STG.
+__device__ __forceinline__ void stg_(uint32_t* p, uint32_t v) {
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stg_(uint64_t* p, uint64_t v) {
+    asm volatile("st.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void stg_(uint4* p, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ldgo_(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint64_t ldgo_(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ldgo_(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint32_t ldg_(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint64_t ldg_(const uint64_t* p) {
     return __ldg(reinterpret_cast<const unsigned long long*>(p));
@@ -344,13 +373,13 @@ template <> struct FloatOf<uint4> {  // never instantiated with ACC (no widening
 template <typename W, int ACC>
 __device__ __forceinline__ void put_out(W* dst, W v, W old, const TileParams& p) {
     if constexpr (ACC == 0) {
-        *dst = v;
+        stg_(dst, v);
     } else {
         typedef FloatOf<W> F;
         const typename F::T alpha = (typename F::T)p.alpha, beta = (typename F::T)p.beta;
         typename F::T r = F::mul(alpha, F::from(v));
         if (!p.betaZero) r = F::add(r, F::mul(beta, F::from(old)));
-        *dst = F::to(r);
+        stg_(dst, F::to(r));
     }
 }
 
@@ -419,7 +448,7 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             const uint32_t needOut = tb.need << 2;
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut) ov[r] = *elem_addr(o, gout[r]);
+                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut) ov[r] = ldgo_(elem_addr(o, gout[r]));
         }
     };
     TileBase<I> cur = walk.seek(t0);
@@ -559,13 +588,13 @@ tile_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in
         W* __restrict__ dst = opaque(out + now.out);
         if (now.need == 0 && allSlots) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+            for (int r = 0; r < NREG; ++r) stg_(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)));
         } else {
             const uint32_t needOut = now.need << 2;
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
                 if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
-                    *elem_addr(dst, gout[r]) = lds<W>(sb + (spk[r] >> 16));
+                    stg_(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)));
         }
 #pragma unroll
         for (int j = 0; j + 1 < S - 1; ++j) q[j] = q[j + 1];
@@ -627,7 +656,7 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
                 if (c + 32 * u < L) t[u] = ldg_(src + c + 32 * u);
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (c + 32 * u < L) dst[c + 32 * u] = t[u];
+                if (c + 32 * u < L) stg_(dst + c + 32 * u, t[u]);
         }
         // odometer step to row r+1
         const uint32_t wraps = __ballot_sync(0xffffffffu, lane < p.h && x == d - 1);
@@ -819,7 +848,7 @@ tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ 
             for (int u = 0; u < TB / 32; ++u) {
                 const int b = lane + 32 * u;
                 if (a < limA && b < limB)
-                    dst[(I)a * sOutA + b] = lds<W>(sb + (uint32_t)((a * RS + b) * sizeof(W)));
+                    stg_(dst + ((I)a * sOutA + b), lds<W>(sb + (uint32_t)((a * RS + b) * sizeof(W))));
             }
         }
         sb = (sb == sm0) ? sm0 + BUF : sm0;
