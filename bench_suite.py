@@ -187,6 +187,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--grid-order", type=int, default=0)
     ap.add_argument("--accumulate", action="store_true",
                     help="TTC-style accumulate form, bandwidth 3*vol*E/D (P:L303)")
@@ -203,6 +204,8 @@ def main():
         opts["ctas_per_sm"] = a.ctas_per_sm
     if a.stages:
         opts["stages"] = a.stages
+    if a.slots:
+        opts["slots"] = a.slots
     if a.grid_order:
         opts["grid_order"] = a.grid_order
     if a.accumulate:

@@ -45,7 +45,7 @@ class PlanOptions(ctypes.Structure):
                 ("threads", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
                 ("no_fusion", ctypes.c_int), ("grid_order", ctypes.c_int),
                 ("no_widen", ctypes.c_int), ("stages", ctypes.c_int),
-                ("accumulate", ctypes.c_int)]
+                ("accumulate", ctypes.c_int), ("slots", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):

@@ -57,6 +57,9 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     *out = nullptr;
     tt_status_t st = validate(rank, dims, perm, elem_size);
     if (st != TT_SUCCESS) return st;
+    if (opts && opts->slots != 0 && opts->slots != 1 && opts->slots != 2 && opts->slots != 4 &&
+        opts->slots != 8 && opts->slots != 16)
+        return TT_INVALID_PARAMETER;
     Plan* p = new (std::nothrow) Plan();
     if (p == nullptr) return TT_INTERNAL_ERROR;
     p->device = dev.device;
@@ -69,7 +72,7 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     // element widening (planner.cpp widen_factor) unless geometry is forced
     const bool forcedGeometry = opts && (opts->no_widen || opts->accumulate ||
                                          (!widenForced && (opts->kernel || opts->run_in ||
-                                                           opts->run_out || opts->threads)));
+                                                           opts->run_out || opts->threads || opts->slots)));
     const int k = forcedGeometry ? 1 : widen_factor(p->prob);
     if (k > 1) {
         Plan* nar = new (std::nothrow) Plan();

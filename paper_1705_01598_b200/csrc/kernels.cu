@@ -342,6 +342,26 @@ __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT
 
 }
 
+// Per-thread slot validity masks, one NREG-bit field per ragged state
+// need = 0..3 (bit n*NREG + r: slot r is valid when the tile's `need` is n):
+// the per-tile test becomes one shift and the per-slot test one bit test,
+// instead of extracting and comparing 4 flag bits per slot.
+template <int NREG, typename FlagT, typename MaskT>
+__device__ __forceinline__ void slot_masks(FlagT flags, int nmine, MaskT& lm, MaskT& sm) {
+    lm = 0;
+    sm = 0;
+#pragma unroll
+    for (int r = 0; r < NREG; ++r) {
+        if (r >= nmine) continue;
+        const uint32_t f = (uint32_t)(flags >> (4 * r)) & 15u;
+#pragma unroll
+        for (uint32_t n = 0; n < 4; ++n) {
+            if ((f & n) == n) lm |= (MaskT)1 << (n * NREG + r);
+            if (((f >> 2) & n) == n) sm |= (MaskT)1 << (n * NREG + r);
+        }
+    }
+}
+
 // Output store of the staged element: plain (out = v) or, for accumulate
 // plans (f-3; "read input, read output, accumulate, write output"),
 // out = alpha*v + beta*out in the element's float type with round-to-nearest
@@ -408,6 +428,9 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
     const bool allSlots = p.V == NT * NREG;  // CTA-uniform
     build_slots<W, NREG, I, FlagT>(p, tid, NT, nmine, gin, gout, spk, flags);
+    typedef typename std::conditional<(4 * NREG > 32), uint64_t, uint32_t>::type MaskT;
+    MaskT lmask, smask;
+    slot_masks<NREG>(flags, nmine, lmask, smask);
 
     // Tile schedule: a contiguous range per CTA walked with the odometer, or
     // (p.interleave) tiles blockIdx.x + k*gridDim.x so that concurrently
@@ -427,14 +450,11 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         if (tb.need == 0 && allSlots) {
 #pragma unroll
             for (int r = 0; r < NREG; ++r) v[r] = ldg_(elem_addr(src, gin[r]));
-        } else if (tb.need == 0) {
-#pragma unroll
-            for (int r = 0; r < NREG; ++r)
-                if (r < nmine) v[r] = ldg_(elem_addr(src, gin[r]));
         } else {
+            const uint32_t m = (uint32_t)(lmask >> (tb.need * NREG));
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine && ((flags >> (4 * r)) & tb.need) == tb.need) v[r] = ldg_(elem_addr(src, gin[r]));
+                if (m & (1u << r)) v[r] = ldg_(elem_addr(src, gin[r]));
         }
     };
     // accumulate plans: the old output values of a tile, prefetched one
@@ -445,10 +465,10 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
         if constexpr (ACC != 0) {
             if (p.betaZero) return;
             const W* __restrict__ o = opaque(out + tb.out);
-            const uint32_t needOut = tb.need << 2;
+            const uint32_t m = (uint32_t)(smask >> (tb.need * NREG));
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut) ov[r] = ldgo_(elem_addr(o, gout[r]));
+                if (m & (1u << r)) ov[r] = ldgo_(elem_addr(o, gout[r]));
         }
     };
     TileBase<I> cur = walk.seek(t0);
@@ -480,17 +500,11 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
             for (int r = 0; r < NREG; ++r)
                 put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
                                 ov[ACC ? r : 0], p);
-        } else if (now.need == 0) {
-#pragma unroll
-            for (int r = 0; r < NREG; ++r)
-                if (r < nmine)
-                    put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
-                                    ov[ACC ? r : 0], p);
         } else {
-            const uint32_t needOut = now.need << 2;
+            const uint32_t m = (uint32_t)(smask >> (now.need * NREG));
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (r < nmine && ((flags >> (4 * r)) & needOut) == needOut)
+                if (m & (1u << r))
                     put_out<W, ACC>(elem_addr(dst, gout[r]), lds<W>(sb + (spk[r] >> 16)),
                                     ov[ACC ? r : 0], p);
         }

@@ -261,7 +261,7 @@ static long smem_cost(const TileParams& tp, int esize, const int32_t* sm) {
 
 // Build the tile of candidate run targets (Tin, Tout) in elements.
 static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
-                           const DeviceInfo& dev, int forceThreads, int maxR = 16) {
+                           const DeviceInfo& dev, int forceThreads, int maxR = 16, int forceR = 0) {
     TileCand c;
     const int n = pr.n;
     int64_t need[kMaxDims];
@@ -424,6 +424,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
             // 16 slots: 256-thread CTAs, 32-bit indices only (kernels.cu launch bounds)
             if (R == 16 && idx64) continue;
             if (R > maxR) continue;
+            if (forceR && R != forceR) continue;
             int T = (int)ceil_div(tp.V, R);
             T = (int)ceil_div(T, 32) * 32;
             if (forceThreads) {
@@ -686,11 +687,12 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         targets.push_back(std::max<int64_t>(2, b / E));
     TileCand best;
     const int forceThreads = opts ? opts->threads : 0;
+    const int forceR = opts ? opts->slots : 0;
     for (int64_t ti : targets) {
         for (int64_t to : targets) {
             int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
             int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16);
+            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR);
             if (!c.ok) continue;
             if (!best.ok || c.cost_us < best.cost_us) best = c;
         }
