@@ -114,10 +114,10 @@ def _arrays(dims, perm):
 
 
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
-             grid_order=0, no_widen=False, stages=0, accumulate=False):
+             grid_order=0, no_widen=False, stages=0, accumulate=False, slots=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
                        1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
-                       1 if accumulate else 0)
+                       1 if accumulate else 0, int(slots))
 
 
 def _ptr(x) -> int:
