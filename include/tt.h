@@ -98,6 +98,7 @@ typedef struct {
     int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner */
     int accumulate;      /* 1 = accumulate plan for tt_execute_scaled (generic tile, 32-bit indices) */
     int slots;           /* TILE: elements per thread per tile (1, 2, 4, 8 or 16)   */
+    int slot_dims;       /* TILE: 1 = slot-dim thread map when it applies, -1 = never, 0 = planner */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

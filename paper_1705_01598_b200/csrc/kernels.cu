@@ -516,6 +516,164 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
 }
 
 // ---------------------------------------------------------------------------
+// generic staged tile, slot-dim variant.  Same tiles, grid walk, staging
+// layout and double-buffered register pipeline as tile_kernel, but a
+// different thread -> element map per phase: in the load phase every thread
+// owns R consecutive elements along one tile dim sL that lies outside the
+// input run (so a warp still reads along the run), in the store phase R
+// consecutive elements along a tile dim sS outside the output run.  Slot r of
+// a pass sits at the pass base + r * (stride of the slot dim) on both the
+// global and the staging side, so the per-slot tables of tile_kernel (three
+// registers per element: Eq. (4) offset, Eq. (5) offset, Eq. (6) staging
+// offsets) shrink to a few registers per pass of R elements.  The freed
+// registers buy occupancy, i.e. loads in flight per SM (the MWP/MLP terms of
+// P:L175-219 on B200).  Remaining dims + the chunk index of the slot dim form
+// the phase's thread space, decoded once per thread (Eqs. 4-6).
+// Validity (ragged split chunks, and a slot-dim extent that R does
+// not divide) is always a prefix r < cnt of a pass; cnt is kept per pass for
+// the four ragged states need = 0..3 (8 bits each).
+// ---------------------------------------------------------------------------
+template <typename W, int QM, int RM>
+__device__ __forceinline__ void build_sd_phase(const TileParams& p, int ph, int tid, int NT,
+                                               uint32_t (&g)[QM], uint32_t (&smp)[QM],
+                                               uint32_t (&cnt)[QM]) {
+    const int sl = p.sdSlot[ph];
+    const int R = p.sdR[ph];
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+        g[q] = 0;
+        cnt[q] = 0;
+        const int u = tid + q * NT;
+        if (q >= p.sdQ[ph] || u >= p.sdU[ph]) continue;
+        int rem = u;
+        uint32_t off = 0, sp = 0;
+        int xs = 0;         // slot-dim coordinate of slot 0
+        uint32_t bad = 0;   // ragged states (split bits) under which this pass is idle
+        for (int jj = 0; jj < p.a; ++jj) {
+            const int t = ph == 0 ? jj : p.tOutOrder[jj];
+            const int e = (t == sl) ? p.sdC[ph] : p.tExt[t];
+            int c = rem % e;
+            rem /= e;
+            if (t == sl) {
+                c *= R;
+                xs = c;
+            } else {
+                if (p.nSplit > 0 && t == p.splitTile[0] && c >= p.splitTail[0]) bad |= 1u;
+                if (p.nSplit > 1 && t == p.splitTile[1] && c >= p.splitTail[1]) bad |= 2u;
+            }
+            off += (uint32_t)c * (uint32_t)(ph == 0 ? p.tSin[t] : p.tSout[t]);
+            sp += (uint32_t)c * (uint32_t)p.tSm[t];
+        }
+        g[q] = off;
+        if (ph == 0) smp[q] = sp * (uint32_t)sizeof(W);
+        else smp[q] |= (sp * (uint32_t)sizeof(W)) << 16;
+        for (uint32_t n = 0; n < 4; ++n) {
+            if (bad & n) continue;
+            int lim = p.tExt[sl];
+            if (p.nSplit > 0 && sl == p.splitTile[0] && (n & 1u)) lim = p.splitTail[0];
+            if (p.nSplit > 1 && sl == p.splitTile[1] && (n & 2u)) lim = p.splitTail[1];
+            const int k = min(max(lim - xs, 0), R);
+            cnt[q] |= (uint32_t)k << (8 * n);
+        }
+    }
+}
+
+template <typename W, int QM, int RM>
+__global__ void __launch_bounds__(sizeof(W) >= 8 ? 384 : 512, 2)
+tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
+    const int tid = threadIdx.x;
+    const int NT = blockDim.x;
+    const int lane = tid & 31;
+
+    uint32_t gin[QM], gout[QM], smp[QM], cntL[QM], cntS[QM];
+#pragma unroll
+    for (int q = 0; q < QM; ++q) smp[q] = 0;
+    build_sd_phase<W, QM, RM>(p, 0, tid, NT, gin, smp, cntL);
+    build_sd_phase<W, QM, RM>(p, 1, tid, NT, gout, smp, cntS);
+    const int QL = p.sdQ[0], QS = p.sdQ[1];
+    // uniform per-slot strides: global (elements) and staging (bytes)
+    const uint32_t sIn = (uint32_t)p.tSin[p.sdSlot[0]];
+    const uint32_t sOut = (uint32_t)p.tSout[p.sdSlot[1]];
+    const uint32_t mIn = (uint32_t)p.tSm[p.sdSlot[0]] * (uint32_t)sizeof(W);
+    const uint32_t mOut = (uint32_t)p.tSm[p.sdSlot[1]] * (uint32_t)sizeof(W);
+
+    const uint32_t nTiles = (uint32_t)p.nTiles;
+    const uint32_t G = (uint32_t)gridDim.x;
+    const uint32_t t0 = (uint32_t)blockIdx.x;
+    if (t0 >= nTiles) return;
+    GridWalker<uint32_t> walk(p, lane);
+
+    W v[QM][RM];
+    auto load = [&](const TileBase<uint32_t>& tb) {
+        const uint32_t sh = 8u * tb.need;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            if (q >= QL) break;
+            const uint32_t c = (cntL[q] >> sh) & 0xffu;
+            const W* __restrict__ src = opaque(in + tb.in + gin[q]);
+            if (c == (uint32_t)RM) {
+#pragma unroll
+                for (int r = 0; r < RM; ++r) v[q][r] = ldg_(elem_addr(src, (uint32_t)r * sIn));
+            } else {
+#pragma unroll
+                for (int r = 0; r < RM; ++r)
+                    if ((uint32_t)r < c) v[q][r] = ldg_(elem_addr(src, (uint32_t)r * sIn));
+            }
+        }
+    };
+    TileBase<uint32_t> cur = walk.seek(t0);
+    load(cur);
+
+    uint32_t sb = sm0;
+    for (uint32_t t = t0; t < nTiles; t += G) {
+        // stage the tile (input-side map)
+        {
+            const uint32_t sh = 8u * cur.need;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+                if (q >= QL) break;
+                const uint32_t c = (cntL[q] >> sh) & 0xffu;
+                const uint32_t a0 = sb + (smp[q] & 0xffffu);
+#pragma unroll
+                for (int r = 0; r < RM; ++r)
+                    if ((uint32_t)r < c) sts(a0 + (uint32_t)r * mIn, v[q][r]);
+            }
+        }
+        __syncthreads();
+        const TileBase<uint32_t> now = cur;
+        if (t + G < nTiles) {
+            cur = walk.seek(t + G);
+            load(cur);
+        }
+        // transposed read of the staged tile, coalesced writes (output-side map)
+        {
+            const uint32_t sh = 8u * now.need;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+                if (q >= QS) break;
+                const uint32_t c = (cntS[q] >> sh) & 0xffu;
+                W* __restrict__ dst = opaque(out + now.out + gout[q]);
+                const uint32_t a0 = sb + (smp[q] >> 16);
+                if (c == (uint32_t)RM) {
+#pragma unroll
+                    for (int r = 0; r < RM; ++r)
+                        stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                } else {
+#pragma unroll
+                    for (int r = 0; r < RM; ++r)
+                        if ((uint32_t)r < c)
+                            stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                }
+            }
+        }
+        sb = (sb == sm0) ? sm0 + sbytes : sm0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // generic staged tile, asynchronous-copy pipeline: the loads go straight from
 // global to the staging buffer with cp.async (LDGSTS), no data registers, so
 // S-1 tiles are in flight per CTA (S stages of shared memory) instead of one.
@@ -872,6 +1030,20 @@ tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ 
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
+// slot-dim variant: (passes, slots) in {(1,16), (2,8), (4,4)}, 4/8-byte words,
+// 32-bit indices
+static const void* pick_tile_sd(int esize, int q, int r) {
+#define TT_PICKSD(W)                                                                  \
+    if (q == 1 && r == 16) return (const void*)&tile_sd_kernel<W, 1, 16>;           \
+    if (q == 2 && r == 8) return (const void*)&tile_sd_kernel<W, 2, 8>;             \
+    if (q == 4 && r == 4) return (const void*)&tile_sd_kernel<W, 4, 4>;             \
+    return nullptr;
+    if (esize == 4) { TT_PICKSD(uint32_t) }
+    if (esize == 8) { TT_PICKSD(uint64_t) }
+    return nullptr;
+#undef TT_PICKSD
+}
+
 template <typename W, int NREG, typename I>
 static const void* tile_fn() {
     return reinterpret_cast<const void*>(&tile_kernel<W, NREG, I>);
@@ -1016,7 +1188,8 @@ static cudaError_t ensure_max_smem(const void* fn) {
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
     const void* fn = q.kernel == TT_KERNEL_TILE
-                         ? (q.acc ? pick_tile_acc(q.esize, q.nreg)
+                         ? (q.sdq ? pick_tile_sd(q.esize, q.sdq, q.sdr)
+                            : q.acc ? pick_tile_acc(q.esize, q.nreg)
                                       : (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
                                                     : pick_tile(q.esize, q.nreg, q.idx64)))
                      : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
@@ -1075,6 +1248,7 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
             smem = kc.fb_smem;
         }
         const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64)
+                            : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr)
                             : kc.acc ? pick_tile_acc(E, kc.nreg)
                                      : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
                                                        : pick_tile(E, kc.nreg, kc.idx64));

@@ -591,10 +591,73 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     return true;
 }
 
+// Slot-dim thread map for a chosen generic tile (kernels.cu tile_sd_kernel):
+// per phase a slot dim outside that side's contiguous run (stride >= run, so
+// a warp still moves along the run) and R slots along it (R | ext preferred);
+// passes Q so that threads * Q * R covers the phase's thread space.  Picks
+// the (Q, R) instantiation with the best slot fill; false if none fills at
+// least 60 % of its slots or the launch would exceed the kernel's bound.
+static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, int& threads,
+                     int& sdq, int& sdr) {
+    struct Pick { int slot = -1, R = 0, C = 0; double eff = 0; };
+    auto pick_slot = [&](int ph, int RM) {
+        Pick best;
+        for (int t = 0; t < tp.a; ++t) {
+            // outside the phase's contiguous run, or inside it with >= 32
+            // contiguous elements before it (a warp still covers 32 in a row)
+            const int64_t stride = ph == 0 ? tp.tSin[t] : tp.tSout[t];
+            const int64_t before = ph == 0 ? tp.tCin[t] : tp.tCout[t];
+            if (stride < (ph == 0 ? runIn : runOut) && before < 32) continue;
+            const int ext = tp.tExt[t];
+            for (int R = std::min(RM, ext); R >= 1; --R) {
+                const int C = (ext + R - 1) / R;
+                const double eff = (double)ext / ((double)C * R) * ((double)R / RM);
+                if (eff > best.eff + 1e-9) { best.slot = t; best.R = R; best.C = C; best.eff = eff; }
+            }
+        }
+        return best;
+    };
+    double bestFill = 0;
+    TileParams bestTp = tp;
+    for (int cfg = 0; cfg < 3; ++cfg) {
+        const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
+        const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
+        const Pick L = pick_slot(0, RM), S = pick_slot(1, RM);
+        if (L.slot < 0 || S.slot < 0) continue;
+        const int64_t UL = (int64_t)tp.V / tp.tExt[L.slot] * L.C;
+        const int64_t US = (int64_t)tp.V / tp.tExt[S.slot] * S.C;
+        int64_t NT = (std::max(UL, US) + QM - 1) / QM;
+        NT = (NT + 31) / 32 * 32;
+        if (NT < 64) NT = 64;
+        if (NT > (esize >= 8 ? 384 : 512)) continue;  // kernels.cu launch bounds
+        const int64_t QL = (UL + NT - 1) / NT, QS = (US + NT - 1) / NT;
+        // slots issued vs elements moved (per phase), then register use
+        const double fill = std::min((double)tp.V / ((double)NT * QL * L.R),
+                                     (double)tp.V / ((double)NT * QS * S.R));
+        const double score = fill * (0.75 + 0.25 * std::min(1.0, (double)tp.V / NT / (QM * RM)));
+        if (fill >= 0.6 && score > bestFill + 1e-9) {
+            bestFill = score;
+            bestTp = tp;
+            bestTp.sdSlot[0] = L.slot; bestTp.sdR[0] = L.R; bestTp.sdC[0] = L.C;
+            bestTp.sdU[0] = (int32_t)UL; bestTp.sdQ[0] = (int32_t)QL;
+            bestTp.sdSlot[1] = S.slot; bestTp.sdR[1] = S.R; bestTp.sdC[1] = S.C;
+            bestTp.sdU[1] = (int32_t)US; bestTp.sdQ[1] = (int32_t)QS;
+            threads = (int)NT;
+            sdq = QM;
+            sdr = RM;
+        }
+    }
+    if (bestFill <= 0) return false;
+    tp = bestTp;
+    return true;
+}
+
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     // register counts of the tile kernels as compiled (ptxas -v, build/obj)
     int regs;
-    if (q.kernel == TT_KERNEL_TILE) {
+    if (q.kernel == TT_KERNEL_TILE && q.sdq) {
+        regs = q.esize == 8 ? 80 : 64;
+    } else if (q.kernel == TT_KERNEL_TILE) {
         const int r8 = q.esize == 8 ? 96 : 64;
         regs = q.nreg >= 16 ? 128 : q.nreg >= 8 ? r8 : q.nreg >= 4 ? 56 : q.nreg >= 2 ? 52 : 44;
         if (q.idx64) regs += 16;
@@ -734,6 +797,25 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
     // the generic tile stays in the plan as the fallback for pointers that
     // are not aligned to the 2-D kernel's vector width
+    // slot-dim thread map (fewer registers per element -> more loads in flight)
+    plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
+    {
+        const int sdOpt = opts ? opts->slot_dims : 0;
+        int thr = 0, sq = 0, sr = 0;
+        if (sdOpt >= 0 && !acc && !kc.idx64 && kc.stages == 0 && (E == 4 || E == 8) &&
+            !(opts && (opts->threads || opts->slots)) &&
+            build_sd(plan.tile, E, best.runIn, best.runOut, thr, sq, sr)) {
+            kc.sdq = sq;
+            kc.sdr = sr;
+            kc.threads = thr;
+            OccQuery qs{TT_KERNEL_TILE, E, sq * sr, 1, thr, kc.smem, false, 0, 0, 0, sq, sr};
+            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qs, dev) : 0);
+            if (per <= 0) per = estimate_occupancy(qs, dev);
+            kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
+        } else {
+            plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
+        }
+    }
     kc.fb_threads = kc.threads;
     kc.fb_grid = kc.grid;
     kc.fb_smem = kc.smem;
@@ -879,6 +961,19 @@ std::string describe_json(const Plan& plan) {
         arr(o, t.gSin, t.h);
         o << ",\"grid_sout\":";
         arr(o, t.gSout, t.h);
+        if (kc.sdq) {
+            o << ",\"sd\":{\"q\":" << kc.sdq << ",\"r\":" << kc.sdr << ",\"slot\":";
+            arr(o, t.sdSlot, 2);
+            o << ",\"R\":";
+            arr(o, t.sdR, 2);
+            o << ",\"C\":";
+            arr(o, t.sdC, 2);
+            o << ",\"U\":";
+            arr(o, t.sdU, 2);
+            o << ",\"Q\":";
+            arr(o, t.sdQ, 2);
+            o << "}";
+        }
         o << "}";
     }
     o << "}";

@@ -71,6 +71,15 @@ struct TileParams {
     int64_t gSout[kMaxDims];
     // 32-bit multiply-shift division magic for / gC and / gD (see fast_div)
     uint32_t gMC[kMaxDims], gLC[kMaxDims], gMD[kMaxDims], gLD[kMaxDims];
+    // slot-dim variant (tile_sd_kernel), per phase ph = 0 (load, tile-input
+    // order) and 1 (store, tile-output order): every thread owns sdR
+    // consecutive elements along tile dim sdSlot per pass, so the per-slot
+    // offsets are uniform strides and only a per-pass base stays per thread.
+    int32_t sdSlot[2];  // tile dim carrying the slots (-1: variant not used)
+    int32_t sdR[2];     // slots per pass along it
+    int32_t sdC[2];     // chunks of the slot dim, ceil(ext / sdR)
+    int32_t sdU[2];     // thread-space size: V / ext * chunks
+    int32_t sdQ[2];     // passes, ceil(sdU / threads)
 };
 
 // Row-copy (fastest dim unchanged, long rows; TiledCopy class P:L141): each
@@ -119,6 +128,7 @@ struct KernelChoice {
     int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
     int stages = 0;                // generic tile: 0 = register double buffer, >= 3 = cp.async ring
     int acc = 0;                   // accumulate plan (f-3): generic tile with alpha/beta
+    int sdq = 0, sdr = 0;          // generic tile, slot-dim variant: passes x slots (0 = classic)
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
     // model features of the generic tile (describe "model"; calibration)
@@ -142,6 +152,7 @@ struct OccQuery {
     bool idx64;
     int ta, tb;  // TILED2D tile
     int acc;     // TILE accumulate variant
+    int sdq, sdr;  // TILE slot-dim variant (passes, slots); 0 = classic
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 

@@ -52,6 +52,8 @@ def interpret_tile_plan(j, words):
         gout.append(off)
         psh.append(sh)
         cout_s.append(cs)
+    if "sd" in t:
+        return _interpret_sd(j, t, words, tails)
     for tile in range(t["nTiles"]):
         q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
         ib = sum(q[g] * gSi[g] for g in range(len(gC)))
@@ -66,6 +68,75 @@ def interpret_tile_plan(j, words):
                 out[ob + gout[k]] = smem[psh[k]]
                 written[ob + gout[k]] += 1
     assert (written == 1).all(), "tile decomposition must cover every output once"
+    return out
+
+
+def _sd_phase(j, t, ph, tails):
+    """Per ragged state need = 0..3, the (global offset, staging offset)
+    pairs one phase of tile_sd_kernel touches: thread u = tid + q*threads
+    decodes the phase's thread space (slot dim replaced by its chunk index),
+    slot r adds r * stride along the slot dim, valid slots are r < cnt."""
+    sd = t["sd"]
+    ext, sm = t["ext"], t["sm"]
+    stride = t["sin"] if ph == 0 else t["sout"]
+    order = list(range(len(ext))) if ph == 0 else t["out_order"]
+    sl, R, C, U, Q = sd["slot"][ph], sd["R"][ph], sd["C"][ph], sd["U"][ph], sd["Q"][ph]
+    assert R <= sd["r"] and Q <= sd["q"] and U <= j["threads"] * Q
+    st = t["split_tile"]
+    lists = [[] for _ in range(4)]
+    for tid in range(j["threads"]):
+        for qq in range(Q):
+            u = tid + qq * j["threads"]
+            if u >= U:
+                continue
+            rem, off, sp, xs, bad = u, 0, 0, 0, 0
+            for ti in order:
+                e = C if ti == sl else ext[ti]
+                c = rem % e
+                rem //= e
+                if ti == sl:
+                    c *= R
+                    xs = c
+                else:
+                    for s in range(len(st)):
+                        if st[s] == ti and c >= tails[s]:
+                            bad |= 1 << s
+                off += c * stride[ti]
+                sp += c * sm[ti]
+            for n in range(4):
+                if bad & n:
+                    continue
+                lim = ext[sl]
+                for s in range(len(st)):
+                    if st[s] == sl and n & (1 << s):
+                        lim = tails[s]
+                cnt = min(max(lim - xs, 0), R)
+                for r in range(cnt):
+                    lists[n].append((off + r * stride[sl], sp + r * sm[sl]))
+    return lists
+
+
+def _interpret_sd(j, t, words, tails):
+    st, sl = t["split_tile"], t["split_lane"]
+    gC, gD, gSi, gSo = t["grid_c"], t["grid_d"], t["grid_sin"], t["grid_sout"]
+    vol = int(np.prod(j["dims"]))
+    out = np.zeros(vol, dtype=words.dtype)
+    written = np.zeros(vol, dtype=np.int64)
+    load, store = _sd_phase(j, t, 0, tails), _sd_phase(j, t, 1, tails)
+    for n in range(4):
+        pos = [p for _, p in load[n]]
+        assert len(set(pos)) == len(pos) and (not pos or max(pos) < t["sbuf"])
+    for tile in range(t["nTiles"]):
+        q = [(tile // gC[g]) % gD[g] for g in range(len(gC))]
+        ib = sum(q[g] * gSi[g] for g in range(len(gC)))
+        ob = sum(q[g] * gSo[g] for g in range(len(gC)))
+        need = sum(1 << s for s in range(len(st)) if q[sl[s]] == gD[sl[s]] - 1
+                   and tails[s] != t["split_chunk"][s])
+        smem = {p: words[ib + g] for g, p in load[need]}
+        for g, p in store[need]:
+            out[ob + g] = smem[p]
+            written[ob + g] += 1
+    assert (written == 1).all(), "slot-dim tiles must cover every output once"
     return out
 
 

@@ -202,3 +202,47 @@ def test_s1_plan_shape():
     t = j["tile"]  # fallback: both runs at least 128 bytes
     assert min(t["ext"]) * 4 >= 128
     assert j["grid"] >= 148
+
+
+def _sd_cases():
+    rng = np.random.default_rng(2024)
+    out = []
+    while len(out) < 24:
+        rank = int(rng.integers(3, 9))
+        dims = tuple(int(x) for x in rng.integers(2, 9, size=rank))
+        if np.prod(dims) > 60000:
+            continue
+        perm = tuple(int(x) for x in rng.permutation(rank))
+        out.append((dims, perm, 4 if len(out) % 2 == 0 else 8))
+    return out + [((5, 3, 2, 4, 7, 6), (5, 4, 3, 2, 1, 0), 4), ((41, 41, 9), (0, 2, 1), 4),
+                  ((6, 40, 35), (2, 0, 1), 8), ((3, 5, 7, 11, 13), (4, 2, 0, 3, 1), 4)]
+
+
+@pytest.mark.parametrize("dims,perm,esize", _sd_cases())
+def test_slot_dim_plans_match_oracle(dims, perm, esize):
+    """Slot-dim thread map (kernels.cu tile_sd_kernel): replayed geometry
+    equals the oracle, with the planner's choice and with the map forced
+    on / off."""
+    words = wl.random_words(int(np.prod(dims)), esize, 11)
+    want = orc.permute(dims, perm, words)
+    for sd in (0, 1, -1):
+        j = tt.plan_offline(dims, perm, esize, slot_dims=sd, no_widen=True)
+        if sd == -1:
+            assert "sd" not in j.get("tile", {})
+        np.testing.assert_array_equal(interpret_plan(j, words), want)
+        if j["kernel"] == "tile" and "sd" in j["tile"]:
+            s = j["tile"]["sd"]
+            for ph in (0, 1):
+                assert s["U"][ph] <= j["threads"] * s["Q"][ph]
+                assert s["Q"][ph] <= s["q"] and s["R"][ph] <= s["r"]
+
+
+def test_slot_dim_map_used_on_suites():
+    """The slot-dim map applies to most generic-tile plans of the random suite."""
+    n = sd = 0
+    for c in wl.s3_random(per_cell=1):
+        j = tt.plan_offline(c.dims, c.perm, c.esize)
+        if j["kernel"] == "tile":
+            n += 1
+            sd += "sd" in j["tile"]
+    assert n > 20 and sd >= n // 2
