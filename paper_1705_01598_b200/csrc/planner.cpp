@@ -595,10 +595,12 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
 // per phase a slot dim outside that side's contiguous run (stride >= run, so
 // a warp still moves along the run) and R slots along it (R | ext preferred);
 // passes Q so that threads * Q * R covers the phase's thread space.  Picks
-// the (Q, R) instantiation with the best slot fill; false if none fills at
-// least 60 % of its slots or the launch would exceed the kernel's bound.
-static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, int& threads,
-                     int& sdq, int& sdr) {
+// the (Q, R) instantiation with the most CTAs (tiles in flight) per SM, then
+// the best slot fill; false if none fills at least 60 % of its slots within
+// the kernel's launch bound.
+template <typename OccOf>
+static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, OccOf occOf,
+                     int& threads, int& sdq, int& sdr, int& ctasPerSm) {
     struct Pick { int slot = -1, R = 0, C = 0; double eff = 0; };
     auto pick_slot = [&](int ph, int RM) {
         Pick best;
@@ -631,11 +633,14 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, i
         if (NT < 64) NT = 64;
         if (NT > (esize >= 8 ? 384 : 512)) continue;  // kernels.cu launch bounds
         const int64_t QL = (UL + NT - 1) / NT, QS = (US + NT - 1) / NT;
-        // slots issued vs elements moved (per phase), then register use
+        // slots issued vs elements moved (per phase); tiles in flight per SM
+        // (CTAs per SM) decide, fill breaks ties
         const double fill = std::min((double)tp.V / ((double)NT * QL * L.R),
                                      (double)tp.V / ((double)NT * QS * S.R));
-        const double score = fill * (0.75 + 0.25 * std::min(1.0, (double)tp.V / NT / (QM * RM)));
-        if (fill >= 0.6 && score > bestFill + 1e-9) {
+        const int per = occOf((int)NT, QM, RM);
+        const double score = per + 0.5 * fill;
+        if (fill >= 0.6 && per > 0 && score > bestFill + 1e-9) {
+            ctasPerSm = per;
             bestFill = score;
             bestTp = tp;
             bestTp.sdSlot[0] = L.slot; bestTp.sdR[0] = L.R; bestTp.sdC[0] = L.C;
@@ -799,21 +804,30 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // are not aligned to the 2-D kernel's vector width
     // slot-dim thread map (fewer registers per element -> more loads in flight)
     plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
+    // Used when it keeps more tiles in flight per SM than the classic map
+    // (measured on the suites: the win/loss boundary for 4-byte words; for
+    // 8-byte words the classic map already holds enough bytes per tile and
+    // the slot-dim map measured mixed, so it is opt-in there).
     {
         const int sdOpt = opts ? opts->slot_dims : 0;
-        int thr = 0, sq = 0, sr = 0;
-        if (sdOpt >= 0 && !acc && !kc.idx64 && kc.stages == 0 && (E == 4 || E == 8) &&
-            !(opts && (opts->threads || opts->slots)) &&
-            build_sd(plan.tile, E, best.runIn, best.runOut, thr, sq, sr)) {
+        int thr = 0, sq = 0, sr = 0, perSd = 0;
+        auto occOf = [&](int T, int q, int r) {
+            OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem, false, 0, 0, 0, q, r};
+            int v = occ ? occ(qs, dev) : 0;
+            return v > 0 ? v : estimate_occupancy(qs, dev);
+        };
+        TileParams sdTile = plan.tile;
+        const bool eligible = sdOpt >= 0 && !acc && !kc.idx64 && kc.stages == 0 &&
+                              (E == 4 || (E == 8 && sdOpt > 0)) &&
+                              !(opts && (opts->threads || opts->slots));
+        if (eligible && build_sd(sdTile, E, best.runIn, best.runOut, occOf, thr, sq, sr, perSd) &&
+            (sdOpt > 0 || perSd > perSm)) {
+            plan.tile = sdTile;
             kc.sdq = sq;
             kc.sdr = sr;
             kc.threads = thr;
-            OccQuery qs{TT_KERNEL_TILE, E, sq * sr, 1, thr, kc.smem, false, 0, 0, 0, sq, sr};
-            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qs, dev) : 0);
-            if (per <= 0) per = estimate_occupancy(qs, dev);
+            const int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : perSd;
             kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
-        } else {
-            plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
         }
     }
     kc.fb_threads = kc.threads;
