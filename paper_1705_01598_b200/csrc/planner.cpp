@@ -115,7 +115,9 @@ Problem widen_problem(const Problem& pr, int k) {
     int64_t d[kMaxDims];
     for (int i = 0; i < pr.n; ++i) d[i] = pr.d[i];
     d[0] /= k;
-    return normalize(pr.n, d, pr.p, pr.esize * k, true);  // d[0] may have become 1
+    Problem w = normalize(pr.n, d, pr.p, pr.esize * k, true);  // d[0] may have become 1
+    w.widen = pr.widen * k;
+    return w;
 }
 
 // --------------------------------------------------------------------------
@@ -805,9 +807,9 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // slot-dim thread map (fewer registers per element -> more loads in flight)
     plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
     // Used when it keeps more tiles in flight per SM than the classic map
-    // (measured on the suites: the win/loss boundary for 4-byte words; for
-    // 8-byte words the classic map already holds enough bytes per tile and
-    // the slot-dim map measured mixed, so it is opt-in there).
+    // (measured on the suites: the win/loss boundary for 4-byte words and
+    // for 8-byte words made of two 4-byte elements; on fp64 tensors the
+    // slot-dim map measured mixed, so it is opt-in there).
     {
         const int sdOpt = opts ? opts->slot_dims : 0;
         int thr = 0, sq = 0, sr = 0, perSd = 0;
@@ -818,7 +820,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         };
         TileParams sdTile = plan.tile;
         const bool eligible = sdOpt >= 0 && !acc && !kc.idx64 && kc.stages == 0 &&
-                              (E == 4 || (E == 8 && sdOpt > 0)) &&
+                              (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                               !(opts && (opts->threads || opts->slots));
         if (eligible && build_sd(sdTile, E, best.runIn, best.runOut, occOf, thr, sq, sr, perSd) &&
             (sdOpt > 0 || perSd > perSm)) {

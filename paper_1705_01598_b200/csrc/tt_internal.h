@@ -22,6 +22,7 @@ struct Problem {
     int64_t d[kMaxDims] = {};
     int p[kMaxDims] = {};
     int esize = 4;
+    int widen = 1;                // words are `widen` caller elements (planner.cpp widen_problem)
     int64_t vol = 1;
     int64_t sin[kMaxDims] = {};   // c(i, I): input stride of input dim i
     int64_t sout[kMaxDims] = {};  // c(i, O): output stride of input dim i

@@ -181,6 +181,26 @@ def test_async_stages(esize):
         check((97, 89, 3), (1, 2, 0), esize, stages=3, kernel=tt.KERNEL_TILE, threads=threads)
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+def test_slot_dim_map(esize):
+    """The slot-dim thread map (tile_sd_kernel) forced on, and the classic
+    map forced, on generic, ragged (split slot dims) and small-extent
+    problems; the describe output says which map ran."""
+    shapes = RANDOM_SHAPES[:11] + [((37, 29, 11), (2, 0, 1)), ((5, 3, 2, 4, 35, 33), (5, 4, 3, 2, 1, 0)),
+                                   ((41, 41, 41), (0, 2, 1)), ((46, 46, 46, 7), (3, 1, 0, 2)),
+                                   ((3, 5, 7, 11, 13, 2), (4, 2, 0, 5, 3, 1))]
+    used = 0
+    for dims, perm in shapes:
+        vol = int(np.prod(dims))
+        if vol > 2_000_000:
+            dims = wl.scaled(wl.Case("x", dims, perm, esize, 3), 1_000_000).dims
+        j = tt.Plan(dims, perm, esize, slot_dims=1, no_widen=True).describe()
+        used += "sd" in j.get("tile", {})
+        check(dims, perm, esize, slot_dims=1, no_widen=True)
+        check(dims, perm, esize, slot_dims=-1, no_widen=True)
+    assert used >= 8
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)
