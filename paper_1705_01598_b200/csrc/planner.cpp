@@ -839,8 +839,11 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // Vectorised 2-D tiled kernel when the tiles are mostly full: it moves
     // VW elements per instruction on both sides (model: its issue cost is a
     // fraction of the generic kernel's, DRAM sectors are whole).
+    // (8-byte words without vectors -- odd extents -- measured faster on the
+    // generic tile: 8 of 10 TTC cases, up to 1.26x, A/B tools/ab_opts.py)
     const bool want2d = forced == TT_KERNEL_TILED2D ||
                         (forced == TT_KERNEL_AUTO && can2d && fill2d >= 0.6 &&
+                         !(E == 8 && vec2d == 1) &&
                          !(opts && (opts->run_in || opts->run_out)));
     if (want2d) {
         kc.kernel = TT_KERNEL_TILED2D;
