@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -133,6 +134,7 @@ constexpr double kIssuePerClk = 4.0;      // warp-instructions per SM per clock
 constexpr double kTileInstr = 90.0;       // per warp per tile: Alg. 1 decode, barrier, loop
 constexpr double kTileInstr64 = 160.0;    // same with 64-bit index arithmetic
 constexpr double kSlotInstr = 11.0;       // per warp per slot: LDG, STS, LDS, STG, masks, address
+constexpr double kSlotInstrSd = 9.0;      // same, slot-dim map (uniform slot strides)
 constexpr double kLaunchUs = 3.0;         // launch + tail
 constexpr double kRunBytes = 12.0;        // per contiguous run: DRAM burst/row locality overhead
 constexpr double kInflightBytes = 49152;  // loads in flight per SM needed for full bandwidth
@@ -140,6 +142,12 @@ constexpr double kTileLatUs = 1.5;        // per tile iteration of one CTA: load
 }  // namespace model
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Calibration knobs (tools/ experiments only; unset = the defaults below).
+static double knob(const char* name, double dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atof(v) : dflt;
+}
 
 // Hacker's Delight unsigned division by invariant integers: l = ceil(log2 d),
 // m = floor(2^32 (2^l - d) / d) + 1; the 33-bit sum umulhi(n, m) + n cannot
@@ -188,6 +196,10 @@ struct TileCand {
     double inflight = 0;             // modelled load bytes in flight per SM
     int smem = 0;
     bool ok = false;
+    // slot-dim launch shape (tile_sd_kernel) won the model: tp carries its
+    // sd* fields, threads its CTA size
+    bool sd = false;
+    int sdq = 0, sdr = 0;
 };
 
 // Shared-memory wavefronts for one warp access of element positions pos[32].
@@ -261,9 +273,76 @@ static long smem_cost(const TileParams& tp, int esize, const int32_t* sm) {
     return cost;
 }
 
+// Slot-dim thread map for a chosen generic tile (kernels.cu tile_sd_kernel):
+// per phase a slot dim outside that side's contiguous run (stride >= run, so
+// a warp still moves along the run) and R slots along it (R | ext preferred);
+// passes Q so that threads * Q * R covers the phase's thread space.  Picks
+// the (Q, R) instantiation with the most CTAs (tiles in flight) per SM, then
+// the best slot fill; false if none fills at least 60 % of its slots within
+// the kernel's launch bound.
+template <typename OccOf>
+static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, OccOf occOf,
+                     int& threads, int& sdq, int& sdr, int& ctasPerSm) {
+    struct Pick { int slot = -1, R = 0, C = 0; double eff = 0; };
+    auto pick_slot = [&](int ph, int RM) {
+        Pick best;
+        for (int t = 0; t < tp.a; ++t) {
+            // outside the phase's contiguous run, or inside it with >= 32
+            // contiguous elements before it (a warp still covers 32 in a row)
+            const int64_t stride = ph == 0 ? tp.tSin[t] : tp.tSout[t];
+            const int64_t before = ph == 0 ? tp.tCin[t] : tp.tCout[t];
+            if (stride < (ph == 0 ? runIn : runOut) && before < 32) continue;
+            const int ext = tp.tExt[t];
+            for (int R = std::min(RM, ext); R >= 1; --R) {
+                const int C = (ext + R - 1) / R;
+                const double eff = (double)ext / ((double)C * R) * ((double)R / RM);
+                if (eff > best.eff + 1e-9) { best.slot = t; best.R = R; best.C = C; best.eff = eff; }
+            }
+        }
+        return best;
+    };
+    double bestFill = 0;
+    TileParams bestTp = tp;
+    for (int cfg = 0; cfg < 3; ++cfg) {
+        const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
+        const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
+        const Pick L = pick_slot(0, RM), S = pick_slot(1, RM);
+        if (L.slot < 0 || S.slot < 0) continue;
+        const int64_t UL = (int64_t)tp.V / tp.tExt[L.slot] * L.C;
+        const int64_t US = (int64_t)tp.V / tp.tExt[S.slot] * S.C;
+        int64_t NT = (std::max(UL, US) + QM - 1) / QM;
+        NT = (NT + 31) / 32 * 32;
+        if (NT < 64) NT = 64;
+        if (NT > (esize >= 8 ? 384 : 512)) continue;  // kernels.cu launch bounds
+        const int64_t QL = (UL + NT - 1) / NT, QS = (US + NT - 1) / NT;
+        // slots issued vs elements moved (per phase); tiles in flight per SM
+        // (CTAs per SM) decide, fill breaks ties
+        const double fill = std::min((double)tp.V / ((double)NT * QL * L.R),
+                                     (double)tp.V / ((double)NT * QS * S.R));
+        const int per = occOf((int)NT, QM, RM);
+        const double score = per + 0.5 * fill;
+        if (fill >= 0.6 && per > 0 && score > bestFill + 1e-9) {
+            ctasPerSm = per;
+            bestFill = score;
+            bestTp = tp;
+            bestTp.sdSlot[0] = L.slot; bestTp.sdR[0] = L.R; bestTp.sdC[0] = L.C;
+            bestTp.sdU[0] = (int32_t)UL; bestTp.sdQ[0] = (int32_t)QL;
+            bestTp.sdSlot[1] = S.slot; bestTp.sdR[1] = S.R; bestTp.sdC[1] = S.C;
+            bestTp.sdU[1] = (int32_t)US; bestTp.sdQ[1] = (int32_t)QS;
+            threads = (int)NT;
+            sdq = QM;
+            sdr = RM;
+        }
+    }
+    if (bestFill <= 0) return false;
+    tp = bestTp;
+    return true;
+}
+
 // Build the tile of candidate run targets (Tin, Tout) in elements.
 static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
-                           const DeviceInfo& dev, int forceThreads, int maxR = 16, int forceR = 0) {
+                           const DeviceInfo& dev, int forceThreads, int maxR = 16, int forceR = 0,
+                           int VmaxSd = 0) {
     TileCand c;
     const int n = pr.n;
     int64_t need[kMaxDims];
@@ -300,7 +379,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
     }
     long double V = 1;
     for (int i = 0; i < n; ++i) V *= (long double)need[i];
-    if (V > Vmax) return c;
+    if (V > std::max(Vmax, VmaxSd)) return c;
 
     TileParams& tp = c.tp;
     std::memset(&tp, 0, sizeof(tp));
@@ -421,7 +500,24 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         // fewer), issue cost with the tiles launched (ragged slots still issue)
         const double bytes = (double)pr.vol / tp.V * modelSec * model::kSector;
         const bool idx64 = pr.vol >= (int64_t(1) << 31);
+        // cost of one launch shape: memory time at the loads in flight it
+        // allows, issue time, per-tile latency floor
+        auto shape_cost = [&](int T, int slots, int occ, double slotInstr, double& inflight) {
+            inflight = (double)occ * std::min<double>((double)T * slots, tp.V) * E;
+            const double mlp = std::min(1.0, inflight / model::kInflightBytes);
+            const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
+            const double warps = T / 32.0;
+            const double perTile = warps * ((idx64 ? model::kTileInstr64 : model::kTileInstr) +
+                                            slots * slotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
+            const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
+                                   std::max(1, dev.num_sms) / model::kClockMHz;
+            static const double tileLat = knob("TT_KNOB_TILE_LAT", model::kTileLatUs);
+            const double t_lat = std::ceil((double)tp.nTiles / ((double)dev.num_sms * occ)) * tileLat;
+            const double top = std::max(std::max(t_mem, t_issue), t_lat);
+            return top + 0.25 * (t_mem + t_issue + t_lat - top) + model::kLaunchUs;
+        };
         for (int R : {8, 16, 4, 2, 1}) {  // ties: 8 slots (more warps, smaller code)
+            if (tp.V > Vmax) break;        // tile only for the slot-dim kernel
             if (pr.esize >= 16 && R > 4) continue;  // 16-byte words: <= 4 slots
             // 16 slots: 256-thread CTAs, 32-bit indices only (kernels.cu launch bounds)
             if (R == 16 && idx64) continue;
@@ -436,28 +532,43 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
             if (T > (R >= 16 ? 256 : 512)) continue;  // kernels.cu launch bounds
             if (T < 64 && R > 1) continue;
             // memory-level parallelism: bytes of loads in flight per SM (the
-            // B200 analogue of the paper's MWP/MLP terms)
+            // B200 analogue of the paper's MWP/MLP terms); latency
+            // floor: every tile iteration of a CTA waits for its loads and a
+            // barrier however few of its slots are valid (ragged tiles)
             const OccQuery oq{TT_KERNEL_TILE, pr.esize, R, 1, T, c.smem, idx64, 0, 0};
-            const double inflight = (double)estimate_occupancy(oq, dev) * T * R * E;
-            const double mlp = std::min(1.0, inflight / model::kInflightBytes);
-            const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
-            const double warps = T / 32.0;
-            const double perTile = warps * ((idx64 ? model::kTileInstr64 : model::kTileInstr) +
-                                            R * model::kSlotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
-            const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
-                                   std::max(1, dev.num_sms) / model::kClockMHz;
-            // latency floor: every tile iteration of a CTA waits for its loads
-            // and a barrier however few of its slots are valid (ragged tiles)
-            const int occ = estimate_occupancy(oq, dev);
-            const double t_lat = std::ceil((double)tp.nTiles / ((double)dev.num_sms * occ)) *
-                                 model::kTileLatUs;
-            const double top = std::max(std::max(t_mem, t_issue), t_lat);
-            const double cost = top + 0.25 * (t_mem + t_issue + t_lat - top) + model::kLaunchUs;
+            double inflight = 0;
+            const double cost = shape_cost(T, R, estimate_occupancy(oq, dev), model::kSlotInstr, inflight);
             if (c.threads == 0 || cost < c.cost_us) {
                 c.cost_us = cost;
                 c.threads = T;
                 c.nreg = R;
                 c.inflight = inflight;
+            }
+        }
+        // slot-dim launch shape: per-pass bases instead of per-element
+        // tables, so more CTAs (tiles in flight) per SM and tiles up to
+        // VmaxSd elements
+        if (VmaxSd > 0 && !idx64 && !forceThreads && !forceR) {
+            TileParams tsd = tp;
+            int thr = 0, q = 0, r = 0, per = 0;
+            auto occOf = [&](int T, int qq, int rr) {
+                const OccQuery qs{TT_KERNEL_TILE, pr.esize, qq * rr, 1, T, c.smem, false, 0, 0, 0, qq, rr};
+                return estimate_occupancy(qs, dev);
+            };
+            if (build_sd(tsd, pr.esize, c.runIn, c.runOut, occOf, thr, q, r, per)) {
+                double inflight = 0;
+                const int slots = std::max(tsd.sdQ[0] * tsd.sdR[0], tsd.sdQ[1] * tsd.sdR[1]);
+                const double cost = shape_cost(thr, slots, per, model::kSlotInstrSd, inflight);
+                if (c.threads == 0 || cost < c.cost_us) {
+                    c.cost_us = cost;
+                    c.threads = thr;
+                    c.nreg = q * r;
+                    c.inflight = inflight;
+                    c.sd = true;
+                    c.sdq = q;
+                    c.sdr = r;
+                    c.tp = tsd;
+                }
             }
         }
         if (c.threads == 0) return c;
@@ -593,72 +704,6 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     return true;
 }
 
-// Slot-dim thread map for a chosen generic tile (kernels.cu tile_sd_kernel):
-// per phase a slot dim outside that side's contiguous run (stride >= run, so
-// a warp still moves along the run) and R slots along it (R | ext preferred);
-// passes Q so that threads * Q * R covers the phase's thread space.  Picks
-// the (Q, R) instantiation with the most CTAs (tiles in flight) per SM, then
-// the best slot fill; false if none fills at least 60 % of its slots within
-// the kernel's launch bound.
-template <typename OccOf>
-static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, OccOf occOf,
-                     int& threads, int& sdq, int& sdr, int& ctasPerSm) {
-    struct Pick { int slot = -1, R = 0, C = 0; double eff = 0; };
-    auto pick_slot = [&](int ph, int RM) {
-        Pick best;
-        for (int t = 0; t < tp.a; ++t) {
-            // outside the phase's contiguous run, or inside it with >= 32
-            // contiguous elements before it (a warp still covers 32 in a row)
-            const int64_t stride = ph == 0 ? tp.tSin[t] : tp.tSout[t];
-            const int64_t before = ph == 0 ? tp.tCin[t] : tp.tCout[t];
-            if (stride < (ph == 0 ? runIn : runOut) && before < 32) continue;
-            const int ext = tp.tExt[t];
-            for (int R = std::min(RM, ext); R >= 1; --R) {
-                const int C = (ext + R - 1) / R;
-                const double eff = (double)ext / ((double)C * R) * ((double)R / RM);
-                if (eff > best.eff + 1e-9) { best.slot = t; best.R = R; best.C = C; best.eff = eff; }
-            }
-        }
-        return best;
-    };
-    double bestFill = 0;
-    TileParams bestTp = tp;
-    for (int cfg = 0; cfg < 3; ++cfg) {
-        const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
-        const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
-        const Pick L = pick_slot(0, RM), S = pick_slot(1, RM);
-        if (L.slot < 0 || S.slot < 0) continue;
-        const int64_t UL = (int64_t)tp.V / tp.tExt[L.slot] * L.C;
-        const int64_t US = (int64_t)tp.V / tp.tExt[S.slot] * S.C;
-        int64_t NT = (std::max(UL, US) + QM - 1) / QM;
-        NT = (NT + 31) / 32 * 32;
-        if (NT < 64) NT = 64;
-        if (NT > (esize >= 8 ? 384 : 512)) continue;  // kernels.cu launch bounds
-        const int64_t QL = (UL + NT - 1) / NT, QS = (US + NT - 1) / NT;
-        // slots issued vs elements moved (per phase); tiles in flight per SM
-        // (CTAs per SM) decide, fill breaks ties
-        const double fill = std::min((double)tp.V / ((double)NT * QL * L.R),
-                                     (double)tp.V / ((double)NT * QS * S.R));
-        const int per = occOf((int)NT, QM, RM);
-        const double score = per + 0.5 * fill;
-        if (fill >= 0.6 && per > 0 && score > bestFill + 1e-9) {
-            ctasPerSm = per;
-            bestFill = score;
-            bestTp = tp;
-            bestTp.sdSlot[0] = L.slot; bestTp.sdR[0] = L.R; bestTp.sdC[0] = L.C;
-            bestTp.sdU[0] = (int32_t)UL; bestTp.sdQ[0] = (int32_t)QL;
-            bestTp.sdSlot[1] = S.slot; bestTp.sdR[1] = S.R; bestTp.sdC[1] = S.C;
-            bestTp.sdU[1] = (int32_t)US; bestTp.sdQ[1] = (int32_t)QS;
-            threads = (int)NT;
-            sdq = QM;
-            sdr = RM;
-        }
-    }
-    if (bestFill <= 0) return false;
-    tp = bestTp;
-    return true;
-}
-
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     // register counts of the tile kernels as compiled (ptxas -v, build/obj)
     int regs;
@@ -752,9 +797,34 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // generic staged tile (Tiled / Packed / PackedSplit classes)
     // 512 threads x 8 slots, and staging byte offsets < 2^16 (16-bit packing)
     const int Vmax = std::min(4096, 57344 / E);
+    // slot-dim map (tile_sd_kernel): 4-byte words and 8-byte words made of
+    // two 4-byte elements by default (on fp64 tensors it measured mixed:
+    // opt-in); larger tiles than the classic map (16 elements x 512 / 384
+    // threads, 16-bit staging offsets)
+    const int sdOpt = opts ? opts->slot_dims : 0;
+    const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3) &&
+                           (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
+                           !(opts && (opts->threads || opts->slots));
+    const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144,
+                                                 (int)knob("TT_KNOB_SD_VMAX", 1 << 20)) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
+    // whole-dimension runs as targets too (no split, no ragged tiles)
+    if (knob("TT_KNOB_PREFIX_TARGETS", 1) != 0) {
+        int64_t P = 1;
+        for (int i = 0; i < pr.n && P * pr.d[i] <= std::max(Vmax, VmaxSd); ++i) {
+            P *= pr.d[i];
+            if (P >= 2) targets.push_back(P);
+        }
+        P = 1;
+        for (int j = 0; j < pr.n && P * pr.d[pr.p[j]] <= std::max(Vmax, VmaxSd); ++j) {
+            P *= pr.d[pr.p[j]];
+            if (P >= 2) targets.push_back(P);
+        }
+        std::sort(targets.begin(), targets.end());
+        targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+    }
     TileCand best;
     const int forceThreads = opts ? opts->threads : 0;
     const int forceR = opts ? opts->slots : 0;
@@ -762,7 +832,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         for (int64_t to : targets) {
             int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
             int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR);
+            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                    VmaxSd);
             if (!c.ok) continue;
             if (!best.ok || c.cost_us < best.cost_us) best = c;
         }
@@ -777,13 +848,14 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     if (!best.ok) return TT_INTERNAL_ERROR;
 
     plan.tile = best.tp;
+    if (!best.sd) plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
     choose_smem(plan.tile, E);
     kc.kernel = TT_KERNEL_TILE;
     kc.threads = best.threads;
     kc.nreg = best.nreg;
     // staging pipeline: register double buffer (default) or a cp.async ring
     // of 3 stages (32-bit indices only)
-    kc.stages = (opts && opts->stages >= 3 && !kc.idx64 && !acc) ? 3 : 0;
+    kc.stages = (opts && opts->stages >= 3 && !kc.idx64 && !acc && !best.sd) ? 3 : 0;
     // interleaved tiles (neighbouring tiles on concurrently running CTAs)
     // measured better than contiguous ranges on 72 of 84 suite cases
     plan.tile.interleave = (opts && opts->grid_order == 2) ? 0 : 1;
@@ -797,32 +869,34 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.m_secIn = best.secIn;
     kc.m_secOut = best.secOut;
     kc.m_inflight = best.inflight;
+    auto occOf = [&](int T, int q, int r) {
+        OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem, false, 0, 0, 0, q, r};
+        int v = occ ? occ(qs, dev) : 0;
+        return v > 0 ? v : estimate_occupancy(qs, dev);
+    };
+    if (best.sd) {
+        // the model picked the slot-dim launch shape (possibly a tile larger
+        // than the classic map can hold)
+        kc.sdq = best.sdq;
+        kc.sdr = best.sdr;
+        const int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm
+                                                  : occOf(kc.threads, kc.sdq, kc.sdr);
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
+    }
     OccQuery q{TT_KERNEL_TILE, E, kc.nreg, kc.stages ? kc.stages : 1, kc.threads, kc.smem,
                kc.idx64, 0, 0, kc.acc};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
-    kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
-    // the generic tile stays in the plan as the fallback for pointers that
-    // are not aligned to the 2-D kernel's vector width
-    // slot-dim thread map (fewer registers per element -> more loads in flight)
-    plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
-    // Used when it keeps more tiles in flight per SM than the classic map
-    // (measured on the suites: the win/loss boundary for 4-byte words and
-    // for 8-byte words made of two 4-byte elements; on fp64 tensors the
-    // slot-dim map measured mixed, so it is opt-in there).
-    {
-        const int sdOpt = opts ? opts->slot_dims : 0;
+    if (!best.sd)
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
+    // The model kept the classic map: switch to the slot-dim map anyway when
+    // it keeps more tiles in flight per SM with the device's real occupancy
+    // (measured on the suites: the win/loss boundary), or when forced.
+    if (!best.sd) {
         int thr = 0, sq = 0, sr = 0, perSd = 0;
-        auto occOf = [&](int T, int q, int r) {
-            OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem, false, 0, 0, 0, q, r};
-            int v = occ ? occ(qs, dev) : 0;
-            return v > 0 ? v : estimate_occupancy(qs, dev);
-        };
         TileParams sdTile = plan.tile;
-        const bool eligible = sdOpt >= 0 && !acc && !kc.idx64 && kc.stages == 0 &&
-                              (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
-                              !(opts && (opts->threads || opts->slots));
-        if (eligible && build_sd(sdTile, E, best.runIn, best.runOut, occOf, thr, sq, sr, perSd) &&
+        if ((sdAllowed || (sdOpt > 0 && !acc && !kc.idx64 && (E == 4 || E == 8))) &&
+            kc.stages == 0 && build_sd(sdTile, E, best.runIn, best.runOut, occOf, thr, sq, sr, perSd) &&
             (sdOpt > 0 || perSd > perSm)) {
             plan.tile = sdTile;
             kc.sdq = sq;

@@ -33,5 +33,5 @@ for g in sorted({k[0] for k in groups}):
     va = [a[k]["frac_memcpy"] for k in common if k.split("_")[0] == g]
     vb = [b[k]["frac_memcpy"] for k in common if k.split("_")[0] == g]
     print(f"{g:5s} all n={len(va)} median {statistics.median(va):.4f} -> {statistics.median(vb):.4f}")
-bad = [k for k in b if not b[k].get("verified", True)]
+bad = [k for k in b if b[k].get("verified") is False]
 print("unverified:", bad)
