@@ -303,7 +303,9 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
     };
     double bestFill = 0;
     TileParams bestTp = tp;
+    const int cfgMask = (int)knob(esize >= 8 ? "TT_KNOB_SD_CFG8" : "TT_KNOB_SD_CFG4", 7);
     for (int cfg = 0; cfg < 3; ++cfg) {
+        if (!(cfgMask & (1 << cfg))) continue;
         const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
         const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
         const Pick L = pick_slot(0, RM), S = pick_slot(1, RM);
