@@ -807,13 +807,18 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3) &&
                            (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                            !(opts && (opts->threads || opts->slots));
+    // Tiles above the classic 4096 elements and whole-dimension run targets
+    // are off by default: on the suites they won and lost by up to 1.5x case
+    // by case with equal medians (tools/knob_sweep.sh), the model cannot
+    // tell them apart; measured planning (tt_plan_measure) reaches them
+    // through forced run targets.
     const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144,
-                                                 (int)knob("TT_KNOB_SD_VMAX", 1 << 20)) : 0;
+                                                 (int)knob("TT_KNOB_SD_VMAX", 4096)) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
     // whole-dimension runs as targets too (no split, no ragged tiles)
-    if (knob("TT_KNOB_PREFIX_TARGETS", 1) != 0) {
+    if (knob("TT_KNOB_PREFIX_TARGETS", 0) != 0) {
         int64_t P = 1;
         for (int i = 0; i < pr.n && P * pr.d[i] <= std::max(Vmax, VmaxSd); ++i) {
             P *= pr.d[i];
@@ -915,11 +920,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // Vectorised 2-D tiled kernel when the tiles are mostly full: it moves
     // VW elements per instruction on both sides (model: its issue cost is a
     // fraction of the generic kernel's, DRAM sectors are whole).
-    // (8-byte words without vectors -- odd extents -- measured faster on the
-    // generic tile: 8 of 10 TTC cases, up to 1.26x, A/B tools/ab_opts.py)
     const bool want2d = forced == TT_KERNEL_TILED2D ||
                         (forced == TT_KERNEL_AUTO && can2d && fill2d >= 0.6 &&
-                         !(E == 8 && vec2d == 1) &&
                          !(opts && (opts->run_in || opts->run_out)));
     if (want2d) {
         kc.kernel = TT_KERNEL_TILED2D;
