@@ -505,7 +505,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         // cost of one launch shape: memory time at the loads in flight it
         // allows, issue time, per-tile latency floor
         auto shape_cost = [&](int T, int slots, int occ, double slotInstr, double& inflight) {
-            inflight = (double)occ * std::min<double>((double)T * slots, tp.V) * E;
+            inflight = (double)occ * T * slots * E;
             const double mlp = std::min(1.0, inflight / model::kInflightBytes);
             const double t_mem = bytes / (model::kBwBytesPerUs * mlp);
             const double warps = T / 32.0;
@@ -807,13 +807,14 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3) &&
                            (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                            !(opts && (opts->threads || opts->slots));
-    // Tiles above the classic 4096 elements and whole-dimension run targets
-    // are off by default: on the suites they won and lost by up to 1.5x case
-    // by case with equal medians (tools/knob_sweep.sh), the model cannot
-    // tell them apart; measured planning (tt_plan_measure) reaches them
-    // through forced run targets.
+    // The slot-dim shape inside the tile model (TT_KNOB_SD_VMAX > 0, tiles up
+    // to 8192 elements) and whole-dimension run targets are off by default:
+    // on the suites they won and lost by up to 2.4x case by case with equal
+    // medians (tools/knob_sweep.sh); the model cannot rank them.  By default
+    // the slot-dim map is applied after the classic tile choice, by real
+    // occupancy (below), which measured no losses.
     const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144,
-                                                 (int)knob("TT_KNOB_SD_VMAX", 4096)) : 0;
+                                                 (int)knob("TT_KNOB_SD_VMAX", 0)) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
