@@ -125,6 +125,32 @@ typedef struct {
 tt_status_t tt_plan(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
                     size_t elem_size, tt_stream_t stream);
 
+/*
+ * tt_plan_strided -- the same permutation between caller-given layouts
+ * (extension beyond P:L167, used by the fused multi-GPU redistribution):
+ *     out[ sum_j x[perm[j]] * out_strides[j] ] = in[ sum_i x[i] * in_strides[i] ]
+ * for every coordinate x, 0 <= x[i] < dims[i].
+ *   in_strides   host array [rank], stride of INPUT dim i in elements (>= 1),
+ *                or NULL for the dense column-major layout of dims.
+ *   out_strides  host array [rank], stride of OUTPUT dim j in elements (>= 1),
+ *                or NULL for the dense layout of the output extents.
+ * The caller guarantees the output positions are distinct (no aliasing); the
+ * library checks strides >= 1 and that both spans fit in 2^62 bytes.  Uses
+ * the generic tile or 2-D kernels (copy, row copy and element widening need
+ * dense layouts); tt_execute_host rejects non-dense plans (TT_UNSUPPORTED).
+ * Executed with tt_execute (in/out = the base addresses of the two layouts).
+ */
+tt_status_t tt_plan_strided(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, const int64_t* in_strides,
+                            const int64_t* out_strides, tt_stream_t stream);
+
+/* tt_plan_strided without a GPU (props/opts as tt_plan_offline); describe only. */
+tt_status_t tt_plan_strided_offline(tt_plan_t* plan, int rank, const int64_t* dims,
+                                    const int* perm, size_t elem_size,
+                                    const int64_t* in_strides, const int64_t* out_strides,
+                                    const tt_device_props_t* props,
+                                    const tt_plan_options_t* opts);
+
 /* tt_plan with planner overrides (opts may be NULL = tt_plan). */
 tt_status_t tt_plan_ex(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
                        size_t elem_size, tt_stream_t stream, const tt_plan_options_t* opts);

@@ -173,6 +173,26 @@ def permute_scaled(dims, perm, words, out_words, alpha: float, beta: float) -> n
     return out
 
 
+def permute_strided(dims, perm, in_buf, in_strides, out_buf, out_strides) -> np.ndarray:
+    """Strided form of the permutation (the layouts of tt_plan_strided):
+    out[sum_j x[perm[j]] * out_strides[j]] = in[sum_i x[i] * in_strides[i]]
+    for every coordinate x (P:L48 scalar positions with caller strides).
+    Returns a copy of ``out_buf`` with those positions written; the rest is
+    left as given.  The definition written out over all coordinates at once
+    (numpy index arithmetic), small and medium sizes."""
+    dims = [int(x) for x in dims]
+    perm = [int(x) for x in perm]
+    n = len(dims)
+    x = np.indices(dims, dtype=np.int64).reshape(n, -1)      # x[i] for every element
+    src = sum(x[i] * int(in_strides[i]) for i in range(n))
+    dst = sum(x[perm[j]] * int(out_strides[j]) for j in range(n))
+    if np.unique(dst).size != dst.size:
+        raise ValueError("output strides map two elements to one position")
+    out = np.array(out_buf, copy=True)
+    out[dst] = np.asarray(in_buf)[src]
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Pure-Python scattered transpose (P:L58) via Eq. (1) (P:L56), small cases.
 # ---------------------------------------------------------------------------

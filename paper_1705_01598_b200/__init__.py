@@ -66,6 +66,10 @@ def _load():
         "tt_plan": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, vp],
         "tt_plan_ex": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, vp,
                        ctypes.POINTER(PlanOptions)],
+        "tt_plan_strided": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, i64p, i64p, vp],
+        "tt_plan_strided_offline": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t,
+                                    i64p, i64p, ctypes.POINTER(DeviceProps),
+                                    ctypes.POINTER(PlanOptions)],
         "tt_plan_offline": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t,
                             ctypes.POINTER(DeviceProps), ctypes.POINTER(PlanOptions)],
         "tt_plan_measure": [ctypes.POINTER(vp), ctypes.c_int, i64p, ip, ctypes.c_size_t, vp, vp, vp,
@@ -142,16 +146,24 @@ class Plan:
     ``perm[j]`` = input dim of output dim j, ``elem_size`` 4 or 8."""
 
     def __init__(self, dims, perm, elem_size: int, stream=None, measure=None,
-                 max_candidates: int = 0, **opts):
+                 max_candidates: int = 0, in_strides=None, out_strides=None, **opts):
         """``measure=(inp, out)``: measurement-based selection on those device
-        buffers (tt_plan_measure) instead of the heuristic."""
+        buffers (tt_plan_measure) instead of the heuristic.  ``in_strides``
+        (per input dim) / ``out_strides`` (per output dim), in elements:
+        a strided plan (tt_plan_strided)."""
         n, d, p = _arrays(dims, perm)
         self.dims, self.perm, self.elem_size = tuple(dims), tuple(perm), int(elem_size)
         self.vol = 1
         for x in self.dims:
             self.vol *= int(x)
         h = ctypes.c_void_p()
-        if measure is not None:
+        if in_strides is not None or out_strides is not None:
+            if measure is not None or opts:
+                raise ValueError("strided plans take no measurement or planner overrides")
+            _check(lib.tt_plan_strided(ctypes.byref(h), n, d, p, self.elem_size,
+                                       _strides(in_strides, n), _strides(out_strides, n),
+                                       _stream_handle(stream)), "tt_plan_strided")
+        elif measure is not None:
             if opts:
                 raise ValueError("measured planning takes no planner overrides")
             _check(lib.tt_plan_measure(ctypes.byref(h), n, d, p, self.elem_size,
@@ -220,14 +232,29 @@ def _describe(h) -> dict:
         return json.loads(buf.value.decode())
 
 
-def plan_offline(dims, perm, elem_size: int, num_sms: int = 148, **opts) -> dict:
+def _strides(st, n):
+    if st is None:
+        return None
+    if len(st) != n:
+        raise ValueError("one stride per dimension")
+    return (ctypes.c_int64 * n)(*[int(x) for x in st])
+
+
+def plan_offline(dims, perm, elem_size: int, num_sms: int = 148, in_strides=None,
+                 out_strides=None, **opts) -> dict:
     """Plan for a described B200 without touching CUDA; returns the JSON plan."""
     n, d, p = _arrays(dims, perm)
     h = ctypes.c_void_p()
     props = DeviceProps(int(num_sms), 0, 0, 0, 0)
     o = _options(**opts)
-    _check(lib.tt_plan_offline(ctypes.byref(h), n, d, p, int(elem_size), ctypes.byref(props),
-                               ctypes.byref(o)), "tt_plan_offline")
+    if in_strides is not None or out_strides is not None:
+        _check(lib.tt_plan_strided_offline(ctypes.byref(h), n, d, p, int(elem_size),
+                                           _strides(in_strides, n), _strides(out_strides, n),
+                                           ctypes.byref(props), ctypes.byref(o)),
+               "tt_plan_strided_offline")
+    else:
+        _check(lib.tt_plan_offline(ctypes.byref(h), n, d, p, int(elem_size), ctypes.byref(props),
+                                   ctypes.byref(o)), "tt_plan_offline")
     try:
         return _describe(h)
     finally:

@@ -50,6 +50,50 @@ tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* pe
     return create_plan_w(out, rank, dims, perm, elem_size, stream, dev, opts, occ, false);
 }
 
+tt_status_t create_plan_s(Plan** out, int rank, const int64_t* dims, const int* perm,
+                          size_t elem_size, void* stream, const DeviceInfo& dev,
+                          const tt_plan_options_t* opts, OccupancyFn occ,
+                          const int64_t* in_str, const int64_t* out_str) {
+    if (in_str == nullptr && out_str == nullptr)
+        return create_plan_w(out, rank, dims, perm, elem_size, stream, dev, opts, occ, false);
+    if (out == nullptr) return TT_INVALID_PARAMETER;
+    *out = nullptr;
+    tt_status_t st = validate(rank, dims, perm, elem_size);
+    if (st != TT_SUCCESS) return st;
+    if (opts && (opts->accumulate || opts->stages >= 3)) return TT_UNSUPPORTED;
+    // dense defaults for the side not given; strides >= 1 (no broadcast: the
+    // map must stay one-to-one on the output)
+    int64_t si[kMaxDims], so[kMaxDims];
+    int64_t acc = 1;
+    for (int i = 0; i < rank; ++i) { si[i] = in_str ? in_str[i] : acc; acc *= dims[i]; }
+    acc = 1;
+    for (int j = 0; j < rank; ++j) { so[j] = out_str ? out_str[j] : acc; acc *= dims[perm[j]]; }
+    long double maxIn = 0, maxOut = 0;
+    for (int i = 0; i < rank; ++i) {
+        if (si[i] < 1 || so[i] < 1) return TT_INVALID_PARAMETER;
+        maxIn += (long double)(dims[i] - 1) * si[i];
+        maxOut += (long double)(dims[perm[i]] - 1) * so[i];
+    }
+    if ((maxIn + 1) * elem_size >= (long double)(1LL << 62) ||
+        (maxOut + 1) * elem_size >= (long double)(1LL << 62))
+        return TT_INVALID_PARAMETER;
+    Plan* p = new (std::nothrow) Plan();
+    if (p == nullptr) return TT_INTERNAL_ERROR;
+    p->device = dev.device;
+    p->stream = stream;
+    p->rank = rank;
+    p->dims.assign(dims, dims + rank);
+    p->perm.assign(perm, perm + rank);
+    p->prob = normalize_strided(rank, dims, perm, (int)elem_size, si, so, !(opts && opts->no_fusion));
+    st = choose_plan(*p, dev, opts, occ);
+    if (st != TT_SUCCESS) {
+        delete p;
+        return st;
+    }
+    *out = p;
+    return TT_SUCCESS;
+}
+
 tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* perm,
                           size_t elem_size, void* stream, const DeviceInfo& dev,
                           const tt_plan_options_t* opts, OccupancyFn occ, bool widenForced) {
@@ -390,6 +434,48 @@ tt_status_t tt_plan_offline(tt_plan_t* plan, int rank, const int64_t* dims, cons
     return make_plan(plan, rank, dims, perm, elem_size, nullptr, dev, opts, nullptr);
 }
 
+static void props_to_dev(const tt_device_props_t* props, DeviceInfo& dev) {
+    dev.device = -1;
+    if (!props) return;
+    if (props->num_sms > 0) dev.num_sms = props->num_sms;
+    if (props->max_smem_per_block > 0) dev.max_smem_per_block = props->max_smem_per_block;
+    if (props->max_smem_per_sm > 0) dev.max_smem_per_sm = props->max_smem_per_sm;
+    if (props->max_threads_per_sm > 0) dev.max_threads_per_sm = props->max_threads_per_sm;
+    if (props->regs_per_sm > 0) dev.regs_per_sm = props->regs_per_sm;
+}
+
+tt_status_t tt_plan_strided(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                            size_t elem_size, const int64_t* in_strides, const int64_t* out_strides,
+                            tt_stream_t stream) {
+    if (plan == nullptr) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    tt_status_t st = validate(rank, dims, perm, elem_size);
+    if (st != TT_SUCCESS) return st;
+    DeviceInfo dev;
+    st = query_device(dev);
+    if (st != TT_SUCCESS) return st;
+    Plan* p = nullptr;
+    st = create_plan_s(&p, rank, dims, perm, elem_size, stream, dev, nullptr, &cuda_occupancy,
+                       in_strides, out_strides);
+    *plan = reinterpret_cast<tt_plan_t>(p);
+    return st;
+}
+
+tt_status_t tt_plan_strided_offline(tt_plan_t* plan, int rank, const int64_t* dims, const int* perm,
+                                    size_t elem_size, const int64_t* in_strides,
+                                    const int64_t* out_strides, const tt_device_props_t* props,
+                                    const tt_plan_options_t* opts) {
+    if (plan == nullptr) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    DeviceInfo dev;
+    props_to_dev(props, dev);
+    Plan* p = nullptr;
+    tt_status_t st = create_plan_s(&p, rank, dims, perm, elem_size, nullptr, dev, opts, nullptr,
+                                   in_strides, out_strides);
+    *plan = reinterpret_cast<tt_plan_t>(p);
+    return st;
+}
+
 static tt_status_t check_exec(Plan* p, const void* in, void* out) {
     if (p == nullptr) return TT_INVALID_PLAN;
     if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
@@ -430,6 +516,7 @@ tt_status_t tt_execute_host(tt_plan_t plan, const void* host_in, void* host_out,
     tt_status_t st = check_exec(p, dev_in, dev_out);
     if (st != TT_SUCCESS) return st;
     if (p->shard) return TT_INVALID_PLAN;
+    if (!p->prob.dense) return TT_UNSUPPORTED;  // host path: dense tensors only
     const size_t bytes = (size_t)p->prob.vol * (size_t)p->prob.esize;
     cudaStream_t s = static_cast<cudaStream_t>(p->stream);
     if (bytes >= kPipeMinBytes) {

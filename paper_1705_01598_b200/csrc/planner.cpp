@@ -46,6 +46,7 @@ static void fill_strides(Problem& pr) {
     acc = 1;
     for (int j = 0; j < pr.n; ++j) { pr.sout[pr.p[j]] = acc; acc *= pr.d[pr.p[j]]; }
     pr.vol = acc;
+    pr.span = acc;
 }
 
 Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, bool fuse) {
@@ -100,12 +101,84 @@ Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, boo
     return pr;
 }
 
+// Strided problems (tt_plan_strided): the same Eq. (1) map between
+// caller-given layouts, in[sum_i x_i s_in(i)] -> out[sum_j x_{p(j)} s_out(j)].
+// Extent-1 dims are dropped; input dims i, i+1 that are consecutive in the
+// output order are fused only when both layouts make them one dimension
+// (s_in(i+1) = s_in(i) d_i and the same on the output side).
+Problem normalize_strided(int rank, const int64_t* dims, const int* perm, int esize,
+                          const int64_t* in_str, const int64_t* out_str, bool fuse) {
+    Problem pr;
+    pr.esize = esize;
+    pr.dense = false;
+    int64_t si[kMaxDims], so[kMaxDims];  // per input dim
+    for (int i = 0; i < rank; ++i) si[i] = in_str[i];
+    for (int j = 0; j < rank; ++j) so[perm[j]] = out_str[j];
+    // keep dims with extent > 1, in output order
+    int keep[kMaxDims], m = 0;
+    for (int j = 0; j < rank; ++j)
+        if (dims[perm[j]] > 1) keep[m++] = perm[j];
+    if (m == 0) {
+        pr.n = 1; pr.d[0] = 1; pr.p[0] = 0; pr.sin[0] = 1; pr.sout[0] = 1;
+        pr.vol = 1; pr.span = 1;
+        return pr;
+    }
+    // fuse output-order neighbours (a, b) with b = next input dim after a
+    // among kept dims and contiguous strides on both sides
+    int64_t gd[kMaxDims], gsi[kMaxDims], gso[kMaxDims];
+    int gfirst[kMaxDims], ng = 0;
+    for (int q = 0; q < m;) {
+        const int a = keep[q];
+        int64_t d = dims[a];
+        int last = a, len = 1;
+        while (fuse && q + len < m) {
+            const int b = keep[q + len];
+            bool nextIn = b > last;
+            for (int i = last + 1; i < b && nextIn; ++i) nextIn = dims[i] == 1;
+            if (!nextIn || si[b] != si[a] * d || so[b] != so[a] * d) break;
+            d *= dims[b];
+            last = b;
+            ++len;
+        }
+        gd[ng] = d; gsi[ng] = si[a]; gso[ng] = so[a]; gfirst[ng] = a; ++ng;
+        q += len;
+    }
+    // input order of the groups = ascending first input dim
+    int order[kMaxDims];
+    for (int g = 0; g < ng; ++g) order[g] = g;
+    std::sort(order, order + ng, [&](int x, int y) { return gfirst[x] < gfirst[y]; });
+    int rankOf[kMaxDims];
+    for (int r = 0; r < ng; ++r) {
+        const int g = order[r];
+        rankOf[g] = r;
+        pr.d[r] = gd[g];
+        pr.sin[r] = gsi[g];
+        pr.sout[r] = gso[g];
+    }
+    pr.n = ng;
+    for (int g = 0; g < ng; ++g) pr.p[g] = rankOf[g];
+    int64_t vol = 1, maxIn = 0, maxOut = 0;
+    for (int i = 0; i < ng; ++i) {
+        vol *= pr.d[i];
+        maxIn += (pr.d[i] - 1) * pr.sin[i];
+        maxOut += (pr.d[i] - 1) * pr.sout[i];
+    }
+    pr.vol = vol;
+    pr.span = std::max(maxIn, maxOut) + 1;
+    // the same layout as the dense problem of these dims: plan it as dense
+    Problem dn = normalize(ng, pr.d, pr.p, esize, false);
+    bool same = true;
+    for (int i = 0; i < ng; ++i) same = same && dn.sin[i] == pr.sin[i] && dn.sout[i] == pr.sout[i];
+    if (same) { dn.dense = true; return dn; }
+    return pr;
+}
+
 // Element widening: when the fastest dim is unchanged (perm[0] == 0) every
 // row of d0 elements is contiguous on both sides, so k consecutive elements
 // can move as one (E*k)-byte word when k divides d0 (bit-exact: the words are
 // opaque).  Returns k in {1, 2, 4} (E*k <= 16).
 int widen_factor(const Problem& pr) {
-    if (pr.n < 2 || pr.p[0] != 0) return 1;
+    if (!pr.dense || pr.n < 2 || pr.p[0] != 0) return 1;
     const int kmax = 16 / pr.esize;
     for (int k = kmax; k >= 2; k /= 2)
         if (pr.d[0] % k == 0) return k;
@@ -501,7 +574,7 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
         // DRAM bytes scale with the elements actually moved (ragged tiles move
         // fewer), issue cost with the tiles launched (ragged slots still issue)
         const double bytes = (double)pr.vol / tp.V * modelSec * model::kSector;
-        const bool idx64 = pr.vol >= (int64_t(1) << 31);
+        const bool idx64 = pr.span >= (int64_t(1) << 31);
         // cost of one launch shape: memory time at the loads in flight it
         // allows, issue time, per-tile latency floor
         auto shape_cost = [&](int T, int slots, int occ, double slotInstr, double& inflight) {
@@ -645,12 +718,24 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
                           double& fill, int wantA, int wantB, int order) {
     if (pr.n < 2 || pr.p[0] == 0) return false;
     const int B = pr.p[0];
+    // the kernels index in[b*sInB + a] and out[a*sOutA + b]: unit strides
+    // for A on the input side and for B on the output side
+    if (pr.sin[0] != 1 || pr.sout[B] != 1) return false;
     const int64_t dA = pr.d[0], dB = pr.d[B];
+    // vectors of v elements: every row start a multiple of v on both sides
+    auto vec_ok = [&](int v) {
+        if (dA % v || dB % v) return false;
+        for (int i = 0; i < pr.n; ++i) {
+            if (i != 0 && pr.sin[i] % v) return false;
+            if (i != B && pr.sout[i] % v) return false;
+        }
+        return true;
+    };
     vec = 0;
     if (pr.esize == 4) {
-        if (dA % 4 == 0 && dB % 4 == 0) vec = 4;
-        else if (dA % 2 == 0 && dB % 2 == 0) vec = 2;
-    } else if (dA % 2 == 0 && dB % 2 == 0) {
+        if (vec_ok(4)) vec = 4;
+        else if (vec_ok(2)) vec = 2;
+    } else if (vec_ok(2)) {
         vec = 2;
     }
     if (vec == 0) vec = 1;  // scalar 2-D kernel (padded staging)
@@ -734,14 +819,15 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const int forced = opts ? opts->kernel : TT_KERNEL_AUTO;
     const int E = pr.esize;
 
-    kc.idx64 = pr.vol >= (int64_t(1) << 31);
+    kc.idx64 = pr.span >= (int64_t(1) << 31);
     const bool acc = opts && opts->accumulate;
     if (acc && (kc.idx64 || E > 8 || (forced != TT_KERNEL_AUTO && forced != TT_KERNEL_TILE)))
         return TT_UNSUPPORTED;
     kc.acc = acc ? 1 : 0;
 
     // (i) rank 1 after fusion: copy (identity; "trivial" permutation)
-    if (!acc && pr.n == 1 && (forced == TT_KERNEL_AUTO || forced == TT_KERNEL_COPY)) {
+    // (strided problems: the copy and row-copy kernels assume dense layouts)
+    if (!acc && pr.n == 1 && pr.dense && (forced == TT_KERNEL_AUTO || forced == TT_KERNEL_COPY)) {
         kc.kernel = TT_KERNEL_COPY;
         kc.threads = opts && opts->threads ? opts->threads : 512;
         kc.vec = 16 / E;
@@ -755,7 +841,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     if (forced == TT_KERNEL_COPY) return TT_UNSUPPORTED;
 
     // (ii) fastest dim unchanged with long rows: row copy, no staging
-    const bool rowClass = pr.n >= 2 && pr.p[0] == 0;
+    const bool rowClass = pr.n >= 2 && pr.p[0] == 0 && pr.dense;
     if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
     if (!acc && rowClass && (forced == TT_KERNEL_ROWCOPY ||
                      (forced == TT_KERNEL_AUTO && pr.d[0] * E >= 512 &&
@@ -986,7 +1072,8 @@ std::string describe_json(const Plan& plan) {
       << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
       << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
-      << ",\"model_dram_eff\":" << kc.model_dram_eff << ",\"widen\":" << plan.widen;
+      << ",\"model_dram_eff\":" << kc.model_dram_eff << ",\"widen\":" << plan.widen
+      << ",\"dense\":" << (pr.dense ? "true" : "false") << ",\"span\":" << (long long)pr.span;
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D)
         o << ",\"model\":{\"run_in\":" << kc.m_runIn << ",\"run_out\":" << kc.m_runOut
           << ",\"sec_in\":" << kc.m_secIn << ",\"sec_out\":" << kc.m_secOut

@@ -23,6 +23,8 @@ struct Problem {
     int p[kMaxDims] = {};
     int esize = 4;
     int widen = 1;                // words are `widen` caller elements (planner.cpp widen_problem)
+    bool dense = true;            // false: caller-given strides (tt_plan_strided)
+    int64_t span = 1;             // 1 + the largest element offset on either side (index width)
     int64_t vol = 1;
     int64_t sin[kMaxDims] = {};   // c(i, I): input stride of input dim i
     int64_t sout[kMaxDims] = {};  // c(i, O): output stride of input dim i
@@ -188,6 +190,9 @@ struct Plan {
 void magic_u31(uint32_t d, uint32_t& m, uint32_t& l);
 tt_status_t validate(int rank, const int64_t* dims, const int* perm, size_t elem_size);
 Problem normalize(int rank, const int64_t* dims, const int* perm, int esize, bool fuse);
+// Strided form: in_str per input dim, out_str per OUTPUT dim (elements).
+Problem normalize_strided(int rank, const int64_t* dims, const int* perm, int esize,
+                          const int64_t* in_str, const int64_t* out_str, bool fuse);
 int widen_factor(const Problem& pr);
 Problem widen_problem(const Problem& pr, int k);
 tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
@@ -201,6 +206,10 @@ tt_status_t query_device(DeviceInfo& dev);
 tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
                         size_t elem_size, void* stream, const DeviceInfo& dev,
                         const tt_plan_options_t* opts, OccupancyFn occ);
+tt_status_t create_plan_s(Plan** out, int rank, const int64_t* dims, const int* perm,
+                          size_t elem_size, void* stream, const DeviceInfo& dev,
+                          const tt_plan_options_t* opts, OccupancyFn occ,
+                          const int64_t* in_str, const int64_t* out_str);
 tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* perm,
                           size_t elem_size, void* stream, const DeviceInfo& dev,
                           const tt_plan_options_t* opts, OccupancyFn occ, bool widenForced);

@@ -365,3 +365,38 @@ def test_execute_host_pipelined(dims, perm, esize):
         np.testing.assert_array_equal(hout.numpy().view(words.dtype), orc.permute_threaded(dims, perm, words))
         hout.zero_()
     plan.destroy()
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+def test_strided_plans(esize):
+    """tt_plan_strided on the GPU vs the strided oracle: padded and reordered
+    layouts, positions outside the output layout untouched."""
+    from test_planner_cpu import strided_layout
+    rng = np.random.default_rng(7 + esize)
+    for it in range(12):
+        rank = int(rng.integers(2, 7))
+        dims = tuple(int(x) for x in rng.integers(1, 14 if rank > 3 else 200, size=rank))
+        perm = tuple(int(x) for x in rng.permutation(rank))
+        sin, nin, sout, nout = strided_layout(rng, dims, perm)
+        inbuf = wl.random_words(nin, esize, it)
+        outbuf = wl.random_words(nout, esize, 100 + it)
+        want = orc.permute_strided(dims, perm, inbuf, sin, outbuf, sout)
+        x = to_dev(inbuf)
+        y = to_dev(outbuf)
+        plan = tt.Plan(dims, perm, esize, in_strides=sin, out_strides=sout)
+        plan.execute(x, y)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy().view(want.dtype)
+        np.testing.assert_array_equal(got, want, err_msg=f"{dims} {perm} {sin} {sout}")
+        plan.destroy()
+    # a 2-D transpose between padded row pitches (vector 2-D kernel)
+    dims, perm, sin, sout = (256, 192), (1, 0), (1, 260), (1, 196)
+    inbuf = wl.random_words(260 * 192, esize, 3)
+    outbuf = wl.random_words(196 * 256, esize, 4)
+    plan = tt.Plan(dims, perm, esize, in_strides=sin, out_strides=sout)
+    assert plan.describe()["kernel"] == "tiled2d"
+    y = to_dev(outbuf)
+    plan.execute(to_dev(inbuf), y)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy().view(outbuf.dtype),
+                                  orc.permute_strided(dims, perm, inbuf, sin, outbuf, sout))

@@ -256,3 +256,35 @@ def test_workload_generators():
     np.testing.assert_array_equal(wl.random_words(10, 4, 5), wl.random_words(10, 4, 5))
     assert wl.random_words(10, 8, 5).dtype == np.uint64
     assert wl.s1().vol == 16384 * 16384
+
+
+def test_permute_strided_pins():
+    """Strided oracle form: dense strides reduce to the C gather odometer;
+    a brute-force loop over coordinates on a padded, reordered layout."""
+    import itertools
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        rank = int(rng.integers(1, 5))
+        dims = [int(x) for x in rng.integers(1, 6, size=rank)]
+        perm = [int(x) for x in rng.permutation(rank)]
+        vol = int(np.prod(dims))
+        words = rng.integers(0, 2**32, size=vol, dtype=np.uint64).astype(np.uint32)
+        din = [int(np.prod(dims[:i])) for i in range(rank)]
+        dout = [int(np.prod([dims[perm[k]] for k in range(j)])) for j in range(rank)]
+        got = orc.permute_strided(dims, perm, words, din, np.zeros(vol, np.uint32), dout)
+        np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
+        # padded extents, memory order of the output layout reversed
+        pin = [d + int(rng.integers(0, 3)) for d in dims]
+        sin = [int(np.prod(pin[:i])) for i in range(rank)]
+        pout = [dims[perm[j]] + int(rng.integers(0, 3)) for j in range(rank)]
+        sout = [0] * rank
+        acc = 1
+        for j in reversed(range(rank)):
+            sout[j] = acc
+            acc *= pout[j]
+        inbuf = rng.integers(0, 2**32, size=int(np.prod(pin)), dtype=np.uint64).astype(np.uint32)
+        outbuf = np.full(acc, 7, np.uint32)
+        want = outbuf.copy()
+        for x in itertools.product(*[range(d) for d in dims]):
+            want[sum(x[perm[j]] * sout[j] for j in range(rank))] = inbuf[sum(x[i] * sin[i] for i in range(rank))]
+        np.testing.assert_array_equal(orc.permute_strided(dims, perm, inbuf, sin, outbuf, sout), want)

@@ -250,3 +250,57 @@ def test_slot_dim_map_used_on_suites():
         if j["kernel"] == "tile" and c.esize == 8:   # fp64 words: opt-in only
             sd8 += "sd" in j["tile"]
     assert n > 20 and sd >= n // 2 and sd8 == 0
+
+
+def strided_layout(rng, dims, perm):
+    """Random padded / reordered layouts for a strided plan test: input
+    strides from padded extents in a random memory order, output strides
+    likewise over the output dims.  Returns (sin, in_size, sout, out_size)."""
+    rank = len(dims)
+
+    def layout(ext):
+        order = list(range(rank))
+        if rng.random() < 0.5:
+            order = [int(v) for v in rng.permutation(rank)]
+        st = [0] * rank
+        acc = 1
+        for k in order:
+            st[k] = acc
+            acc *= ext[k] + int(rng.integers(0, 3))
+        return st, acc
+
+    sin, nin = layout(list(dims))
+    sout, nout = layout([dims[perm[j]] for j in range(rank)])
+    return sin, nin, sout, nout
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_strided_plans_match_oracle(seed):
+    """tt_plan_strided geometry (offline plan replayed on the host) against
+    the strided oracle: padded and reordered layouts on both sides."""
+    rng = np.random.default_rng(100 + seed)
+    rank = int(rng.integers(2, 7))
+    dims = tuple(int(x) for x in rng.integers(1, 12, size=rank))
+    perm = tuple(int(x) for x in rng.permutation(rank))
+    esize = 4 if seed % 2 == 0 else 8
+    sin, nin, sout, nout = strided_layout(rng, dims, perm)
+    inbuf = wl.random_words(nin, esize, seed)
+    outbuf = np.zeros(nout, dtype=inbuf.dtype)
+    want = orc.permute_strided(dims, perm, inbuf, sin, outbuf, sout)
+    j = tt.plan_offline(dims, perm, esize, in_strides=sin, out_strides=sout)
+    assert j["kernel"] in ("tile", "tiled2d")
+    fj = dict(j)
+    fj["dims"] = j["fused"]["dims"]
+    got = interpret_tile_plan(fj, inbuf, out=outbuf.copy())
+    np.testing.assert_array_equal(got, want)
+    if j["kernel"] == "tiled2d":
+        np.testing.assert_array_equal(interpret_tiled2d_plan(fj, inbuf, out=outbuf.copy()), want)
+
+
+def test_strided_plan_validation():
+    with pytest.raises(tt.TTError):
+        tt.plan_offline((4, 5), (1, 0), 4, in_strides=(1, 0))       # stride 0
+    j = tt.plan_offline((4, 5), (1, 0), 4, in_strides=(1, 4), out_strides=(1, 5))
+    assert j["dense"] is True and j["kernel"] in ("tiled2d", "tile")   # dense layout recognised
+    j = tt.plan_offline((64, 64), (1, 0), 4, in_strides=(1, 66), out_strides=(1, 68))
+    assert j["dense"] is False and j["kernel"] == "tiled2d" and j["vec"] == 2
