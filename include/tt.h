@@ -291,6 +291,73 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
  * (synchronises on that execution); zeros for the local case. */
 tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3);
 
+/* ------------------------------------------------------------------------
+ * Fused redistribution (SURVEY f-1): the permutation kernels store straight
+ * into the peers' output slabs over NVLink / NVSwitch -- no pack, no NCCL
+ * copy, no unpack (2 x shard bytes of HBM traffic instead of ~6x).
+ *
+ * Geometry (same sharded layout as above; t = perm[n-1] != n-1, c =
+ * global_dims[t]/nranks, j* the output position of input dim n-1): rank r's
+ * slab is cut along input dim t into nranks sub-boxes x_t in [q*c, (q+1)*c);
+ * sub-box q is a contiguous range of output dim j* of output slab q, at
+ * y_{j*} = r*global_dims[n-1]/nranks + x_{n-1}.  Every sub-box is the same
+ * strided permutation (tt_plan_strided) with different base pointers, so one
+ * execute = nranks launches of one plan, own slab last.  t == n-1 is the
+ * local case (one launch into the own slab).
+ * ---------------------------------------------------------------------- */
+
+/*
+ * tt_plan_sharded_p2p -- fused plan for process `proc` of `nranks` (1..64)
+ * on the current device.
+ *   comm  NULL: single-process form -- execute with tt_execute_sharded_p2p,
+ *         giving every rank's output slab as a pointer valid in this process
+ *         (one process driving several GPUs with peer access enabled, or
+ *         several slabs on one GPU).  Non-NULL: the multi-process form; nranks
+ *         and proc must equal the communicator's (else TT_INVALID_PARAMETER);
+ *         call tt_sharded_register_output once, then tt_execute_sharded.
+ * Divisibility rules and errors as tt_plan_sharded.  No device allocation.
+ */
+tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int rank,
+                                const int64_t* global_dims, const int* perm, size_t elem_size,
+                                tt_stream_t stream);
+
+/* tt_plan_sharded_p2p geometry without a GPU (describe only): "mode" "p2p",
+ * "fused" (the strided sub-box plan), "in_step" / "out_offset" (elements),
+ * "dest_order". */
+tt_status_t tt_plan_sharded_p2p_offline(tt_plan_t* plan, int nranks, int proc, int rank,
+                                        const int64_t* global_dims, const int* perm,
+                                        size_t elem_size);
+
+/*
+ * tt_sharded_register_output -- collective over the plan's communicator:
+ * every rank passes the device buffer that will receive its output slab
+ * (shard bytes, anywhere inside a cudaMalloc'd allocation).  CUDA IPC handles
+ * of the buffers and of a small signal array (allocated here, freed by
+ * tt_destroy) are all-gathered with NCCL and opened.  Once per plan; the
+ * buffer must stay allocated while the plan lives.  Synchronises the plan's
+ * stream.  TT_INVALID_PLAN for plans without a communicator.
+ */
+tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local);
+
+/*
+ * tt_execute_sharded_p2p -- single-process form: in_local = this process's
+ * input slab (device pointer), out_slabs = host array [nranks] of every
+ * rank's output slab, each writable from the plan's device.  Enqueues the
+ * nranks sub-box launches on the plan's stream; NO barrier -- the caller
+ * orders the ranks' executes against readers of the slabs.
+ *
+ * tt_execute_sharded on a registered p2p plan (out_local must be the
+ * registered buffer, else TT_INVALID_PARAMETER) runs: entry barrier (every
+ * peer reached this execute on its stream, so its slab is free), the
+ * sub-box launches, exit barrier (every peer's stores into this slab have
+ * landed).  The barriers are system-scope release/acquire signal words in
+ * device memory; a peer missing for 30 s sets an error word instead of
+ * hanging, reported by tt_sharded_timings as TT_CUDA_ERROR.
+ * tt_sharded_timings then returns (entry barrier, fused permute, exit
+ * barrier) milliseconds.
+ */
+tt_status_t tt_execute_sharded_p2p(tt_plan_t plan, const void* in_local, void* const* out_slabs);
+
 /* Shard geometry: local input dims and local output dims (output order),
  * `rank` entries each (either pointer may be NULL). */
 tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* local_out_dims);

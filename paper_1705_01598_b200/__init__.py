@@ -88,6 +88,12 @@ def _load():
         "tt_sharded_timings": [vp, ctypes.POINTER(ctypes.c_float)],
         "tt_execute_sharded": [vp, vp, vp],
         "tt_plan_shard_dims": [vp, i64p, i64p],
+        "tt_plan_sharded_p2p": [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                i64p, ip, ctypes.c_size_t, vp],
+        "tt_plan_sharded_p2p_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        i64p, ip, ctypes.c_size_t],
+        "tt_sharded_register_output": [vp, vp],
+        "tt_execute_sharded_p2p": [vp, vp, ctypes.POINTER(vp)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -289,4 +295,5 @@ def permute_torch(x, axes, out=None, stream=None, **opts):
     return out
 
 
-from ._dist import Comm, ShardedPlan, unique_id, plan_sharded_offline  # noqa: E402
+from ._dist import (Comm, ShardedPlan, P2PShardedPlan, unique_id, plan_sharded_offline,  # noqa: E402
+                    plan_sharded_p2p_offline)

@@ -2,7 +2,9 @@
 
 One process per GPU.  The NCCL unique id is created by rank 0 through the
 library and broadcast with ``torch.distributed`` (plumbing only); the
-exchange itself is the library's ncclAlltoAll on the plan's stream.
+exchange itself is the library's ncclAlltoAll on the plan's stream
+(``ShardedPlan``), or the fused form (``P2PShardedPlan``, SURVEY f-1) whose
+permute kernels store straight into the peers' output slabs.
 """
 from __future__ import annotations
 
@@ -98,6 +100,63 @@ class ShardedPlan:
             self.destroy()
         except Exception:
             pass
+
+
+class P2PShardedPlan(ShardedPlan):
+    """Fused redistribution (tt_plan_sharded_p2p): the permutation kernels
+    write every destination sub-box straight into its rank's output slab.
+
+    ``comm`` given: multi-process form -- ``register_output(buf)`` once
+    (collective), then ``execute(in_local, buf)`` (collective; device-side
+    entry/exit barriers).  ``comm=None``: single-process form for process
+    ``proc`` of ``nranks`` -- ``execute_slabs(in_local, [out_0, ...])`` with
+    every rank's output slab as a device tensor (no barriers)."""
+
+    def __init__(self, comm, global_dims, perm, elem_size: int, stream=None, nranks=None,
+                 proc=None):
+        n, d, p = _arrays(global_dims, perm)
+        self.comm = comm
+        if comm is not None:
+            nranks, proc = comm.nranks, comm.rank
+        if nranks is None or proc is None:
+            raise ValueError("nranks and proc are required without a communicator")
+        self.nranks, self.proc = int(nranks), int(proc)
+        self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
+        h = ctypes.c_void_p()
+        _check(lib.tt_plan_sharded_p2p(ctypes.byref(h), comm._h if comm is not None else None,
+                                       self.nranks, self.proc, n, d, p, self.elem_size,
+                                       _stream_handle(stream)), "tt_plan_sharded_p2p")
+        self._h = h
+        a = (ctypes.c_int64 * n)()
+        b = (ctypes.c_int64 * n)()
+        _check(lib.tt_plan_shard_dims(h, a, b), "tt_plan_shard_dims")
+        self.local_in_dims = tuple(a)
+        self.local_out_dims = tuple(b)
+        self._registered = None
+
+    def register_output(self, out_local) -> None:
+        _check(lib.tt_sharded_register_output(self._h, _ptr(out_local)),
+               "tt_sharded_register_output")
+        self._registered = out_local   # keep the buffer alive with the plan
+
+    def execute_slabs(self, in_local, out_slabs) -> None:
+        if len(out_slabs) != self.nranks:
+            raise ValueError(f"need {self.nranks} output slabs")
+        arr = (ctypes.c_void_p * self.nranks)(*[_ptr(o) for o in out_slabs])
+        _check(lib.tt_execute_sharded_p2p(self._h, _ptr(in_local), arr), "tt_execute_sharded_p2p")
+
+
+def plan_sharded_p2p_offline(nranks: int, proc: int, global_dims, perm, elem_size: int) -> dict:
+    """Fused-redistribution geometry for process ``proc`` of ``nranks``
+    without a GPU (JSON description: "fused", "in_step", "out_offset")."""
+    n, d, p = _arrays(global_dims, perm)
+    h = ctypes.c_void_p()
+    _check(lib.tt_plan_sharded_p2p_offline(ctypes.byref(h), int(nranks), int(proc), n, d, p,
+                                           int(elem_size)), "tt_plan_sharded_p2p_offline")
+    try:
+        return _describe(h)
+    finally:
+        lib.tt_destroy(h)
 
 
 def plan_sharded_offline(nranks: int, proc: int, global_dims, perm, elem_size: int) -> dict:

@@ -17,7 +17,24 @@
 //                             moving the source rank next to the output
 //                             position j* of input dim n-1 (p[j*] = n-1).
 //
-// Both local steps are ordinary single-GPU plans (planner.cpp + kernels.cu).
+//   t != n-1  "p2p" (SURVEY f-1, fused): no pack, no NCCL copy, no unpack.
+//             Rank r's slab splits along input dim t into P sub-boxes
+//             x_t in [q*c, (q+1)*c), c = D[t]/P; sub-box q lands in output
+//             slab q (on rank q's GPU) as a contiguous range of output dim
+//             j* (p[j*] = n-1), at y_{j*} = r*D[n-1]/P + x_{n-1}.  All P
+//             sub-boxes share ONE strided plan (tt_plan_strided geometry):
+//             extents = slab with dim t cut to c, input strides = the slab's,
+//             output strides = the output slab's; only the base pointers
+//             differ: in + q*c*S_in[t], out_q + r*(D[n-1]/P)*S_out[j*].
+//             The permute kernel stores straight into the peers' output
+//             slabs over NVLink (CUDA IPC mappings), so HBM traffic is the
+//             2S minimum and the transfer overlaps the permutation tile by
+//             tile.  Two device-side barriers over IPC-mapped signal words
+//             (entry: peers are done with their output slabs; exit: all
+//             stores into mine have landed) replace the collective.
+//
+// All local steps are ordinary single-GPU plans (planner.cpp + kernels.cu).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -53,6 +70,18 @@ struct ShardInfo {
     std::vector<int64_t> local_in, local_out;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool timed = false;
+    // p2p mode (f-1)
+    bool p2p = false;
+    int proc = 0;                   // this process's slab index
+    Plan* fused = nullptr;          // one strided plan for every destination sub-box
+    int64_t in_step = 0;            // elements between destination sub-boxes in the input slab
+    int64_t out_off = 0;            // this rank's block inside every output slab (elements)
+    void* reg_out = nullptr;        // registered output slab (tt_sharded_register_output)
+    std::vector<void*> peer_out;    // [P] output slabs as mapped in this process
+    std::vector<void*> ipc_bases;   // peer allocations opened with cudaIpcOpenMemHandle
+    int* sig = nullptr;             // [P] signal words of this rank (device), + [P] error word
+    std::vector<int*> peer_sig;     // [P] peers' signal arrays as mapped here
+    int epoch = 0;
 };
 
 void destroy_shard(ShardInfo* s) {
@@ -60,6 +89,9 @@ void destroy_shard(ShardInfo* s) {
     destroy_plan(s->local);
     destroy_plan(s->pack);
     destroy_plan(s->unpack);
+    destroy_plan(s->fused);
+    for (void* b : s->ipc_bases) cudaIpcCloseMemHandle(b);
+    if (s->sig) cudaFree(s->sig);
     if (s->send) cudaFree(s->send);
     if (s->recv) cudaFree(s->recv);
     for (auto& e : s->ev)
@@ -69,6 +101,7 @@ void destroy_shard(ShardInfo* s) {
 
 int shard_launches(const ShardInfo* s) {
     if (!s->redistribute) return 1;
+    if (s->p2p) return s->nranks + (s->comm ? 2 : 0);  // P sub-box launches (+ 2 barriers)
     return s->nranks > 1 ? 3 : 2;  // pack, (NCCL all-to-all), unpack
 }
 
@@ -81,7 +114,8 @@ std::string describe_shard_json(const Plan& plan) {
         o << "]";
     };
     o << "{\"version\":" << TT_VERSION << ",\"sharded\":true,\"nranks\":" << s->nranks
-      << ",\"rank\":" << s->rank << ",\"mode\":\"" << (s->redistribute ? "redistribute" : "local")
+      << ",\"rank\":" << s->rank << ",\"mode\":\""
+      << (s->redistribute ? (s->p2p ? "p2p" : "redistribute") : "local")
       << "\",\"elem_size\":" << s->esize << ",\"global_dims\":";
     arr(plan.dims);
     o << ",\"perm\":[";
@@ -95,6 +129,12 @@ std::string describe_shard_json(const Plan& plan) {
     if (s->local) o << ",\"local\":" << describe_json(*s->local);
     if (s->pack) o << ",\"pack\":" << describe_json(*s->pack);
     if (s->unpack) o << ",\"unpack\":" << describe_json(*s->unpack);
+    if (s->fused) {
+        o << ",\"in_step\":" << (long long)s->in_step << ",\"out_offset\":" << (long long)s->out_off
+          << ",\"dest_order\":[";
+        for (int k = 1; k <= s->nranks; ++k) o << (k > 1 ? "," : "") << (s->proc + k) % s->nranks;
+        o << "],\"fused\":" << describe_json(*s->fused);
+    }
     o << "}";
     return o.str();
 }
@@ -102,7 +142,7 @@ std::string describe_shard_json(const Plan& plan) {
 // Geometry + sub-plans; comm may be null (offline).
 static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int rank, int n,
                                  const int64_t* gd, const int* perm, size_t esize, void* stream,
-                                 const DeviceInfo& dev, OccupancyFn occ) {
+                                 const DeviceInfo& dev, OccupancyFn occ, bool p2p = false) {
     *out = nullptr;
     tt_status_t st = validate(n, gd, perm, esize);
     if (st != TT_SUCCESS) return st;
@@ -124,6 +164,8 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
     s->rank = rank;
     s->esize = (int)esize;
     s->redistribute = redist;
+    s->proc = rank;
+    s->p2p = redist && p2p;
     outer->device = dev.device;
     outer->stream = stream;
     outer->rank = n;
@@ -152,8 +194,30 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
         return TT_SUCCESS;
     }
 
-    // pack: split input dim t into (c = D[t]/P, P), P-part outermost
     const int64_t c = gd[t] / P;
+    if (s->p2p) {
+        // fused: one strided plan per destination sub-box (x_t in [q*c, (q+1)*c))
+        std::vector<int64_t> fd = L, si(n), so(n);
+        fd[t] = c;
+        int64_t acc = 1;
+        for (int i = 0; i < n; ++i) { si[i] = acc; acc *= L[i]; }  // the slab's strides
+        acc = 1;
+        int jstar = -1;
+        for (int j = 0; j < n; ++j) {                              // the output slab's strides
+            so[j] = acc;
+            acc *= s->local_out[j];
+            if (perm[j] == n - 1) jstar = j;
+        }
+        s->in_step = c * si[t];
+        s->out_off = (int64_t)rank * L[n - 1] * so[jstar];
+        st = create_plan_s(&s->fused, n, fd.data(), perm, esize, stream, dev, nullptr, occ,
+                           si.data(), so.data());
+        if (st != TT_SUCCESS) { destroy_plan(outer); return st; }
+        *out = outer;
+        return TT_SUCCESS;
+    }
+
+    // pack: split input dim t into (c = D[t]/P, P), P-part outermost
     std::vector<int64_t> pd;
     auto ni = [&](int i) { return i < t ? i : (i == t ? t : i + 1); };
     for (int i = 0; i < n; ++i) {
@@ -184,6 +248,112 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
     *out = outer;
     return TT_SUCCESS;
 }
+
+// ---- p2p (f-1): device-side barrier over IPC-mapped signal words ----------
+//
+// Rank r's signal array sig[0..P-1] (+ one error word at sig[P]) lives in its
+// own HBM; peer q writes sig[q] = epoch when it arrives.  Thread q of the
+// barrier kernel publishes this rank's arrival in peer q's array with a
+// system-scope release store and then waits, with system-scope acquire loads,
+// until peer q's word in its own array reaches the epoch.  The fence before the
+// release makes every store this rank issued earlier on the stream (the fused
+// permute kernels writing into peers' slabs over NVLink) visible first.  A
+// peer that never arrives sets the error word after kP2PTimeoutNs instead of
+// hanging the GPU (reported by tt_sharded_timings).
+constexpr int kMaxPeers = 64;
+constexpr unsigned long long kP2PTimeoutNs = 30ull * 1000 * 1000 * 1000;
+
+struct BarrierArgs {
+    int* peer_sig[kMaxPeers];
+    int* mine;
+    int P, rank, epoch;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
+    const int q = threadIdx.x;
+    if (q >= a.P) return;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(a.peer_sig[q] + a.rank), "r"(a.epoch)
+                 : "memory");
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+        int v;
+        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(a.mine + q) : "memory");
+        if (v - a.epoch >= 0) break;
+        if (global_ns() - t0 > kP2PTimeoutNs) {
+            atomicExch(a.mine + a.P, 1);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
+
+static int launch_barrier(ShardInfo* s, cudaStream_t st) {
+    BarrierArgs a;
+    std::memset(&a, 0, sizeof(a));
+    for (int q = 0; q < s->nranks; ++q) a.peer_sig[q] = s->peer_sig[q];
+    a.mine = s->sig;
+    a.P = s->nranks;
+    a.rank = s->proc;
+    a.epoch = ++s->epoch;
+    p2p_barrier_kernel<<<1, 64, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// The P sub-box permutations of one fused execute, nearest-rank-last order
+// (destination proc+1 first, own slab last) so that at any moment the ranks
+// write to different peers.
+static tt_status_t launch_fused(ShardInfo* s, const void* in, void* const* outs, void* stream) {
+    const char* ib = static_cast<const char*>(in);
+    for (int k = 1; k <= s->nranks; ++k) {
+        const int q = (s->proc + k) % s->nranks;
+        const void* i = ib + (size_t)q * (size_t)s->in_step * s->esize;
+        void* o = static_cast<char*>(outs[q]) + (size_t)s->out_off * s->esize;
+        if (launch_plan(*s->fused, i, o, stream) != 0) return TT_CUDA_ERROR;
+    }
+    return TT_SUCCESS;
+}
+
+// Base and offset of a device pointer inside its allocation (for CUDA IPC,
+// whose handles name whole allocations).  Driver entry point, so libtt does
+// not link libcuda directly.
+typedef CUresult (*MemRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+static bool alloc_base(const void* p, void** base, size_t* off) {
+    static MemRangeFn fn = nullptr;
+    if (fn == nullptr) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault,
+                                             &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || f == nullptr) {
+            cudaGetLastError();
+            return false;
+        }
+        fn = reinterpret_cast<MemRangeFn>(f);
+    }
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+    *base = reinterpret_cast<void*>(b);
+    *off = reinterpret_cast<uintptr_t>(p) - (uintptr_t)b;
+    return true;
+}
+
+// What each rank contributes to the registration all-gather.
+struct RegRecord {
+    cudaIpcMemHandle_t out;
+    cudaIpcMemHandle_t sig;
+    int64_t out_off;
+    int32_t device, proc;
+    char pad[256 - 2 * sizeof(cudaIpcMemHandle_t) - 16];
+};
+static_assert(sizeof(RegRecord) == 256, "registration record");
 
 }  // namespace tt
 
@@ -303,6 +473,20 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
     if (!s->redistribute)
         return launch_plan(*s->local, in_local, out_local, p->stream) == 0 ? TT_SUCCESS : TT_CUDA_ERROR;
+    if (s->p2p) {
+        // fused: entry barrier, P sub-box permutations into the peers' slabs, exit barrier
+        if (s->reg_out == nullptr || out_local != s->reg_out) return TT_INVALID_PARAMETER;
+        cudaEventRecord(s->ev[0], st);
+        if (launch_barrier(s, st) != 0) return TT_CUDA_ERROR;
+        cudaEventRecord(s->ev[1], st);
+        tt_status_t rc = launch_fused(s, in_local, s->peer_out.data(), p->stream);
+        if (rc != TT_SUCCESS) return rc;
+        cudaEventRecord(s->ev[2], st);
+        if (launch_barrier(s, st) != 0) return TT_CUDA_ERROR;
+        cudaEventRecord(s->ev[3], st);
+        s->timed = true;
+        return TT_SUCCESS;
+    }
     cudaEventRecord(s->ev[0], st);
     if (launch_plan(*s->pack, in_local, s->send, p->stream) != 0) return TT_CUDA_ERROR;
     cudaEventRecord(s->ev[1], st);
@@ -329,6 +513,14 @@ tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3) {
             cudaGetLastError();
             return TT_CUDA_ERROR;
         }
+    if (s->p2p && s->sig) {  // a peer that never reached a barrier
+        int err = 0;
+        if (cudaMemcpy(&err, s->sig + s->nranks, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return TT_CUDA_ERROR;
+        }
+        if (err != 0) return TT_CUDA_ERROR;
+    }
     return TT_SUCCESS;
 }
 
@@ -343,4 +535,148 @@ tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* 
     return TT_SUCCESS;
 }
 
-}  // extern "C"
+tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int ndims,
+                                const int64_t* global_dims, const int* perm, size_t elem_size,
+                                tt_stream_t stream) {
+    if (plan == nullptr || ndims < 1) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    tt_comm_impl* c = nullptr;
+    if (comm != nullptr) {
+        c = as_comm(comm);
+        if (c == nullptr || c->nranks != nranks || c->rank != proc) return TT_INVALID_PARAMETER;
+    }
+    if (nranks < 1 || nranks > kMaxPeers) return TT_UNSUPPORTED;
+    DeviceInfo dev;
+    tt_status_t st = query_device(dev);
+    if (st != TT_SUCCESS) return st;
+    if (c && dev.device != c->device) return TT_INVALID_DEVICE;
+    Plan* p = nullptr;
+    st = build_shard_n(&p, c, nranks, proc, ndims, global_dims, perm, elem_size, stream, dev,
+                       &cuda_occupancy, true);
+    if (st != TT_SUCCESS) return st;
+    ShardInfo* s = p->shard;
+    for (auto& e : s->ev) {
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            cudaGetLastError();
+            destroy_plan(p);
+            return TT_CUDA_ERROR;
+        }
+    }
+    *plan = reinterpret_cast<tt_plan_t>(p);
+    return TT_SUCCESS;
+}
+
+tt_status_t tt_plan_sharded_p2p_offline(tt_plan_t* plan, int nranks, int proc, int ndims,
+                                        const int64_t* global_dims, const int* perm,
+                                        size_t elem_size) {
+    if (plan == nullptr || ndims < 1) return TT_INVALID_PARAMETER;
+    *plan = nullptr;
+    if (nranks < 1 || nranks > kMaxPeers) return TT_UNSUPPORTED;
+    DeviceInfo dev;
+    dev.device = -1;
+    Plan* p = nullptr;
+    tt_status_t st = build_shard_n(&p, nullptr, nranks, proc, ndims, global_dims, perm, elem_size,
+                                   nullptr, dev, nullptr, true);
+    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(p);
+    return st;
+}
+
+tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr || p->shard == nullptr) return TT_INVALID_PLAN;
+    ShardInfo* s = p->shard;
+    if (!s->p2p || s->comm == nullptr) return TT_INVALID_PLAN;
+    if (out_local == nullptr || (reinterpret_cast<uintptr_t>(out_local) & (uintptr_t)(s->esize - 1)))
+        return TT_INVALID_PARAMETER;
+    if (s->reg_out != nullptr) return TT_INVALID_PARAMETER;  // once per plan
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    const int P = s->nranks;
+    cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+    // own signal words (+ error word), zeroed before any peer can see them
+    if (cudaMalloc(&s->sig, (P + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(s->sig, 0, (P + 1) * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    RegRecord mine;
+    std::memset(&mine, 0, sizeof(mine));
+    void* base = nullptr;
+    size_t off = 0;
+    if (!alloc_base(out_local, &base, &off) ||
+        cudaIpcGetMemHandle(&mine.out, base) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.sig, s->sig) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    mine.out_off = (int64_t)off;
+    mine.device = d;
+    mine.proc = s->proc;
+    // all-gather the records with the communicator (no host-side rendezvous)
+    void* dbuf = nullptr;
+    std::vector<RegRecord> all(P);
+    if (cudaMalloc(&dbuf, (size_t)(P + 1) * sizeof(RegRecord)) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    char* dsend = static_cast<char*>(dbuf) + (size_t)P * sizeof(RegRecord);
+    tt_status_t rc = TT_SUCCESS;
+    if (cudaMemcpyAsync(dsend, &mine, sizeof(mine), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = TT_CUDA_ERROR;
+    else if (ncclAllGather(dsend, dbuf, sizeof(RegRecord), ncclUint8, s->comm->nccl, st) != ncclSuccess)
+        rc = TT_NCCL_ERROR;
+    else if (cudaMemcpyAsync(all.data(), dbuf, (size_t)P * sizeof(RegRecord), cudaMemcpyDeviceToHost,
+                             st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+        rc = TT_CUDA_ERROR;
+    cudaFree(dbuf);
+    if (rc != TT_SUCCESS) { cudaGetLastError(); return rc; }
+    s->peer_out.assign(P, nullptr);
+    s->peer_sig.assign(P, nullptr);
+    for (int q = 0; q < P; ++q) {
+        if (all[q].proc != q) return TT_INTERNAL_ERROR;
+        if (q == s->proc) {
+            s->peer_out[q] = out_local;
+            s->peer_sig[q] = s->sig;
+            continue;
+        }
+        void* ob = nullptr;
+        void* sb = nullptr;
+        if (cudaIpcOpenMemHandle(&ob, all[q].out, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return TT_CUDA_ERROR;
+        }
+        s->ipc_bases.push_back(ob);
+        if (cudaIpcOpenMemHandle(&sb, all[q].sig, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return TT_CUDA_ERROR;
+        }
+        s->ipc_bases.push_back(sb);
+        s->peer_out[q] = static_cast<char*>(ob) + all[q].out_off;
+        s->peer_sig[q] = static_cast<int*>(sb);
+    }
+    s->reg_out = out_local;
+    return TT_SUCCESS;
+}
+
+tt_status_t tt_execute_sharded_p2p(tt_plan_t plan, const void* in_local, void* const* out_slabs) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr || p->shard == nullptr) return TT_INVALID_PLAN;
+    ShardInfo* s = p->shard;
+    if (in_local == nullptr || out_slabs == nullptr) return TT_INVALID_PARAMETER;
+    uintptr_t bits = reinterpret_cast<uintptr_t>(in_local);
+    for (int q = 0; q < s->nranks; ++q) {
+        if (out_slabs[q] == nullptr || out_slabs[q] == in_local) return TT_INVALID_PARAMETER;
+        bits |= reinterpret_cast<uintptr_t>(out_slabs[q]);
+    }
+    if ((bits & (uintptr_t)(s->esize - 1)) != 0) return TT_INVALID_PARAMETER;
+    if (p->device < 0) return TT_INVALID_DEVICE;
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    if (!s->redistribute)
+        return launch_plan(*s->local, in_local, out_slabs[s->proc], p->stream) == 0 ? TT_SUCCESS
+                                                                                   : TT_CUDA_ERROR;
+    if (!s->p2p) return TT_INVALID_PLAN;
+    return launch_fused(s, in_local, out_slabs, p->stream);
+}
+
+}  // extern "C\"

@@ -100,3 +100,88 @@ def test_single_rank_nccl_redistribution_path(monkeypatch):
         assert pack_ms > 0 and unpack_ms > 0 and a2a_ms >= 0
         sp.destroy()
     comm.destroy()
+
+
+# ---- fused redistribution (SURVEY f-1): tt_plan_sharded_p2p ----------------
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("perm,esize", [((3, 2, 1, 0), 8), ((2, 3, 0, 1), 4), ((1, 0, 3, 2), 8),
+                                        ((0, 3, 1, 2), 4), ((2, 0, 3, 1), 8), ((1, 0, 2, 3), 4)])
+def test_p2p_emulated_ranks(P, perm, esize):
+    """Single-process form: P emulated ranks on one GPU, each storing its P
+    sub-boxes straight into the P output slabs (tt_execute_sharded_p2p);
+    the slabs together equal the oracle's output of the global tensor.
+    Extents leave ragged tiles (24*7 = 168 etc.)."""
+    gdims = (24, 56, 16, 40)
+    vol = int(np.prod(gdims))
+    words = wl.random_words(vol, esize, 11)
+    x = torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
+    slab = vol // P
+    outs = [torch.full((slab,), -1, dtype=x.dtype, device=x.device) for _ in range(P)]
+    plans = [tt.P2PShardedPlan(None, gdims, perm, esize, nranks=P, proc=r) for r in range(P)]
+    want_mode = "local" if perm[-1] == 3 else "p2p"
+    for r, sp in enumerate(plans):
+        assert sp.describe()["mode"] == want_mode
+        sp.execute_slabs(x[r * slab:(r + 1) * slab], outs)
+    torch.cuda.synchronize()
+    got = torch.cat(outs).cpu().numpy().view(words.dtype)
+    np.testing.assert_array_equal(got, orc.permute(gdims, perm, words))
+    for sp in plans:
+        sp.destroy()
+
+
+def test_p2p_emulated_full_size_s5():
+    """BJ configs[4] at full size (112x112x112x104 fp64, 1.17 GB), 8 emulated
+    ranks in the launch configuration the plans choose; sampled output
+    positions against the oracle computed one by one, plus the wrapping sum
+    of the words (multiset invariant)."""
+    c = [c for c in wl.s5_sharded() if tuple(c.perm) == (3, 2, 1, 0)][0]
+    P, gdims, perm = 8, c.dims, c.perm
+    vol = int(np.prod(gdims))
+    words = c.words()
+    x = torch.from_numpy(words.view(np.int64)).to(_dev())
+    slab = vol // P
+    out = torch.empty_like(x)
+    outs = [out[q * slab:(q + 1) * slab] for q in range(P)]
+    for r in range(P):
+        sp = tt.P2PShardedPlan(None, gdims, perm, 8, nranks=P, proc=r)
+        sp.execute_slabs(x[r * slab:(r + 1) * slab], outs)
+        sp.destroy()
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(words.dtype)
+    rng = np.random.default_rng(3)
+    pos = np.concatenate([rng.integers(0, vol, 4096), [0, vol - 1, slab - 1, slab]])
+    np.testing.assert_array_equal(got[pos], orc.permute_sample(gdims, perm, words, pos))
+    assert int(got.view(np.uint64).sum(dtype=np.uint64)) == int(words.view(np.uint64).sum(dtype=np.uint64))
+
+
+def test_p2p_single_rank_comm_barriers(monkeypatch):
+    """Multi-process form with one rank (forced redistribution): IPC
+    registration through the NCCL all-gather, entry/exit barrier kernels
+    over the signal words, repeated executes (epochs), timings."""
+    _dev()
+    monkeypatch.setenv("TT_SHARD_FORCE_REDIST", "1")
+    comm = tt.Comm(tt.unique_id(), 1, 0)
+    for perm, esize in [((3, 2, 1, 0), 8), ((2, 3, 0, 1), 4)]:
+        gdims = (16, 24, 8, 40)
+        words = wl.random_words(int(np.prod(gdims)), esize, 8)
+        x = torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
+        big = torch.empty(x.numel() + 64, dtype=x.dtype, device=x.device)
+        y = big[32:32 + x.numel()]          # inside an allocation: IPC base + offset
+        sp = tt.P2PShardedPlan(comm, gdims, perm, esize)
+        d = sp.describe()
+        assert d["mode"] == "p2p" and d["launches"] == 3
+        with pytest.raises(tt.TTError):      # not registered yet
+            sp.execute(x, y)
+        sp.register_output(y)
+        with pytest.raises(tt.TTError):      # not the registered buffer
+            sp.execute(x, torch.empty_like(x))
+        for _ in range(3):
+            y.fill_(-1)
+            sp.execute(x, y)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(y.cpu().numpy().view(words.dtype), orc.permute(gdims, perm, words))
+        bar_in, fused_ms, bar_out = sp.timings()
+        assert fused_ms > 0 and bar_in >= 0 and bar_out >= 0
+        sp.destroy()
+    comm.destroy()
