@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -48,6 +49,8 @@
 #include "tt_internal.h"
 
 namespace tt {
+
+static int64_t ceil_div_i64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct tt_comm_impl {
     uint32_t magic = 0x5454434du;  // "TTCM"
@@ -82,6 +85,13 @@ struct ShardInfo {
     int* sig = nullptr;             // [P] signal words of this rank (device), + [P] error word
     std::vector<int*> peer_sig;     // [P] peers' signal arrays as mapped here
     int epoch = 0;
+    // the P sub-box launches run concurrently on P streams forked from the
+    // plan's stream, each with 1/P of the plan's persistent grid: together
+    // they sweep the input slab densely (one launch per destination after
+    // another would read it P times at 1/P density -- measured 3-8x slower)
+    std::vector<cudaStream_t> sub;
+    std::vector<cudaEvent_t> join;
+    cudaEvent_t fork = nullptr;
 };
 
 void destroy_shard(ShardInfo* s) {
@@ -92,6 +102,9 @@ void destroy_shard(ShardInfo* s) {
     destroy_plan(s->fused);
     for (void* b : s->ipc_bases) cudaIpcCloseMemHandle(b);
     if (s->sig) cudaFree(s->sig);
+    for (cudaStream_t x : s->sub) cudaStreamDestroy(x);
+    for (cudaEvent_t e : s->join) cudaEventDestroy(e);
+    if (s->fork) cudaEventDestroy(s->fork);
     if (s->send) cudaFree(s->send);
     if (s->recv) cudaFree(s->recv);
     for (auto& e : s->ev)
@@ -213,6 +226,10 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
         st = create_plan_s(&s->fused, n, fd.data(), perm, esize, stream, dev, nullptr, occ,
                            si.data(), so.data());
         if (st != TT_SUCCESS) { destroy_plan(outer); return st; }
+        // the P sub-box launches run concurrently (launch_fused): 1/P of the grid each
+        KernelChoice& kc = s->fused->kc;
+        kc.grid = (int)std::max<int64_t>(1, ceil_div_i64(kc.grid, P));
+        kc.fb_grid = (int)std::max<int64_t>(1, ceil_div_i64(kc.fb_grid, P));
         *out = outer;
         return TT_SUCCESS;
     }
@@ -310,13 +327,30 @@ static int launch_barrier(ShardInfo* s, cudaStream_t st) {
 // (destination proc+1 first, own slab last) so that at any moment the ranks
 // write to different peers.
 static tt_status_t launch_fused(ShardInfo* s, const void* in, void* const* outs, void* stream) {
+    const int P = s->nranks;
+    cudaStream_t main = static_cast<cudaStream_t>(stream);
+    if (P > 1 && s->sub.empty()) {  // first execute: fork/join streams and events
+        s->sub.assign(P, nullptr);
+        s->join.assign(P, nullptr);
+        bool ok = cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int q = 0; q < P && ok; ++q)
+            ok = cudaStreamCreateWithFlags(&s->sub[q], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&s->join[q], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) { cudaGetLastError(); return TT_CUDA_ERROR; }
+    }
+    if (P > 1 && cudaEventRecord(s->fork, main) != cudaSuccess) return TT_CUDA_ERROR;
     const char* ib = static_cast<const char*>(in);
-    for (int k = 1; k <= s->nranks; ++k) {
-        const int q = (s->proc + k) % s->nranks;
+    for (int k = 1; k <= P; ++k) {
+        const int q = (s->proc + k) % P;
         const void* i = ib + (size_t)q * (size_t)s->in_step * s->esize;
         void* o = static_cast<char*>(outs[q]) + (size_t)s->out_off * s->esize;
-        if (launch_plan(*s->fused, i, o, stream) != 0) return TT_CUDA_ERROR;
+        cudaStream_t x = P > 1 ? s->sub[q] : main;
+        if (P > 1 && cudaStreamWaitEvent(x, s->fork, 0) != cudaSuccess) return TT_CUDA_ERROR;
+        if (launch_plan(*s->fused, i, o, x) != 0) return TT_CUDA_ERROR;
+        if (P > 1 && cudaEventRecord(s->join[q], x) != cudaSuccess) return TT_CUDA_ERROR;
     }
+    for (int q = 0; q < P && P > 1; ++q)
+        if (cudaStreamWaitEvent(main, s->join[q], 0) != cudaSuccess) return TT_CUDA_ERROR;
     return TT_SUCCESS;
 }
 

@@ -864,6 +864,39 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.kernel = TT_KERNEL_ROWCOPY;
         kc.threads = opts && opts->threads ? opts->threads : 256;
         const int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : 4;
+        // Few long rows (e.g. the sharded unpack's (inner, middle, P) rows of
+        // megabytes): a warp per row leaves most warps idle, so cut each row
+        // into nseg segments of `seg` elements (seg | row, seg*E >= 2 KB).
+        // Segment k of row q is a virtual row v = q*nseg + k whose output
+        // starts at v*seg -- a new fastest row dim of extent nseg and input
+        // stride seg; the kernel is unchanged.
+        const int64_t warpsTotal = (int64_t)dev.num_sms * perSm * (kc.threads / 32);
+        if (r.nRows < 4 * warpsTotal && r.h < kMaxDims - 1) {
+            int64_t best = 0;
+            for (int64_t seg = r.row / 2; seg >= 1 && seg * E >= 2048; --seg) {
+                if (r.row % seg) continue;
+                best = seg;  // smallest admissible so far (most segments)
+                if (r.nRows * (r.row / seg) >= 4 * warpsTotal) break;  // largest reaching the target
+            }
+            if (best > 0) {
+                const int64_t nseg = r.row / best;
+                for (int j = r.h; j > 0; --j) {
+                    r.rC[j] = r.rC[j - 1] * nseg;
+                    r.rD[j] = r.rD[j - 1];
+                    r.rSin[j] = r.rSin[j - 1];
+                }
+                r.rC[0] = 1;
+                r.rD[0] = nseg;
+                r.rSin[0] = best;
+                r.h += 1;
+                r.row = best;
+                r.nRows *= nseg;
+                for (int j = 0; j < r.h; ++j) {
+                    if (r.rC[j] < (int64_t(1) << 31)) magic_u31((uint32_t)r.rC[j], r.gMC[j], r.gLC[j]);
+                    if (r.rD[j] < (int64_t(1) << 31)) magic_u31((uint32_t)r.rD[j], r.gMD[j], r.gLD[j]);
+                }
+            }
+        }
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)dev.num_sms * perSm,
                                                               ceil_div(r.nRows * 32, kc.threads)));
         kc.predicted_us = 2.0 * pr.vol * E / model::kBwBytesPerUs + model::kLaunchUs;

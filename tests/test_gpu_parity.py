@@ -147,7 +147,9 @@ def test_forced_tiled2d(esize):
 
 ROW_SHAPES = [((600, 7, 5), (0, 2, 1)), ((256, 3, 5, 2), (0, 3, 1, 2)), ((8, 7, 5), (0, 2, 1)),
               ((6, 5, 7), (0, 2, 1)), ((1001, 3, 4), (0, 2, 1)), ((2, 300, 3, 17), (0, 3, 2, 1)),
-              ((128, 2, 2, 2, 2, 2), (0, 5, 3, 1, 4, 2)), ((4, 4), (0, 1))]
+              ((128, 2, 2, 2, 2, 2), (0, 5, 3, 1, 4, 2)), ((4, 4), (0, 1)),
+              # few long rows: segmented into a new fastest row dim
+              ((6144, 5, 3), (0, 2, 1)), ((2048 * 9, 3, 7), (0, 2, 1)), ((4099, 3, 2), (0, 2, 1))]
 
 
 @pytest.mark.parametrize("esize", [4, 8])

@@ -304,3 +304,22 @@ def test_strided_plan_validation():
     assert j["dense"] is True and j["kernel"] in ("tiled2d", "tile")   # dense layout recognised
     j = tt.plan_offline((64, 64), (1, 0), 4, in_strides=(1, 66), out_strides=(1, 68))
     assert j["dense"] is False and j["kernel"] == "tiled2d" and j["vec"] == 2
+
+
+@pytest.mark.parametrize("dims,perm,esize", [
+    ((6144, 5, 3), (0, 2, 1), 4),        # 15 rows of 24 KB -> segmented
+    ((2048, 3, 7), (0, 2, 1), 8),        # 21 rows of 16 KB
+    ((1536, 4, 3, 2), (0, 3, 1, 2), 4),
+    ((4099, 3, 2), (0, 2, 1), 4),        # prime row: no admissible segment
+])
+def test_rowcopy_segmented_rows_match_oracle(dims, perm, esize):
+    """Few long rows are cut into segments (a new fastest row dim); the
+    replayed plan must still equal the oracle."""
+    j = tt.plan_offline(dims, perm, esize)
+    assert j["kernel"] == "rowcopy"
+    r = j["rowcopy"]
+    vol = int(np.prod(dims))
+    if dims[0] != 4099:
+        assert r["nRows"] > vol // dims[0] and r["row"] * j["word_size"] >= 2048
+    words = wl.random_words(vol, esize, 78)
+    np.testing.assert_array_equal(interpret_plan(j, words), orc.permute(dims, perm, words))
