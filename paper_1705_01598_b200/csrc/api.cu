@@ -358,9 +358,13 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
         const int tiles4[4][2] = {{64, 128}, {128, 64}, {128, 128}, {64, 64}};
         const int tiles8[4][2] = {{64, 64}, {64, 32}, {32, 64}, {32, 32}};
         for (int t = 0; t < 4; ++t)
-            for (int cps : {1, 2, 3})
-                vars.push_back(W == 4 ? opt(TT_KERNEL_TILED2D, tiles4[t][0], tiles4[t][1], 0, cps, 2)
-                                      : opt(TT_KERNEL_TILED2D, tiles8[t][0], tiles8[t][1], 0, cps, 2));
+            for (int cps : {1, 2, 3, 4})
+                for (int st : {0, 4}) {  // stages 4: the scalar kernel's cp.async ring
+                    tt_plan_options_t o = W == 4 ? opt(TT_KERNEL_TILED2D, tiles4[t][0], tiles4[t][1], 0, cps, 2)
+                                                 : opt(TT_KERNEL_TILED2D, tiles8[t][0], tiles8[t][1], 0, cps, 2);
+                    o.stages = st;
+                    vars.push_back(o);
+                }
     }
     if (hp.n >= 2 && hp.p[0] == 0)
         for (int cps : {2, 4, 8}) vars.push_back(opt(TT_KERNEL_ROWCOPY, 0, 0, 0, cps, 0));

@@ -1030,6 +1030,92 @@ tiled2d_s_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ 
     }
 }
 
+// scalar 2-D tile, asynchronous-copy pipeline: the same tiles, thread map
+// and padded staging rows as tiled2d_s_kernel, but the loads go straight to
+// shared memory with cp.async (no data registers), so S-1 tiles per CTA are
+// in flight instead of one (ncu on odd-extent fp64 cases of the register
+// version: 24 warps/SM, long-scoreboard 46 %, DRAM traffic = algorithmic --
+// latency-bound, not traffic-bound).
+template <typename W, int MA, int MB, typename I, int S>
+__global__ void __launch_bounds__(256)
+tiled2d_sa_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in, W* __restrict__ out) {
+    constexpr int TA = 32 * MA;
+    constexpr int TB = 8 * MB;
+    constexpr int RS = TB + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    constexpr uint32_t BUF = (uint32_t)(TA * RS * sizeof(W));
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int wid = tid >> 5;
+
+    const I nTiles = (I)p.nTiles;
+    I t = (I)blockIdx.x;
+    if (t >= nTiles) return;
+    const I stride = (I)gridDim.x;
+    const I sInB = (I)p.sInB;
+    const I sOutA = (I)p.sOutA;
+
+    auto issue = [&](const TileBase<I>& tb, uint32_t sb) {
+        const int limA = (tb.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (tb.need & 2u) ? p.splitTail[1] : TB;
+        const W* __restrict__ src = opaque(in + tb.in);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int b = wid + 8 * mb;
+#pragma unroll
+            for (int ma = 0; ma < MA; ++ma) {
+                const int a = lane + 32 * ma;
+                if (a < limA && b < limB)
+                    cp_async<sizeof(W)>(sb + (uint32_t)((a * RS + b) * sizeof(W)), src + ((I)b * sInB + a));
+            }
+        }
+    };
+    TileBase<I> q[S - 1];
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        const I tj = t + (I)j * stride;
+        if (tj < nTiles) {
+            q[j] = decode_tile<I>(p, tj, lane);
+            issue(q[j], sm0 + (uint32_t)j * BUF);
+        }
+        cp_async_commit();
+    }
+    int stage = 0;
+    for (; t < nTiles; t += stride) {
+        cp_async_wait<S - 2>();  // this thread's copies for tile t have landed
+        __syncthreads();         // ... and everyone's; last iteration's stage is free
+        const I tn = t + (I)(S - 1) * stride;
+        const bool more = tn < nTiles;
+        TileBase<I> nw;
+        if (more) {
+            nw = decode_tile<I>(p, tn, lane);
+            issue(nw, sm0 + (uint32_t)((stage + S - 1) % S) * BUF);
+        }
+        cp_async_commit();
+        const TileBase<I> now = q[0];
+        const uint32_t sb = sm0 + (uint32_t)stage * BUF;
+        const int limA = (now.need & 1u) ? p.splitTail[0] : TA;
+        const int limB = (now.need & 2u) ? p.splitTail[1] : TB;
+        W* __restrict__ dst = opaque(out + now.out);
+#pragma unroll
+        for (int j = 0; j < TA / 8; ++j) {
+            const int a = wid + 8 * j;
+#pragma unroll
+            for (int u = 0; u < TB / 32; ++u) {
+                const int b = lane + 32 * u;
+                if (a < limA && b < limB)
+                    stg_(dst + ((I)a * sOutA + b), lds<W>(sb + (uint32_t)((a * RS + b) * sizeof(W))));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < S - 1; ++j) q[j] = q[j + 1];
+        if (more) q[S - 2] = nw;
+        stage = (stage + 1 == S) ? 0 : stage + 1;
+    }
+    cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
@@ -1139,6 +1225,23 @@ static const void* t2ds_fn(bool idx64) {
                  : (const void*)&tiled2d_s_kernel<W, MA, MB, uint32_t>;
 }
 
+template <typename W, int MA, int MB>
+static const void* t2dsa_fn(int stages) {
+    return stages == 4 ? (const void*)&tiled2d_sa_kernel<W, MA, MB, uint32_t, 4>
+                       : (const void*)&tiled2d_sa_kernel<W, MA, MB, uint32_t, 3>;
+}
+
+// scalar 2-D kernel with the cp.async ring (3 or 4 stages, 32-bit indices)
+static const void* pick_tiled2d_async(int esize, int ta, int tb, int stages) {
+    if (esize == 4 && ta == 64 && tb == 64) return t2dsa_fn<uint32_t, 2, 8>(stages);
+    if (esize == 4 && ta == 128 && tb == 64) return t2dsa_fn<uint32_t, 4, 8>(stages);
+    if (esize == 4 && ta == 64 && tb == 128) return t2dsa_fn<uint32_t, 2, 16>(stages);
+    if (esize == 8 && ta == 64 && tb == 64) return t2dsa_fn<uint64_t, 2, 8>(stages);
+    if (esize == 8 && ta == 32 && tb == 64) return t2dsa_fn<uint64_t, 1, 8>(stages);
+    if (esize == 8 && ta == 64 && tb == 32) return t2dsa_fn<uint64_t, 2, 4>(stages);
+    return nullptr;
+}
+
 static const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64) {
     if (vec == 1) {  // scalar 2-D kernel: TA = 32*MA, TB = 8*MB
         if (esize == 4 && ta == 64 && tb == 64) return t2ds_fn<uint32_t, 2, 8>(idx64);
@@ -1195,7 +1298,10 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
                             : q.acc ? pick_tile_acc(q.esize, q.nreg)
                                       : (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
                                                     : pick_tile(q.esize, q.nreg, q.idx64)))
-                     : q.kernel == TT_KERNEL_TILED2D ? pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64)
+                     : q.kernel == TT_KERNEL_TILED2D
+                         ? (q.vec == 1 && q.sdq >= 3 && !q.idx64  // sdq = stages for the 2-D ring
+                                ? pick_tiled2d_async(q.esize, q.ta, q.tb, q.sdq)
+                                : pick_tiled2d(q.esize, q.vec, q.ta, q.tb, q.idx64))
                      : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
     if (!fn) return 0;
@@ -1250,7 +1356,9 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
             grid = kc.fb_grid;
             smem = kc.fb_smem;
         }
-        const void* fn = t2 ? pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64)
+        const void* fn = t2 ? (kc.vec == 1 && kc.stages >= 3 && !kc.idx64
+                                   ? pick_tiled2d_async(E, kc.tile0, kc.tile1, kc.stages)
+                                   : pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64))
                             : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr)
                             : kc.acc ? pick_tile_acc(E, kc.nreg)
                                      : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)

@@ -744,7 +744,9 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     // vectors, 64 x 64 otherwise; two CTAs per SM, B-chunks fastest.
     if (pr.esize == 4) { ta = 64; tb = vec == 4 ? 128 : 64; }
     else { ta = 64; tb = 64; }
-    if (vec == 1) { ta = pr.esize == 4 ? 64 : 32; tb = 64; }  // sweep_t2ds: 3 CTAs/SM
+    // scalar kernel: 64 x 64 (tools/sweep_t2d_async.py on odd-extent S2
+    // shapes: fp64 64x64 at 4 CTAs/SM beat 32x64 at 3 by 8-18 %)
+    if (vec == 1) { ta = 64; tb = 64; }
     if (wantA || wantB) {
         if (wantA) ta = wantA;
         if (wantB) tb = wantB;
@@ -1049,13 +1051,22 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.tile0 = ta2d;
         kc.tile1 = tb2d;
         kc.threads = 256;
-        kc.smem = vec2d == 1 ? 2 * ta2d * (tb2d + 1) * E : 2 * ta2d * tb2d * E;
-        OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64, ta2d, tb2d};
+        // scalar 2-D kernel: register double buffer, or a cp.async ring of
+        // 3-4 stages (tiled2d_sa_kernel; 32-bit indices)
+        const int st2 = opts && opts->stages >= 3 ? std::min(4, opts->stages) : 0;
+        kc.stages = (vec2d == 1 && st2 && !kc.idx64) ? st2 : 0;
+        kc.smem = vec2d == 1 ? (kc.stages ? kc.stages : 2) * ta2d * (tb2d + 1) * E
+                             : 2 * ta2d * tb2d * E;
+        OccQuery q2{TT_KERNEL_TILED2D, E, 0, vec2d, 256, kc.smem, kc.idx64, ta2d, tb2d, 0, kc.stages, 0};
         int occ2 = occ ? occ(q2, dev) : 0;
         if (occ2 <= 0) occ2 = std::min(8, dev.max_smem_per_sm / (kc.smem + 1024));
         // two CTAs per SM measured best (fewer concurrent tiles, whole DRAM
         // rows); never more than fit, so the persistent grid is one wave
-        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm : std::min(vec2d == 1 ? 3 : 2, occ2);
+        // (scalar kernel: 3 CTAs/SM for 4-byte words; 4 for 8-byte words --
+        // beyond the 3 that fit, a second partial wave that balances the
+        // tail, measured best)
+        int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm
+                   : vec2d == 1 ? (E == 8 ? 4 : std::min(3, occ2)) : std::min(2, occ2);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
         const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
         kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;

@@ -155,7 +155,7 @@ struct OccQuery {
     bool idx64;
     int ta, tb;  // TILED2D tile
     int acc;     // TILE accumulate variant
-    int sdq, sdr;  // TILE slot-dim variant (passes, slots); 0 = classic
+    int sdq, sdr;  // TILE slot-dim variant (passes, slots); 0 = classic; TILED2D: sdq = cp.async stages
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 

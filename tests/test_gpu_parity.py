@@ -145,6 +145,26 @@ def test_forced_tiled2d(esize):
         np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("stages", [3, 4])
+def test_scalar_tiled2d_async_ring(esize, stages):
+    """Scalar 2-D kernel with the cp.async ring (tiled2d_sa_kernel): odd
+    extents, ragged tiles on both sides, batched dims, every instantiated
+    tile, and more CTAs than fit (second partial wave)."""
+    shapes = [((67, 45), (1, 0)), ((13, 3, 67), (2, 1, 0)), ((1001, 999), (1, 0)),
+              ((129, 5, 65), (2, 0, 1)), ((585, 7, 33), (1, 0, 2)), ((119, 5, 3, 119), (3, 2, 1, 0))]
+    tiles = [(64, 64), (128, 64), (64, 128)] if esize == 4 else [(64, 64), (32, 64), (64, 32)]
+    for dims, perm in shapes:
+        for ta, tb in tiles:
+            for cps in (2, 6):
+                p = tt.Plan(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb,
+                            stages=stages, ctas_per_sm=cps)
+                d = p.describe()
+                assert d["vec"] == 1 and d["stages"] == stages
+                check(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb,
+                      stages=stages, ctas_per_sm=cps)
+
+
 ROW_SHAPES = [((600, 7, 5), (0, 2, 1)), ((256, 3, 5, 2), (0, 3, 1, 2)), ((8, 7, 5), (0, 2, 1)),
               ((6, 5, 7), (0, 2, 1)), ((1001, 3, 4), (0, 2, 1)), ((2, 300, 3, 17), (0, 3, 2, 1)),
               ((128, 2, 2, 2, 2, 2), (0, 5, 3, 1, 4, 2)), ((4, 4), (0, 1)),
