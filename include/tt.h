@@ -99,6 +99,8 @@ typedef struct {
     int accumulate;      /* 1 = accumulate plan for tt_execute_scaled (generic tile, 32-bit indices) */
     int slots;           /* TILE: elements per thread per tile (1, 2, 4, 8 or 16)   */
     int slot_dims;       /* TILE: 1 = slot-dim thread map when it applies, -1 = never, 0 = planner */
+    int sd_vmax;         /* TILE: largest slot-dim tile searched by the model, elements
+                            (<= 8192 for 4-byte, 6144 for 8-byte words); 0 = planner's default */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

@@ -372,6 +372,16 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
         for (int bi : {128, 256, 512, 1024})
             for (int bo : {128, 256, 512, 1024})
                 vars.push_back(opt(TT_KERNEL_TILE, std::max(2, bi / W), std::max(2, bo / W), 0, 0, 0));
+    // larger slot-dim tiles (up to 8192 elements; whole short dims instead of
+    // split ones): won up to 1.6x on Set-2 shapes and lost elsewhere, which the
+    // model cannot rank -- measurement can (tools/tile_runs_sweep.py)
+    if (hp.n >= 2 && hp.p[0] != 0)
+        for (int bi : {64, 128, 256, 512})
+            for (int bo : {64, 128, 256, 512}) {
+                tt_plan_options_t o = opt(TT_KERNEL_TILE, std::max(2, bi / W), std::max(2, bo / W), 0, 0, 0);
+                o.sd_vmax = 8192;
+                vars.push_back(o);
+            }
 
     std::vector<Plan*> cands{heur};
     std::vector<std::string> keys{describe_json(*heur)};

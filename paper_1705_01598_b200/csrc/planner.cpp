@@ -934,8 +934,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // medians (tools/knob_sweep.sh); the model cannot rank them.  By default
     // the slot-dim map is applied after the classic tile choice, by real
     // occupancy (below), which measured no losses.
-    const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144,
-                                                 (int)knob("TT_KNOB_SD_VMAX", 0)) : 0;
+    const int sdVmaxReq = opts && opts->sd_vmax ? opts->sd_vmax : (int)knob("TT_KNOB_SD_VMAX", 0);
+    const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144, sdVmaxReq) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
