@@ -13,6 +13,9 @@ OBJS      := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(SRCS_CU)) $(patsubst $(CSRC)
 HDRS      := $(wildcard $(CSRC)/*.h) include/tt.h
 NCCL_INC  := $(if $(NCCL_DIR),-I$(NCCL_DIR)/include,)
 NCCL_LNK  := $(if $(NCCL_DIR),-L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib,)
+CUDA_LIB  := /usr/local/cuda/lib64
+BLAS_DIR  := $(shell $(PYTHON) -c "import nvidia.cublas; print(list(nvidia.cublas.__path__)[0])" 2>/dev/null)
+BLAS_LNK  := -L$(CUDA_LIB) -lcublas $(if $(BLAS_DIR),-Xlinker -rpath=$(BLAS_DIR)/lib,) -Xlinker -rpath=$(CUDA_LIB)
 
 all: $(LIB) oracle/liboracle.so
 
@@ -25,7 +28,7 @@ $(BUILD)/%.o: $(CSRC)/%.cpp $(HDRS)
 	$(NVCC) $(NVFLAGS) $(NCCL_INC) -x cu -c $< -o $@ 2> $@.ptxas.txt || (cat $@.ptxas.txt; exit 1)
 
 $(LIB): $(OBJS) $(CSRC)/exports.map
-	$(NVCC) $(ARCH) -shared -Xlinker --version-script=$(CSRC)/exports.map -o $@.tmp $(OBJS) $(NCCL_LNK)
+	$(NVCC) $(ARCH) -shared -Xlinker --version-script=$(CSRC)/exports.map -o $@.tmp $(OBJS) $(NCCL_LNK) $(BLAS_LNK)
 	mv $@.tmp $@
 
 oracle/liboracle.so: oracle/tt_oracle.c

@@ -364,6 +364,58 @@ tt_status_t tt_execute_sharded_p2p(tt_plan_t plan, const void* in_local, void* c
  * `rank` entries each (either pointer may be NULL). */
 tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* local_out_dims);
 
+/* ------------------------------------------------------------------------
+ * Tensor contraction by TTGT (SURVEY f-4; Section 3.4): the
+ * workload the paper uses to show the transpose overhead inside a binary
+ * contraction, D = alpha * L . R + beta * D ("D = D + L . R"), as up
+ * to four transposes around one library GEMM (cuBLAS).
+ *
+ * Labels: modes_x[i] is the integer label (>= 0, distinct within a tensor)
+ * of dimension i of tensor x (dim 0 = stride-1, as tt_plan).  A label in L
+ * and R but not in D is contracted (summed); every label of D occurs in
+ * exactly one of L and R (labels in all three -- batch/Hadamard -- are
+ * TT_UNSUPPORTED); a label in one input only and not in D is
+ * TT_INVALID_PARAMETER.  D's extents come from L and R; contracted extents
+ * must match.  Elements: 4 = float, 8 = double (IEEE GEMM, no TF32).
+ * ---------------------------------------------------------------------- */
+typedef struct tt_contract_s* tt_contract_t;
+
+/*
+ * tt_contract_plan -- plan the contraction on the current device, enqueued on
+ * `stream`.  Allocates device workspace for the operands that need a
+ * transpose (vol(L), vol(R) and/or vol(D) elements; freed by
+ * tt_contract_destroy) and a cuBLAS handle.  rank_d may be 0 (full
+ * contraction to one element).  m, n, k >= 2^31 -> TT_UNSUPPORTED.
+ */
+tt_status_t tt_contract_plan(tt_contract_t* plan, int rank_d, const int* modes_d, int rank_l,
+                             const int64_t* dims_l, const int* modes_l, int rank_r,
+                             const int64_t* dims_r, const int* modes_r, size_t elem_size,
+                             tt_stream_t stream);
+
+/* Same without a GPU (describe only; execute returns TT_INVALID_DEVICE). */
+tt_status_t tt_contract_plan_offline(tt_contract_t* plan, int rank_d, const int* modes_d,
+                                     int rank_l, const int64_t* dims_l, const int* modes_l,
+                                     int rank_r, const int64_t* dims_r, const int* modes_r,
+                                     size_t elem_size);
+
+/*
+ * tt_contract_execute -- D = alpha * L . R + beta * D (device pointers, dense
+ * column-major tensors, aligned to elem_size; D distinct from L and R).
+ * Stream-ordered, asynchronous.  beta != 0 with a back transpose needs the
+ * accumulate form (32-bit indices) -- else TT_UNSUPPORTED.
+ */
+tt_status_t tt_contract_execute(tt_contract_t plan, const void* l, const void* r, void* d,
+                                double alpha, double beta);
+
+/* Milliseconds of the last execute's steps: transpose L, transpose R, GEMM,
+ * transpose D (zero for skipped steps; synchronises on that execute). */
+tt_status_t tt_contract_timings(tt_contract_t plan, float* ms4);
+
+/* JSON: m, n, k, which transposes run, GEMM ops, sub-plans. */
+tt_status_t tt_contract_describe(tt_contract_t plan, char* buf, size_t len);
+
+tt_status_t tt_contract_destroy(tt_contract_t plan);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

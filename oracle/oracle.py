@@ -72,6 +72,11 @@ def _load():
                                                   ctypes.c_void_p, ctypes.c_void_p,
                                                   ctypes.c_double, ctypes.c_double]
             lib.oracle_permute_scaled.restype = ctypes.c_int
+            dp = ctypes.POINTER(ctypes.c_double)
+            lib.oracle_contract.argtypes = [ctypes.c_int, i32p, ctypes.c_int, i64p, i32p, ctypes.c_int,
+                                            i64p, i32p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                            dp, dp, ctypes.c_double, ctypes.c_double]
+            lib.oracle_contract.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -243,4 +248,41 @@ def permute_scatter_py(dims, perm, words) -> np.ndarray:
             raise AssertionError("Eq. (1) map is not a bijection")
         written[q] = True
         out[q] = words[p_in]
+    return out
+
+
+def contract(modes_d, dims_l, modes_l, dims_r, modes_r, L, R, D0=None, alpha=1.0, beta=0.0):
+    """D = alpha * sum_contracted L * R + beta * D0, in float64, by
+    the plain double odometer of tt_oracle.c.  L, R: flat float32/float64
+    arrays in column-major order (dim 0 stride-1); D0: flat array or None.
+    Returns a flat float64 array in D's column-major order."""
+    L = np.ascontiguousarray(L)
+    R = np.ascontiguousarray(R)
+    if L.dtype != R.dtype or L.dtype not in (np.float32, np.float64):
+        raise ValueError("L and R must both be float32 or float64")
+    esize = L.dtype.itemsize
+    md = [int(x) for x in modes_d]
+    ml, mr = [int(x) for x in modes_l], [int(x) for x in modes_r]
+    dl, dr = [int(x) for x in dims_l], [int(x) for x in dims_r]
+    if L.size != int(np.prod(dl, dtype=np.int64)) or R.size != int(np.prod(dr, dtype=np.int64)):
+        raise ValueError("operand sizes do not match their dims")
+    ext = {}
+    for m, d in list(zip(ml, dl)) + list(zip(mr, dr)):
+        ext[m] = d
+    vol_d = int(np.prod([ext.get(m, 1) for m in md], dtype=np.int64))
+    out = np.empty(vol_d, dtype=np.float64)
+    dp = ctypes.POINTER(ctypes.c_double)
+    d0 = None
+    if D0 is not None:
+        d0 = np.ascontiguousarray(D0, dtype=np.float64)
+        if d0.size != vol_d:
+            raise ValueError("D0 size")
+    a32 = lambda v: (ctypes.c_int * max(1, len(v)))(*v)  # noqa: E731
+    a64 = lambda v: (ctypes.c_int64 * max(1, len(v)))(*v)  # noqa: E731
+    rc = _load().oracle_contract(
+        len(md), a32(md), len(ml), a64(dl), a32(ml), len(mr), a64(dr), a32(mr), esize,
+        L.ctypes.data, R.ctypes.data, d0.ctypes.data_as(dp) if d0 is not None else None,
+        out.ctypes.data_as(dp), float(alpha), float(beta))
+    if rc != 0:
+        raise ValueError("oracle rejected the contraction")
     return out

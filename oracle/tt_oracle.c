@@ -186,3 +186,99 @@ int oracle_permute_scaled(int rank, const int64_t* dims, const int* perm, int es
     }
     return ORACLE_OK;
 }
+
+/*
+ * Tensor contraction (Section 3.4; the contraction
+ * "D = D + L . R" of P:L321, with scale factors):
+ *
+ *   D[y] = alpha * sum_z L[x_L(y, z)] * R[x_R(y, z)] + beta * D0[y]
+ *
+ * Every dimension carries an integer label; y runs over D's labels, z over
+ * the contracted labels (in L and R, not in D); a tensor's element for a
+ * labelled coordinate is at sum over its dims of coordinate * stride, with
+ * column-major strides (dim 0 stride-1, as above).  Written out plainly: an
+ * odometer over D's coordinates, and for each output an odometer over the
+ * contracted coordinates, products and sums in double (float inputs are
+ * converted exactly), in the order the odometers visit them.  No blocking,
+ * no transposes, no GEMM.  D0 may be NULL (beta ignored).  Result in double.
+ * Returns ORACLE_BAD_ARG for labels that do not form a contraction.
+ */
+#define ORACLE_MAX_LABELS 64
+int oracle_contract(int rd, const int* md, int rl, const int64_t* dl, const int* ml, int rr,
+                    const int64_t* dr, const int* mr, int esize, const void* L, const void* R,
+                    const double* D0, double* D, double alpha, double beta) {
+    if (rd < 0 || rl < 0 || rr < 0 || rd > ORACLE_MAX_LABELS || rl > ORACLE_MAX_LABELS ||
+        rr > ORACLE_MAX_LABELS || (esize != 4 && esize != 8))
+        return ORACLE_BAD_ARG;
+    /* per D label: extent, stride in L, stride in R (0 when absent) */
+    int64_t ye[ORACLE_MAX_LABELS], ysl[ORACLE_MAX_LABELS], ysr[ORACLE_MAX_LABELS];
+    int64_t ze[ORACLE_MAX_LABELS], zsl[ORACLE_MAX_LABELS], zsr[ORACLE_MAX_LABELS];
+    int64_t sl[ORACLE_MAX_LABELS], sr[ORACLE_MAX_LABELS];
+    int64_t acc = 1;
+    for (int i = 0; i < rl; ++i) { sl[i] = acc; acc *= dl[i]; }
+    acc = 1;
+    for (int i = 0; i < rr; ++i) { sr[i] = acc; acc *= dr[i]; }
+    int nz = 0;
+    for (int j = 0; j < rd; ++j) {
+        int a = -1, b = -1;
+        for (int i = 0; i < rl; ++i) if (ml[i] == md[j]) a = i;
+        for (int i = 0; i < rr; ++i) if (mr[i] == md[j]) b = i;
+        if ((a < 0) == (b < 0)) return ORACLE_BAD_ARG;   /* in exactly one input */
+        ye[j] = a >= 0 ? dl[a] : dr[b];
+        ysl[j] = a >= 0 ? sl[a] : 0;
+        ysr[j] = b >= 0 ? sr[b] : 0;
+    }
+    for (int i = 0; i < rl; ++i) {
+        int inD = 0, b = -1;
+        for (int j = 0; j < rd; ++j) if (md[j] == ml[i]) inD = 1;
+        if (inD) continue;
+        for (int k = 0; k < rr; ++k) if (mr[k] == ml[i]) b = k;
+        if (b < 0 || dr[b] != dl[i]) return ORACLE_BAD_ARG;
+        ze[nz] = dl[i];
+        zsl[nz] = sl[i];
+        zsr[nz] = sr[b];
+        ++nz;
+    }
+    for (int k = 0; k < rr; ++k) {          /* every label of R is in D or in L */
+        int seen = 0;
+        for (int j = 0; j < rd; ++j) if (md[j] == mr[k]) seen = 1;
+        for (int i = 0; i < rl; ++i) if (ml[i] == mr[k]) seen = 1;
+        if (!seen) return ORACLE_BAD_ARG;
+    }
+    int64_t y[ORACLE_MAX_LABELS], z[ORACLE_MAX_LABELS];
+    int64_t volD = 1;
+    for (int j = 0; j < rd; ++j) { volD *= ye[j]; y[j] = 0; }
+    int64_t offL = 0, offR = 0;   /* of the current D coordinate y */
+    for (int64_t pos = 0; pos < volD; ++pos) {
+        double sum = 0.0;
+        int64_t zl = offL, zr = offR;
+        for (int k = 0; k < nz; ++k) z[k] = 0;
+        for (;;) {
+            double a, b;
+            if (esize == 4) {
+                a = (double)((const float*)L)[zl];
+                b = (double)((const float*)R)[zr];
+            } else {
+                a = ((const double*)L)[zl];
+                b = ((const double*)R)[zr];
+            }
+            sum += a * b;
+            int k = 0;
+            for (; k < nz; ++k) {           /* odometer over the contracted labels */
+                if (++z[k] < ze[k]) { zl += zsl[k]; zr += zsr[k]; break; }
+                zl -= (ze[k] - 1) * zsl[k];
+                zr -= (ze[k] - 1) * zsr[k];
+                z[k] = 0;
+            }
+            if (k == nz) break;
+        }
+        D[pos] = alpha * sum + (D0 ? beta * D0[pos] : 0.0);
+        for (int j = 0; j < rd; ++j) {      /* odometer over D's coordinates */
+            if (++y[j] < ye[j]) { offL += ysl[j]; offR += ysr[j]; break; }
+            offL -= (ye[j] - 1) * ysl[j];
+            offR -= (ye[j] - 1) * ysr[j];
+            y[j] = 0;
+        }
+    }
+    return 0;
+}

@@ -298,3 +298,4 @@ def permute_torch(x, axes, out=None, stream=None, **opts):
 
 from ._dist import (Comm, ShardedPlan, P2PShardedPlan, unique_id, plan_sharded_offline,  # noqa: E402
                     plan_sharded_p2p_offline)
+from ._contract import Contraction, contract_offline  # noqa: E402
