@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="s1", choices=["s1", "s2", "s5local", "s5redist"])
+    ap.add_argument("--config", default="s1", choices=["s1", "s2", "s5local", "s5redist", "s5p2p"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -56,7 +56,7 @@ def workload(name: str):
     if name == "s2":
         c = wl.s2_ttc()[30]
         return c, f"S2 TTC-style rank-{c.rank} fp64 case {c.name} dims {c.dims} perm {c.perm}"
-    if name in ("s5local", "s5redist"):
+    if name in ("s5local", "s5redist", "s5p2p"):
         c = wl.s5_sharded()[0 if name == "s5local" else 5]
         return c, f"S5 {name[2:]} 112x112x112x104 fp64 perm {c.perm} (BASELINE.json configs[4])"
     raise ValueError(name)
@@ -245,7 +245,12 @@ def run_ours(args):
     case, desc = workload(args.config)
     E = case.esize
     tdt = torch.int32 if E == 4 else torch.int64
-    sharded = args.config == "s5redist" and world > 1
+    # s5p2p: the fused redistribution (f-1); on one GPU the redistribution is
+    # forced with a one-rank communicator (registration + both barriers run)
+    p2p = args.config == "s5p2p"
+    if p2p and world == 1:
+        os.environ["TT_SHARD_FORCE_REDIST"] = "1"
+    sharded = (args.config == "s5redist" and world > 1) or p2p
     local_vol = case.vol // world if sharded else case.vol
 
     # seeded input, resident in HBM before timing (rank-specific seed).
@@ -259,7 +264,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=dev)
 
-    if sharded:
+    if p2p:
+        comm = tt.Comm.from_process_group() if world > 1 else tt.Comm(tt.unique_id(), 1, 0)
+        plan = tt.P2PShardedPlan(comm, case.dims, case.perm, E, stream=stream)
+        plan.register_output(y)
+        execute = plan.execute
+        units_per_step_all = case.vol  # global tensor per step
+    elif sharded:
         comm = tt.Comm.from_process_group()
         plan = tt.ShardedPlan(comm, case.dims, case.perm, E, stream=stream)
         execute = plan.execute
@@ -372,7 +383,8 @@ def run_ours(args):
             "config": {
                 "workload": desc, "dims": list(case.dims), "perm": list(case.perm),
                 "elem_bytes": E, "global_batch": world if not sharded else 1,
-                "parallelism": ("sharded all-to-all" if sharded else
+                "parallelism": ("sharded, fused P2P redistribution" if p2p else
+                                "sharded all-to-all" if sharded else
                                 ("independent tensor per GPU" if world > 1 else "single GPU")),
                 "l2": "inputs larger than L2 (%.0f MB per tensor > 126 MB L2); no flush" % (local_vol * E / 1e6),
                 "plan": {k: desc_plan.get(k) for k in ("kernel", "threads", "grid", "smem", "nreg")},
