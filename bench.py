@@ -280,6 +280,11 @@ def run_ours(args):
         execute = plan.execute
         units_per_step_all = case.vol * world
     desc_plan = plan.describe()
+    if desc_plan.get("sharded"):  # report the dominant sub-plan (fused / local / pack)
+        for key in ("fused", "local", "pack"):
+            if key in desc_plan:
+                desc_plan = dict(desc_plan[key], sharded_mode=desc_plan["mode"])
+                break
 
     sampler = ClockSampler(local)
     sampler.start()
