@@ -372,6 +372,20 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
         for (int bi : {128, 256, 512, 1024})
             for (int bo : {128, 256, 512, 1024})
                 vars.push_back(opt(TT_KERNEL_TILE, std::max(2, bi / W), std::max(2, bo / W), 0, 0, 0));
+    // whole-dimension prefix products as run targets (tiles without split
+    // dims; the heuristic takes them only when they keep the output run)
+    if (hp.n >= 2 && hp.p[0] != 0) {
+        std::vector<int64_t> pin, pout;
+        int64_t P = 1;
+        for (int i = 0; i < hp.n && P * hp.d[i] <= 4096; ++i) { P *= hp.d[i]; if (P >= 8) pin.push_back(P); }
+        P = 1;
+        for (int j = 0; j < hp.n && P * hp.d[hp.p[j]] <= 4096; ++j) {
+            P *= hp.d[hp.p[j]];
+            if (P >= 8) pout.push_back(P);
+        }
+        for (int64_t a : pin)
+            for (int64_t b : pout) vars.push_back(opt(TT_KERNEL_TILE, (int)a, (int)b, 0, 0, 0));
+    }
     // larger slot-dim tiles (up to 8192 elements; whole short dims instead of
     // split ones): won up to 1.6x on Set-2 shapes and lost elsewhere, which the
     // model cannot rank -- measurement can (tools/tile_runs_sweep.py)

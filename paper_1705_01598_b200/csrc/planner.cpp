@@ -939,33 +939,58 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
-    // whole-dimension runs as targets too (no split, no ragged tiles)
-    if (knob("TT_KNOB_PREFIX_TARGETS", 0) != 0) {
+    // Whole-dimension prefix products as run targets too (tiles without a
+    // split dim, no ragged chunks).  They are searched separately: on the
+    // suites (tools/knob_ab.sh, profiles/round1_knob_ab_prefix.txt) they won
+    // up to 1.36x where they kept or lengthened the OUTPUT run and lost up to
+    // 0.62x where they bought a longer input run with a shorter output run --
+    // short write runs cost more on B200 than the sector model charges.  So a
+    // prefix tile replaces the power-of-two choice only when the model prefers
+    // it AND its output run is at least as long (and its input run not below
+    // half, unless the output run at least doubles).
+    std::vector<int64_t> prefix;
+    const int prefixKnob = (int)knob("TT_KNOB_PREFIX_TARGETS", -1);  // -1 default rule, 0 off, 1 free
+    if (prefixKnob != 0) {
         int64_t P = 1;
         for (int i = 0; i < pr.n && P * pr.d[i] <= std::max(Vmax, VmaxSd); ++i) {
             P *= pr.d[i];
-            if (P >= 2) targets.push_back(P);
+            if (P >= 2) prefix.push_back(P);
         }
         P = 1;
         for (int j = 0; j < pr.n && P * pr.d[pr.p[j]] <= std::max(Vmax, VmaxSd); ++j) {
             P *= pr.d[pr.p[j]];
-            if (P >= 2) targets.push_back(P);
+            if (P >= 2) prefix.push_back(P);
         }
-        std::sort(targets.begin(), targets.end());
-        targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+        std::sort(prefix.begin(), prefix.end());
+        prefix.erase(std::unique(prefix.begin(), prefix.end()), prefix.end());
     }
     TileCand best;
     const int forceThreads = opts ? opts->threads : 0;
     const int forceR = opts ? opts->slots : 0;
-    for (int64_t ti : targets) {
-        for (int64_t to : targets) {
-            int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
-            int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-            TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                    VmaxSd);
-            if (!c.ok) continue;
-            if (!best.ok || c.cost_us < best.cost_us) best = c;
+    auto search = [&](const std::vector<int64_t>& tin, const std::vector<int64_t>& tout, TileCand& b) {
+        for (int64_t ti : tin) {
+            for (int64_t to : tout) {
+                int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
+                int64_t Tout = opts && opts->run_out ? opts->run_out : to;
+                TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                        VmaxSd);
+                if (!c.ok) continue;
+                if (!b.ok || c.cost_us < b.cost_us) b = c;
+            }
         }
+    };
+    search(targets, targets, best);
+    if (!prefix.empty() && !(opts && (opts->run_in || opts->run_out))) {
+        std::vector<int64_t> all = targets;
+        all.insert(all.end(), prefix.begin(), prefix.end());
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+        TileCand px;
+        search(all, all, px);
+        const bool keepsOut = best.ok && px.ok && px.runOut >= best.runOut &&
+                              (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
+        if (px.ok && (!best.ok || (px.cost_us < best.cost_us && (prefixKnob == 1 || keepsOut))))
+            best = px;
     }
     if (!best.ok) {
         // fall back to the smallest legal tile

@@ -10,7 +10,12 @@ import torch  # noqa: E402
 
 import paper_1705_01598_b200 as tt  # noqa: E402
 
-CASES = [((5, 3, 2, 4, 35, 33, 37, 40), (7, 6, 5, 4, 3, 2, 1, 0), 4),
+CASES = [((7,) * 10, (0, 2, 1, 3, 5, 4, 8, 7, 9, 6), 4),
+         ((7, 4, 11, 14, 12, 3, 12, 5, 5, 3), (0, 6, 8, 1, 3, 5, 4, 9, 2, 7), 4),
+         ((5, 7, 7, 7, 7, 7, 7, 7, 7, 7), (0, 8, 3, 1, 5, 7, 4, 6, 2, 9), 8),
+         ((1, 2, 25, 2, 3, 2, 6, 4, 23, 19, 2, 19), (0, 8, 11, 4, 10, 3, 2, 6, 1, 7, 5, 9), 8),
+         ((5,) * 12, (0, 11, 3, 10, 6, 8, 4, 7, 2, 9, 5, 1), 8),
+((5, 3, 2, 4, 35, 33, 37, 40), (7, 6, 5, 4, 3, 2, 1, 0), 4),
          ((5,) * 12, (0, 8, 4, 10, 1, 3, 9, 5, 7, 2, 6, 11), 4),
          ((2, 3, 4, 3, 2, 2, 3, 2, 20, 18, 22, 24), tuple(range(11, -1, -1)), 4),
          ((5, 3, 2, 4, 35, 33, 37, 40), (6, 4, 1, 7, 5, 3, 0, 2), 4),
@@ -44,10 +49,23 @@ def main():
         t0 = timed(p0, x, ref)
         res = {"dims": dims, "perm": perm, "default": round(2 * n * E / t0 / 1e6, 1),
                "default_tile": p0.describe()["tile"]["ext"], "v": []}
+        # run targets: powers of two and whole-dimension prefix products
+        pin, pout, acc = [], [], 1
+        for d in dims:
+            acc *= d
+            if 2 <= acc <= 8192:
+                pin.append(acc)
+        acc = 1
+        for j in perm:
+            acc *= dims[j]
+            if 2 <= acc <= 8192:
+                pout.append(acc)
+        tin = sorted(set([16, 32, 64, 128, 256, 512] + pin))
+        tout = sorted(set([16, 32, 64, 128, 256, 512, 1024] + pout))
         for vmax in ("0", "8192"):
             os.environ["TT_KNOB_SD_VMAX"] = vmax
-            for ri in (16, 32, 64, 128, 256, 512):
-                for ro in (16, 32, 64, 128, 256, 512, 1024):
+            for ri in tin:
+                for ro in tout:
                     try:
                         p = tt.Plan(dims, perm, E, run_in=ri, run_out=ro)
                     except tt.TTError:
@@ -61,7 +79,7 @@ def main():
                                      d["threads"], d["grid"], "sd" in d["tile"]))
         os.environ["TT_KNOB_SD_VMAX"] = "0"
         res["v"].sort(key=lambda r: -r[3] if isinstance(r[3], float) else 0)
-        res["v"] = res["v"][:8]
+        res["v"] = res["v"][:6]
         print(json.dumps(res), flush=True)
 
 
