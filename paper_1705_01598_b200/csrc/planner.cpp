@@ -936,6 +936,13 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // occupancy (below), which measured no losses.
     const int sdVmaxReq = opts && opts->sd_vmax ? opts->sd_vmax : (int)knob("TT_KNOB_SD_VMAX", 0);
     const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144, sdVmaxReq) : 0;
+    // Larger slot-dim tiles (up to 8192 elements) under the same output-run
+    // rule as the prefix targets (TT_KNOB_SD_RULE: 0 off, else the tile
+    // limit).  Same-box A/B on the suites (profiles/round1_knob_ab_sd_rule.txt):
+    // 17 cases changed, median 1.016x, up to 1.28x, one loss of 0.88x; Set 2
+    // median 0.796 -> 0.803 of memcpy.
+    const int sdRule = (int)knob("TT_KNOB_SD_RULE", 8192);
+    const int VmaxSdRule = (sdAllowed && VmaxSd == 0 && sdRule > 0) ? std::min(E == 4 ? 8192 : 6144, sdRule) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
         targets.push_back(std::max<int64_t>(2, b / E));
@@ -991,6 +998,30 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
                               (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
         if (px.ok && (!best.ok || (px.cost_us < best.cost_us && (prefixKnob == 1 || keepsOut))))
             best = px;
+    }
+    if (VmaxSdRule > 0 && !(opts && (opts->run_in || opts->run_out)) && best.ok) {
+        std::vector<int64_t> all = targets;
+        all.insert(all.end(), prefix.begin(), prefix.end());
+        for (int i = 0, P = 1; i < pr.n && P * pr.d[i] <= VmaxSdRule; ++i) {
+            P *= (int)pr.d[i];
+            if (P >= 2) all.push_back(P);
+        }
+        for (int j = 0, P = 1; j < pr.n && P * pr.d[pr.p[j]] <= VmaxSdRule; ++j) {
+            P *= (int)pr.d[pr.p[j]];
+            if (P >= 2) all.push_back(P);
+        }
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+        TileCand sx;
+        for (int64_t ti : all)
+            for (int64_t to : all) {
+                TileCand c = build_tile(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                        VmaxSdRule);
+                if (c.ok && (!sx.ok || c.cost_us < sx.cost_us)) sx = c;
+            }
+        const bool keepsOut = sx.ok && sx.runOut >= best.runOut &&
+                              (2 * sx.runIn >= best.runIn || sx.runOut >= 2 * best.runOut);
+        if (sx.ok && sx.cost_us < best.cost_us && keepsOut) best = sx;
     }
     if (!best.ok) {
         // fall back to the smallest legal tile
