@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out/final
+O=gpurun_out/final
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu2.txt 2>&1
+timeout 2400 python bench_suite.py --suite s2,s3,set2,s4 --per-cell 1 --plan both --out $O/suites.jsonl > /dev/null 2> $O/suites.err
+timeout 600 python bench.py > $O/bench2.json 2> $O/bench2.err
