@@ -738,6 +738,22 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     } else if (vec_ok(2)) {
         vec = 2;
     }
+    // 2-element vectors vs the scalar kernel (knobs TT_KNOB_T2D_VEC2 /
+    // TT_KNOB_T2D_VEC8: 1 = always vectors, 0 = always scalar).
+    //
+    // Defaults from the same-box A/B (tools/vec2_ab.py,
+    // profiles/round1_vec2_ab.jsonl): for 4-byte words the scalar kernel beat
+    // 8-byte vectors on every shape (+12-17 %); for 8-byte words 16-byte
+    // vectors win on large 2-D extents (+17 %) but lose on ragged ~100-600
+    // extents (-6-8 %), so they are kept only when 64x64 tiles are >= 95 %
+    // full.
+    {
+        const double fill64 = (double)dA / (64.0 * ceil_div(dA, 64)) * (double)dB / (64.0 * ceil_div(dB, 64));
+        if (pr.esize == 4 && vec == 2 && knob("TT_KNOB_T2D_VEC2", 0) == 0) vec = 0;
+        if (pr.esize == 8 && vec == 2 &&
+            (knob("TT_KNOB_T2D_VEC8", -1) == 0 || (knob("TT_KNOB_T2D_VEC8", -1) < 0 && fill64 < 0.95)))
+            vec = 0;
+    }
     if (vec == 0) vec = 1;  // scalar 2-D kernel (padded staging)
     // default tiles from the B200 calibration sweep (tools/sweep.py t2d,
     // profiles/round1_sweep_t2d.md): 64 x 128 for 4-byte words with 16-byte

@@ -146,6 +146,23 @@ def test_forced_tiled2d(esize):
 
 
 @pytest.mark.parametrize("esize", [4, 8])
+def test_two_element_vector_2d_kernels(esize, monkeypatch):
+    """The 2-element-vector 2-D kernels (8-byte vectors of fp32, 16-byte of
+    fp64), reachable through TT_KNOB_T2D_VEC2 / _VEC8 = 1 since the scalar
+    kernel is the default for most of their shapes."""
+    monkeypatch.setenv("TT_KNOB_T2D_VEC2", "1")
+    monkeypatch.setenv("TT_KNOB_T2D_VEC8", "1")
+    shapes = [((66, 62), (1, 0)), ((130, 6, 34), (2, 1, 0)), ((1002, 998), (1, 0)),
+              ((34, 3, 98), (2, 1, 0)), ((586, 5, 42), (1, 0, 2))]
+    tiles = [(32, 64), (64, 64)] if esize == 4 else [(32, 32), (64, 32), (32, 64), (64, 64)]
+    for dims, perm in shapes:
+        assert tt.Plan(dims, perm, esize, kernel=tt.KERNEL_TILED2D).describe()["vec"] == 2
+        check(dims, perm, esize, kernel=tt.KERNEL_TILED2D)
+        for ta, tb in tiles:
+            check(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta, run_out=tb)
+
+
+@pytest.mark.parametrize("esize", [4, 8])
 @pytest.mark.parametrize("stages", [3, 4])
 def test_scalar_tiled2d_async_ring(esize, stages):
     """Scalar 2-D kernel with the cp.async ring (tiled2d_sa_kernel): odd

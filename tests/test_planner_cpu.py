@@ -139,7 +139,9 @@ def test_tiled2d_geometry(dims, perm, esize):
                 j = tt.plan_offline(dims, perm, esize, kernel=tt.KERNEL_TILED2D, run_in=ta,
                                     run_out=tb, grid_order=order)
             except tt.TTError:
-                assert esize == 4 and 2 in {dims[0] % 4, dims[perm[0]] % 4}  # VW=2 tiles only
+                # tile not instantiated for the vector width the planner chose
+                # (2-element vectors only where the knobs allow them; scalar
+                # kernel tiles are 64x64, 128x64, 64x128 / 64x64, 32x64, 64x32)
                 continue
             assert j["kernel"] == "tiled2d"
             fj = dict(j)
@@ -147,12 +149,22 @@ def test_tiled2d_geometry(dims, perm, esize):
             np.testing.assert_array_equal(interpret_tiled2d_plan(fj, words), want)
 
 
-def test_tiled2d_vector_width_and_rejections():
-    # odd extents take the scalar 2-D kernel (vec 1), even ones vectors
+def test_tiled2d_vector_width_and_rejections(monkeypatch):
+    # odd extents take the scalar 2-D kernel (vec 1), multiples of 4 16-byte vectors
     assert tt.plan_offline((13, 64), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 1
     assert tt.plan_offline((64, 63), (1, 0), 8, kernel=tt.KERNEL_TILED2D)["vec"] == 1
-    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 2
     assert tt.plan_offline((64, 60), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 4
+    # 2-element vectors (profiles/round1_vec2_ab.jsonl): 4-byte words -> scalar
+    # kernel; 8-byte words keep 16-byte vectors only with >= 95 % full 64x64 tiles
+    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 1
+    assert tt.plan_offline((11586, 11586), (1, 0), 8)["vec"] == 2
+    assert tt.plan_offline((584, 584, 584), (2, 1, 0), 8)["vec"] == 1
+    monkeypatch.setenv("TT_KNOB_T2D_VEC2", "1")
+    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 2
+    monkeypatch.setenv("TT_KNOB_T2D_VEC8", "1")
+    assert tt.plan_offline((584, 584, 584), (2, 1, 0), 8)["vec"] == 2
+    monkeypatch.delenv("TT_KNOB_T2D_VEC2")
+    monkeypatch.delenv("TT_KNOB_T2D_VEC8")
     with pytest.raises(tt.TTError):   # fastest dim unchanged: not the Tiled class
         tt.plan_offline((64, 8, 8), (0, 2, 1), 4, kernel=tt.KERNEL_TILED2D)
     with pytest.raises(tt.TTError):   # tile not instantiated for the scalar kernel
@@ -303,7 +315,9 @@ def test_strided_plan_validation():
     j = tt.plan_offline((4, 5), (1, 0), 4, in_strides=(1, 4), out_strides=(1, 5))
     assert j["dense"] is True and j["kernel"] in ("tiled2d", "tile")   # dense layout recognised
     j = tt.plan_offline((64, 64), (1, 0), 4, in_strides=(1, 66), out_strides=(1, 68))
-    assert j["dense"] is False and j["kernel"] == "tiled2d" and j["vec"] == 2
+    # strides 66 / 68 are multiples of 2, not 4: 2-element rows -> the scalar
+    # 2-D kernel by default for 4-byte words
+    assert j["dense"] is False and j["kernel"] == "tiled2d" and j["vec"] == 1
 
 
 @pytest.mark.parametrize("dims,perm,esize", [
