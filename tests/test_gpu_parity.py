@@ -153,7 +153,7 @@ def test_two_element_vector_2d_kernels(esize, monkeypatch):
     monkeypatch.setenv("TT_KNOB_T2D_VEC2", "1")
     monkeypatch.setenv("TT_KNOB_T2D_VEC8", "1")
     shapes = [((66, 62), (1, 0)), ((130, 6, 34), (2, 1, 0)), ((1002, 998), (1, 0)),
-              ((34, 3, 98), (2, 1, 0)), ((586, 5, 42), (1, 0, 2))]
+              ((34, 3, 98), (2, 1, 0)), ((586, 6, 42), (1, 0, 2))]
     tiles = [(32, 64), (64, 64)] if esize == 4 else [(32, 32), (64, 32), (32, 64), (64, 64)]
     for dims, perm in shapes:
         assert tt.Plan(dims, perm, esize, kernel=tt.KERNEL_TILED2D).describe()["vec"] == 2
