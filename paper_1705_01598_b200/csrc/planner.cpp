@@ -1125,7 +1125,14 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.threads = 256;
         // scalar 2-D kernel: register double buffer, or a cp.async ring of
         // 3-4 stages (tiled2d_sa_kernel; 32-bit indices)
-        const int st2 = opts && opts->stages >= 3 ? std::min(4, opts->stages) : 0;
+        // Default: the ring (4 stages, 1 CTA/SM) for 8-byte words on a plain
+        // rank-2 problem (no batch dims): +5-10 % over the register version
+        // on large odd 2-D fp64 transposes; batched (rank >= 3) and 4-byte
+        // cases stay on the register version (tools/sweep_t2d_async.py big,
+        // profiles/round1_sweep_t2d_big.jsonl).
+        const bool ringDefault = vec2d == 1 && E == 8 && pr.n == 2 &&
+                                 !(opts && (opts->stages || opts->ctas_per_sm));
+        const int st2 = opts && opts->stages >= 3 ? std::min(4, opts->stages) : (ringDefault ? 4 : 0);
         kc.stages = (vec2d == 1 && st2 && !kc.idx64) ? st2 : 0;
         kc.smem = vec2d == 1 ? (kc.stages ? kc.stages : 2) * ta2d * (tb2d + 1) * E
                              : 2 * ta2d * tb2d * E;
@@ -1138,6 +1145,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         // beyond the 3 that fit, a second partial wave that balances the
         // tail, measured best)
         int per2 = opts && opts->ctas_per_sm ? opts->ctas_per_sm
+                   : (ringDefault && kc.stages) ? 1
                    : vec2d == 1 ? (E == 8 ? 4 : std::min(3, occ2)) : std::min(2, occ2);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.t2d.nTiles, (int64_t)dev.num_sms * per2));
         const double bytes = 2.0 * pr.vol * E / std::max(0.3, std::min(1.0, fill2d + 0.3));
