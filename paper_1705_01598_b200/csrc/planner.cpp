@@ -1130,7 +1130,9 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         // on large odd 2-D fp64 transposes; batched (rank >= 3) and 4-byte
         // cases stay on the register version (tools/sweep_t2d_async.py big,
         // profiles/round1_sweep_t2d_big.jsonl).
-        const bool ringDefault = vec2d == 1 && E == 8 && pr.n == 2 &&
+        // Suites: it lost where the output-fastest extent was short (585:
+        // 0.87 -> 0.64 of memcpy, 154: -1 %), so only from 2048 up.
+        const bool ringDefault = vec2d == 1 && E == 8 && pr.n == 2 && pr.d[pr.p[0]] >= 2048 &&
                                  !(opts && (opts->stages || opts->ctas_per_sm));
         const int st2 = opts && opts->stages >= 3 ? std::min(4, opts->stages) : (ringDefault ? 4 : 0);
         kc.stages = (vec2d == 1 && st2 && !kc.idx64) ? st2 : 0;
