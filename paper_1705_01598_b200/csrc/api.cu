@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -176,7 +177,16 @@ static tt_status_t build_pipe(Plan& p) {
     const int t = p.perm[n - 1];
     const int64_t dt = p.dims[t];
     if (dt < 2) return TT_UNSUPPORTED;
-    const int nch = (int)std::min<int64_t>(dt, 8);
+    // chunks of >= 16 MB, at most 32 (S1 e2e: 4 / 8 / 16 / 32 chunks =
+    // 82 / 88 / 90 / 92 GB/s -- both PCIe directions near their limit; more
+    // chunks shorten the pipeline's fill and drain); knob for calibration
+    const char* kn = std::getenv("TT_KNOB_PIPE_CHUNKS");
+    int64_t volAll = 1;
+    for (int64_t x : p.dims) volAll *= x;
+    const int64_t bytesAll = volAll * (p.prob.esize / p.widen);
+    const int want = kn && *kn ? std::max(2, std::atoi(kn))
+                               : (int)std::max<int64_t>(2, std::min<int64_t>(32, bytesAll >> 24));
+    const int nch = (int)std::min<int64_t>(dt, want);
     HostPipe* hp = new (std::nothrow) HostPipe();
     if (!hp) return TT_INTERNAL_ERROR;
     hp->device = p.device;
