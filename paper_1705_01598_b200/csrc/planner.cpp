@@ -932,6 +932,13 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
                                      force2d && opts ? opts->run_out : 0,
                                      opts && opts->grid_order ? opts->grid_order : 2);
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
+    // fill of the output-fastest (B) side alone: short B extents leave the
+    // 2-D kernel short write runs and half-empty tiles
+    // Same-box A/B over the S2/S3/Set-2 suites (tools/ab_fillb.sh,
+    // profiles/round1_ab_fillb.txt): below these fills the generic tile won
+    // (up to 1.5x); 8-byte words lost above 0.8.
+    const double fillB2d = can2d ? (double)pr.d[pr.p[0]] / ((double)tb2d * ceil_div(pr.d[pr.p[0]], tb2d)) : 0.0;
+    const double fillBMin = knob(E == 4 ? "TT_KNOB_T2D_FILLB4" : "TT_KNOB_T2D_FILLB8", E == 4 ? 0.9 : 0.8);
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
     // 512 threads x 8 slots, and staging byte offsets < 2^16 (16-bit packing)
@@ -1115,7 +1122,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // VW elements per instruction on both sides (model: its issue cost is a
     // fraction of the generic kernel's, DRAM sectors are whole).
     const bool want2d = forced == TT_KERNEL_TILED2D ||
-                        (forced == TT_KERNEL_AUTO && can2d && fill2d >= 0.6 &&
+                        (forced == TT_KERNEL_AUTO && can2d && fill2d >= knob("TT_KNOB_T2D_FILL", 0.6) &&
+                         fillB2d >= fillBMin &&
                          !(opts && (opts->run_in || opts->run_out)));
     if (want2d) {
         kc.kernel = TT_KERNEL_TILED2D;

@@ -429,9 +429,9 @@ def test_strided_plans(esize):
         np.testing.assert_array_equal(got, want, err_msg=f"{dims} {perm} {sin} {sout}")
         plan.destroy()
     # a 2-D transpose between padded row pitches (vector 2-D kernel)
-    dims, perm, sin, sout = (256, 192), (1, 0), (1, 260), (1, 196)
-    inbuf = wl.random_words(260 * 192, esize, 3)
-    outbuf = wl.random_words(196 * 256, esize, 4)
+    dims, perm, sin, sout = (192, 256), (1, 0), (1, 196), (1, 260)
+    inbuf = wl.random_words(196 * 256, esize, 3)
+    outbuf = wl.random_words(260 * 192, esize, 4)
     plan = tt.Plan(dims, perm, esize, in_strides=sin, out_strides=sout)
     assert plan.describe()["kernel"] == "tiled2d"
     y = to_dev(outbuf)

@@ -4,6 +4,7 @@ arm A = the default plan, arm B = the plan with the given options.
     python tools/ab_opts.py --suite s3,set2 [--kernel-filter tile] slots=8 [key=value ...]
 Ratio = time(B) / time(A) (< 1: the options are faster)."""
 import argparse
+import json
 import os
 import statistics
 import sys
@@ -25,6 +26,8 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--kernel-filter", default="")
     ap.add_argument("--esize", type=int, default=0)
+    ap.add_argument("--env", action="append", default=[],
+                    help="KEY=VAL planner knob set for arm B only; cases whose plans agree are skipped")
     a = ap.parse_args()
     opts = {k: int(v) for k, v in (o.split("=") for o in a.opts)}
     s = torch.cuda.current_stream()
@@ -37,13 +40,22 @@ def main():
         if a.kernel_filter and da["kernel"] != a.kernel_filter:
             pa.destroy()
             continue
+        env = dict(kv.split("=", 1) for kv in a.env)
+        os.environ.update(env)
         try:
             pb = tt.Plan(c.dims, c.perm, c.esize, **opts)
         except tt.TTError as e:
             print(f"{c.name:14s} B plan failed: {e}")
             pa.destroy()
             continue
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
         db = pb.describe()
+        if env and json.dumps(da, sort_keys=True) == json.dumps(db, sort_keys=True):
+            pa.destroy()
+            pb.destroy()
+            continue
         td = torch.int32 if c.esize == 4 else torch.int64
         x = torch.randint(-2**31, 2**31 - 1, (c.vol,), dtype=td, device="cuda")
         ya, yb = torch.empty_like(x), torch.empty_like(x)
