@@ -860,9 +860,15 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
 
     // (ii) fastest dim unchanged with long rows: row copy, no staging
     const bool rowClass = pr.n >= 2 && pr.p[0] == 0 && pr.dense;
+    // Minimum row bytes for the row copy.  Same-box A/B over the suites
+    // (tools/ab_rowmin.sh, profiles/round1_ab_rowmin.txt): for widened rows
+    // (several elements per word) the generic tile beat the row copy on 12
+    // of 13 cases below 4 KB rows (up to 1.39x, one loss of 0.95x); for
+    // un-widened rows it lost on 7 of 8, so those keep 512 B.
+    const double rowMin = pr.widen > 1 ? knob("TT_KNOB_ROW_MIN_W", 4096) : knob("TT_KNOB_ROW_MIN", 512);
     if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
     if (!acc && rowClass && (forced == TT_KERNEL_ROWCOPY ||
-                     (forced == TT_KERNEL_AUTO && pr.d[0] * E >= 512 &&
+                     (forced == TT_KERNEL_AUTO && pr.d[0] * E >= rowMin &&
                       !(opts && (opts->run_in || opts->run_out))))) {
         RowParams& r = plan.row;
         std::memset(&r, 0, sizeof(r));
