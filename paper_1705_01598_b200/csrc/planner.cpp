@@ -452,6 +452,19 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
             P *= pr.d[i];
         }
     }
+    // Balanced chunks: a split dim cut into k chunks of `need` with a short
+    // tail keeps k chunks but leaves slots idle in every ragged tile (5 in
+    // chunks of 3, 4 in chunks of 3); when the chunks fill less than
+    // TT_KNOB_SPLIT_BAL of k * need, use k equal chunks instead.
+    {
+        const double bal = knob("TT_KNOB_SPLIT_BAL", 0.0);
+        for (int i = 0; i < n; ++i) {
+            if (need[i] > 1 && need[i] < pr.d[i]) {
+                const int64_t k = ceil_div(pr.d[i], need[i]);
+                if ((double)pr.d[i] / ((double)k * need[i]) < bal) need[i] = ceil_div(pr.d[i], k);
+            }
+        }
+    }
     long double V = 1;
     for (int i = 0; i < n; ++i) V *= (long double)need[i];
     if (V > std::max(Vmax, VmaxSd)) return c;
