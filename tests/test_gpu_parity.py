@@ -439,3 +439,15 @@ def test_strided_plans(esize):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(y.cpu().numpy().view(outbuf.dtype),
                                   orc.permute_strided(dims, perm, inbuf, sin, outbuf, sout))
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_classification_threshold_shapes(case):
+    """The shapes on both sides of the measured classification thresholds
+    (test_planner_cpu.RULE_SHAPES), bit-exact on the GPU."""
+    from test_planner_cpu import RULE_SHAPES
+    dims, perm, esize, kernel = RULE_SHAPES[case]
+    plan = tt.Plan(dims, perm, esize)
+    assert plan.describe()["kernel"] == kernel
+    plan.destroy()
+    check(dims, perm, esize, seed=case)

@@ -337,3 +337,22 @@ def test_rowcopy_segmented_rows_match_oracle(dims, perm, esize):
         assert r["nRows"] > vol // dims[0] and r["row"] * j["word_size"] >= 2048
     words = wl.random_words(vol, esize, 78)
     np.testing.assert_array_equal(interpret_plan(j, words), orc.permute(dims, perm, words))
+
+
+# Shapes where the measured classification thresholds decide (DESIGN.md,
+# "Classification thresholds"): short output-fastest extents leave the 2-D
+# kernel for the generic tile; widened rows under 4 KB leave the row copy.
+RULE_SHAPES = [((1304, 101, 50), (1, 0, 2), 8, "tile"),    # B fill 101/128 < 0.8
+               ((300, 57, 40), (1, 0, 2), 4, "tile"),      # B fill 57/64 < 0.9
+               ((1000, 125, 24), (1, 0, 2), 8, "tiled2d"),  # B fill 125/128
+               ((138, 21, 16, 10), (0, 2, 3, 1), 4, "tile"),    # 2 x 69 words, 552-byte rows
+               ((1304, 21, 16, 10), (0, 2, 3, 1), 8, "rowcopy"),  # 16-byte words, 10 KB rows
+               ((1001, 3, 4), (0, 2, 1), 8, "rowcopy")]   # un-widened 8 KB rows
+
+
+@pytest.mark.parametrize("dims,perm,esize,kernel", RULE_SHAPES)
+def test_classification_thresholds(dims, perm, esize, kernel):
+    j = tt.plan_offline(dims, perm, esize)
+    assert j["kernel"] == kernel
+    words = wl.random_words(int(np.prod(dims)), esize, 91)
+    np.testing.assert_array_equal(interpret_plan(j, words), orc.permute(dims, perm, words))
