@@ -95,7 +95,9 @@ typedef struct {
     int grid_order;      /* TILED2D tile order: 1 = A-chunks fastest, 2 = B-chunks fastest;
                             TILE: 1/0 = interleaved tiles over CTAs, 2 = contiguous ranges */
     int no_widen;        /* 1 = never regroup elements of an unchanged fastest dim into wider words */
-    int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner */
+    int stages;          /* TILE: -1 = register double buffer, 3 = cp.async 3-stage ring, 0 = planner;
+                            with slot_dims = 1: 3 or 4 = slot-dim map with a cp.async ring of that
+                            many stages (tile_sd_async_kernel)                                   */
     int accumulate;      /* 1 = accumulate plan for tt_execute_scaled (generic tile, 32-bit indices) */
     int slots;           /* TILE: elements per thread per tile (1, 2, 4, 8 or 16)   */
     int slot_dims;       /* TILE: 1 = slot-dim thread map when it applies, -1 = never, 0 = planner */

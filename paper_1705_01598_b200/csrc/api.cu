@@ -407,6 +407,17 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
                 vars.push_back(o);
             }
 
+    // the heuristic tile on the slot-dim map with a cp.async ring of 3 or 4
+    // stages (tile_sd_async_kernel): mixed on the suites, up to 1.18x on
+    // latency-bound 4-byte gathers (profiles/round1_ab_sd_async.txt)
+    if (hp.n >= 2 && hp.p[0] != 0)
+        for (int st : {3, 4}) {
+            tt_plan_options_t o = opt(TT_KERNEL_TILE, 0, 0, 0, 0, 0);
+            o.slot_dims = 1;
+            o.stages = st;
+            vars.push_back(o);
+        }
+
     std::vector<Plan*> cands{heur};
     std::vector<std::string> keys{describe_json(*heur)};
     for (const auto& o : vars) {

@@ -690,6 +690,99 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// ---------------------------------------------------------------------------
+// slot-dim map with a cp.async ring: same thread maps, tables and staging
+// layout as tile_sd_kernel, but the load phase copies global -> staging with
+// cp.async (no data registers), so S-1 tiles are in flight per CTA instead of
+// one tile's worth of registers (the loads-in-flight limit of 4-byte gathers,
+// profiles/worst_cases/README.md).  Interleaved schedule t0 + k*G as in
+// tile_sd_kernel; stage k % S holds tile k of this CTA.
+// ---------------------------------------------------------------------------
+template <typename W, int QM, int RM, int S>
+__global__ void __launch_bounds__(512, 2)
+tile_sd_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
+    const int tid = threadIdx.x;
+    const int NT = blockDim.x;
+    const int lane = tid & 31;
+
+    uint32_t gin[QM], gout[QM], smp[QM], cntL[QM], cntS[QM];
+#pragma unroll
+    for (int q = 0; q < QM; ++q) smp[q] = 0;
+    build_sd_phase<W, QM, RM>(p, 0, tid, NT, gin, smp, cntL);
+    build_sd_phase<W, QM, RM>(p, 1, tid, NT, gout, smp, cntS);
+    const int QL = p.sdQ[0], QS = p.sdQ[1];
+    const uint32_t sIn = (uint32_t)p.tSin[p.sdSlot[0]];
+    const uint32_t sOut = (uint32_t)p.tSout[p.sdSlot[1]];
+    const uint32_t mIn = (uint32_t)p.tSm[p.sdSlot[0]] * (uint32_t)sizeof(W);
+    const uint32_t mOut = (uint32_t)p.tSm[p.sdSlot[1]] * (uint32_t)sizeof(W);
+
+    const uint32_t nTiles = (uint32_t)p.nTiles;
+    const uint32_t G = (uint32_t)gridDim.x;
+    const uint32_t t0 = (uint32_t)blockIdx.x;
+    if (t0 >= nTiles) return;
+    GridWalker<uint32_t> walk(p, lane);
+
+    // load phase of tile t into the staging buffer at byte address sb
+    auto issue = [&](uint32_t t, uint32_t sb) {
+        const TileBase<uint32_t> tb = walk.seek(t);
+        const uint32_t sh = 8u * tb.need;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            if (q >= QL) break;
+            const uint32_t c = (cntL[q] >> sh) & 0xffu;
+            const W* src = in + tb.in + gin[q];
+            const uint32_t a0 = sb + (smp[q] & 0xffffu);
+#pragma unroll
+            for (int r = 0; r < RM; ++r)
+                if ((uint32_t)r < c) cp_async<sizeof(W)>(a0 + (uint32_t)r * mIn, elem_addr(src, (uint32_t)r * sIn));
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+        const uint32_t t = t0 + (uint32_t)s * G;
+        if (t < nTiles) issue(t, sm0 + (uint32_t)s * sbytes);
+        cp_async_commit();
+    }
+    uint32_t k = 0;
+    for (uint32_t t = t0; t < nTiles; t += G) {
+        cp_async_wait<S - 2>();
+        __syncthreads();
+        // refill the stage read in the previous iteration (all threads are
+        // past its reads: they passed this iteration's barrier)
+        {
+            const uint32_t tn = t + (uint32_t)(S - 1) * G;
+            const uint32_t kn = (k + S - 1) % S;
+            if (tn < nTiles) issue(tn, sm0 + kn * sbytes);
+            cp_async_commit();
+        }
+        const TileBase<uint32_t> now = walk.seek(t);
+        const uint32_t sb = sm0 + k * sbytes;
+        const uint32_t sh = 8u * now.need;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            if (q >= QS) break;
+            const uint32_t c = (cntS[q] >> sh) & 0xffu;
+            W* __restrict__ dst = opaque(out + now.out + gout[q]);
+            const uint32_t a0 = sb + (smp[q] >> 16);
+            if (c == (uint32_t)RM) {
+#pragma unroll
+                for (int r = 0; r < RM; ++r)
+                    stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+            } else {
+#pragma unroll
+                for (int r = 0; r < RM; ++r)
+                    if ((uint32_t)r < c)
+                        stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+            }
+        }
+        k = (k + 1 == (uint32_t)S) ? 0u : k + 1;
+    }
+    cp_async_wait<0>();
+}
+
 template <typename W, int NREG, typename I, int S>
 __global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, 2)
 tile_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
@@ -1121,8 +1214,20 @@ tiled2d_sa_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__
 // ---------------------------------------------------------------------------
 // slot-dim variant: (passes, slots) in {(1,16), (2,8), (4,4)}, 4/8-byte words,
 // 32-bit indices
-static const void* pick_tile_sd(int esize, int q, int r) {
+static const void* pick_tile_sd(int esize, int q, int r, int stages = 0) {
 #define TT_PICKSD(W)                                                                  \
+    if (stages == 3) {                                                                \
+        if (q == 1 && r == 16) return (const void*)&tile_sd_async_kernel<W, 1, 16, 3>; \
+        if (q == 2 && r == 8) return (const void*)&tile_sd_async_kernel<W, 2, 8, 3>;   \
+        if (q == 4 && r == 4) return (const void*)&tile_sd_async_kernel<W, 4, 4, 3>;   \
+        return nullptr;                                                               \
+    }                                                                                 \
+    if (stages == 4) {                                                                \
+        if (q == 1 && r == 16) return (const void*)&tile_sd_async_kernel<W, 1, 16, 4>; \
+        if (q == 2 && r == 8) return (const void*)&tile_sd_async_kernel<W, 2, 8, 4>;   \
+        if (q == 4 && r == 4) return (const void*)&tile_sd_async_kernel<W, 4, 4, 4>;   \
+        return nullptr;                                                               \
+    }                                                                                 \
     if (q == 1 && r == 16) return (const void*)&tile_sd_kernel<W, 1, 16>;           \
     if (q == 2 && r == 8) return (const void*)&tile_sd_kernel<W, 2, 8>;             \
     if (q == 4 && r == 4) return (const void*)&tile_sd_kernel<W, 4, 4>;             \
@@ -1294,7 +1399,7 @@ static cudaError_t ensure_max_smem(const void* fn) {
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
     const void* fn = q.kernel == TT_KERNEL_TILE
-                         ? (q.sdq ? pick_tile_sd(q.esize, q.sdq, q.sdr)
+                         ? (q.sdq ? pick_tile_sd(q.esize, q.sdq, q.sdr, q.vec >= 3 ? q.vec : 0)
                             : q.acc ? pick_tile_acc(q.esize, q.nreg)
                                       : (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
                                                     : pick_tile(q.esize, q.nreg, q.idx64)))
@@ -1359,7 +1464,7 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
         const void* fn = t2 ? (kc.vec == 1 && kc.stages >= 3 && !kc.idx64
                                    ? pick_tiled2d_async(E, kc.tile0, kc.tile1, kc.stages)
                                    : pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64))
-                            : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr)
+                            : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr, kc.stages)
                             : kc.acc ? pick_tile_acc(E, kc.nreg)
                                      : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
                                                        : pick_tile(E, kc.nreg, kc.idx64));

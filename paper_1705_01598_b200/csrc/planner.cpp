@@ -967,7 +967,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // opt-in); larger tiles than the classic map (16 elements x 512 / 384
     // threads, 16-bit staging offsets)
     const int sdOpt = opts ? opts->slot_dims : 0;
-    const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3) &&
+    const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3 && sdOpt <= 0) &&
                            (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                            !(opts && (opts->threads || opts->slots));
     // The slot-dim shape inside the tile model (TT_KNOB_SD_VMAX > 0, tiles up
@@ -1082,7 +1082,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     kc.nreg = best.nreg;
     // staging pipeline: register double buffer (default) or a cp.async ring
     // of 3 stages (32-bit indices only)
-    kc.stages = (opts && opts->stages >= 3 && !kc.idx64 && !acc && !best.sd) ? 3 : 0;
+    kc.stages = (opts && opts->stages >= 3 && opts->slot_dims <= 0 && !kc.idx64 && !acc && !best.sd) ? 3 : 0;
     // interleaved tiles (neighbouring tiles on concurrently running CTAs)
     // measured better than contiguous ranges on 72 of 84 suite cases
     plan.tile.interleave = (opts && opts->grid_order == 2) ? 0 : 1;
@@ -1130,6 +1130,26 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
             kc.sdr = sr;
             kc.threads = thr;
             const int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : perSd;
+            kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
+        }
+    }
+    // slot-dim map with a cp.async ring of S stages (tile_sd_async_kernel):
+    // S-1 tiles in flight per CTA without data registers.  Experimental,
+    // options slot_dims > 0 with stages 3 or 4 (measured planning), or
+    // TT_KNOB_SD_STAGES; off by default (suites: mixed, up to 1.18x faster
+    // and 1.3x slower case by case, profiles/round1_ab_sd_async.txt).
+    if (kc.sdq && !acc && !kc.idx64) {
+        const int S = (opts && opts->slot_dims > 0 && opts->stages >= 3) ? opts->stages
+                                                                          : (int)knob("TT_KNOB_SD_STAGES", 0);
+        if ((S == 3 || S == 4) && (int64_t)S * plan.tile.sbuf * E <= dev.max_smem_per_block) {
+            kc.stages = S;
+            kc.smem = S * plan.tile.sbuf * E;
+            OccQuery qa{TT_KERNEL_TILE, E, kc.sdq * kc.sdr, S, kc.threads, kc.smem, false, 0, 0, 0, kc.sdq, kc.sdr};
+            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qa, dev) : 0);
+            if (per <= 0)
+                per = std::max(1, std::min({dev.max_smem_per_sm / (kc.smem + 1024),
+                                            dev.max_threads_per_sm / kc.threads,
+                                            dev.regs_per_sm / (kc.threads * 64)}));
             kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
         }
     }

@@ -240,6 +240,26 @@ def test_slot_dim_map(esize):
     assert used >= 8
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("stages", [3, 4])
+def test_slot_dim_async_ring(esize, stages):
+    """The slot-dim map with a cp.async ring (tile_sd_async_kernel): ragged
+    split chunks, small extents, more tiles than CTAs (ring wrap-around) and
+    fewer tiles than stages."""
+    shapes = RANDOM_SHAPES[:11] + [((37, 29, 11), (2, 0, 1)), ((5, 3, 2, 4, 35, 33), (5, 4, 3, 2, 1, 0)),
+                                   ((46, 46, 46, 7), (3, 1, 0, 2)), ((3, 5, 7, 11, 13, 2), (4, 2, 0, 5, 3, 1)),
+                                   ((5, 5, 5, 5, 5, 5, 5, 5), (0, 6, 3, 7, 1, 4, 2, 5)), ((6, 7), (1, 0))]
+    used = 0
+    for dims, perm in shapes:
+        vol = int(np.prod(dims))
+        if vol > 2_000_000:
+            dims = wl.scaled(wl.Case("x", dims, perm, esize, 3), 1_000_000).dims
+        j = tt.Plan(dims, perm, esize, slot_dims=1, stages=stages, no_widen=True).describe()
+        used += "sd" in j.get("tile", {}) and j["stages"] == stages
+        check(dims, perm, esize, slot_dims=1, stages=stages, no_widen=True)
+    assert used >= 8
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)
