@@ -141,6 +141,31 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
+    // 8-byte elements on the generic tile: the slot-dim map with a 4-stage
+    // cp.async ring (tile_sd_async_kernel) when that plan runs at one CTA per
+    // SM.  Same-box A/B over the suites' fp64 generic-tile cases
+    // (profiles/round1_ab_sd_async8.txt): 18 of 20 such cases faster, median
+    // 1.10x, none slower; at 2+ CTAs per SM it was a wash.  Planner-chosen
+    // plans only (no options); TT_KNOB_SD_RING8=0 turns it off.
+    static const tt_plan_options_t zero{};
+    const bool noOpts = opts == nullptr || std::memcmp(opts, &zero, sizeof(zero)) == 0;
+    const char* kv = std::getenv("TT_KNOB_SD_RING8");
+    if (noOpts && !(kv && *kv && std::atoi(kv) == 0) && elem_size == 8 && p->widen == 1 &&
+        p->kc.kernel == TT_KERNEL_TILE && !p->kc.idx64) {
+        Plan alt;
+        alt.device = p->device;
+        alt.stream = p->stream;
+        alt.rank = rank;
+        alt.prob = p->prob;
+        tt_plan_options_t o{};
+        o.slot_dims = 1;
+        o.stages = 4;
+        if (choose_plan(alt, dev, &o, occ) == TT_SUCCESS && alt.kc.kernel == TT_KERNEL_TILE &&
+            alt.kc.sdq && alt.kc.stages == 4 && alt.kc.grid <= dev.num_sms) {
+            p->tile = alt.tile;
+            p->kc = alt.kc;
+        }
+    }
     *out = p;
     return TT_SUCCESS;
 }

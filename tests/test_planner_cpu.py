@@ -251,17 +251,19 @@ def test_slot_dim_plans_match_oracle(dims, perm, esize):
 
 def test_slot_dim_map_used_on_suites():
     """The slot-dim map is the default for most 4-byte generic-tile plans of
-    the random suite (offline occupancy estimate), and opt-in for 8-byte
-    elements (8-byte words widened from 4-byte elements do use it)."""
+    the random suite (offline occupancy estimate); 8-byte elements use it
+    only with the 4-stage cp.async ring at one CTA per SM."""
     n = sd = sd8 = 0
     for c in wl.s3_random(per_cell=1):
         j = tt.plan_offline(c.dims, c.perm, c.esize)
         if j["kernel"] == "tile" and j["word_size"] == 4:
             n += 1
             sd += "sd" in j["tile"]
-        if j["kernel"] == "tile" and c.esize == 8:   # fp64 words: opt-in only
-            sd8 += "sd" in j["tile"]
-    assert n > 20 and sd >= n // 2 and sd8 == 0
+        if j["kernel"] == "tile" and c.esize == 8 and "sd" in j["tile"]:
+            # fp64 words: only the 4-stage cp.async ring at one CTA per SM
+            assert j["stages"] == 4 and j["grid"] <= 148
+            sd8 += 1
+    assert n > 20 and sd >= n // 2 and sd8 > 0
 
 
 def strided_layout(rng, dims, perm):
