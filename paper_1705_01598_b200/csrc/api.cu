@@ -150,7 +150,13 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     static const tt_plan_options_t zero{};
     const bool noOpts = opts == nullptr || std::memcmp(opts, &zero, sizeof(zero)) == 0;
     const char* kv = std::getenv("TT_KNOB_SD_RING8");
-    if (noOpts && !(kv && *kv && std::atoi(kv) == 0) && elem_size == 8 && p->widen == 1 &&
+    // also 8-byte words widened from 4-byte elements (A/B: 5 of 5 faster,
+    // 0.93-0.99x time, profiles/round1_ab_sd_async8.txt); TT_KNOB_SD_RING8W=0
+    // keeps those on the register pipeline
+    const char* kw = std::getenv("TT_KNOB_SD_RING8W");
+    const bool word8 = elem_size == 8 ? p->widen == 1
+                                      : (!(kw && *kw && std::atoi(kw) == 0) && p->prob.esize == 8);
+    if (noOpts && !(kv && *kv && std::atoi(kv) == 0) && word8 &&
         p->kc.kernel == TT_KERNEL_TILE && !p->kc.idx64) {
         Plan alt;
         alt.device = p->device;

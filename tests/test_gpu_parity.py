@@ -471,3 +471,17 @@ def test_classification_threshold_shapes(case):
     assert plan.describe()["kernel"] == kernel
     plan.destroy()
     check(dims, perm, esize, seed=case)
+
+
+@pytest.mark.parametrize("dims,perm,esize", [((597, 41, 85), (2, 1, 0), 8), ((45, 45, 45, 45), (0, 3, 2, 1), 8),
+                                             ((5, 29, 7, 31, 81), (4, 0, 3, 1, 2), 8),
+                                             ((11, 11, 11, 11, 11, 11), (2, 1, 5, 0, 4, 3), 8),
+                                             ((2, 37, 13, 11, 11, 15), (0, 3, 2, 1, 4, 5), 4)])
+def test_default_cp_async_slot_dim_plans(dims, perm, esize):
+    """Planner-chosen plans of 8-byte words that take the slot-dim map with the
+    4-stage cp.async ring at one CTA per SM (api.cu create_plan_w), bit-exact;
+    at least the fp64 ones take it on the B200."""
+    j = tt.Plan(dims, perm, esize).describe()
+    if esize == 8:
+        assert j["kernel"] == "tile" and j["stages"] == 4 and "sd" in j["tile"]
+    check(dims, perm, esize, seed=5)
