@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <vector>
 
 #include "tt_internal.h"
 
@@ -227,8 +228,7 @@ static double knob(const char* name, double dflt) {
 // overflow for n < 2^31.
 void magic_u31(uint32_t d, uint32_t& m, uint32_t& l) {
     if (d == 0) d = 1;
-    l = 0;
-    while ((uint64_t(1) << l) < d) ++l;
+    l = d <= 1 ? 0u : (uint32_t)(32 - __builtin_clz(d - 1));  // ceil(log2 d)
     m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
 }
 
@@ -276,36 +276,26 @@ struct TileCand {
 };
 
 // Shared-memory wavefronts for one warp access of element positions pos[32].
+// The staging layout is injective (padded strides >= dense ones), so the
+// lanes of one access touch distinct positions: the wavefront count is the
+// largest number of lanes on one bank (4-byte words), or on one bank pair
+// per half-warp phase (8-byte words; 16-byte words use the same half-warp
+// model, as the padding search was calibrated with it).
 static int warp_wavefronts(const int* pos, int nlanes, int esize) {
     if (nlanes <= 0) return 0;
     if (esize == 4) {
+        int cnt[32] = {};
         int worst = 0;
-        for (int b = 0; b < 32; ++b) {
-            int distinct[32], nd = 0;
-            for (int l = 0; l < nlanes; ++l) {
-                if ((pos[l] & 31) != b) continue;
-                bool dup = false;
-                for (int q = 0; q < nd; ++q) dup |= distinct[q] == pos[l];
-                if (!dup) distinct[nd++] = pos[l];
-            }
-            worst = std::max(worst, nd);
-        }
+        for (int l = 0; l < nlanes; ++l) worst = std::max(worst, ++cnt[pos[l] & 31]);
         return worst;
     }
-    // 8-byte elements: two half-warp phases, 16 bank pairs each
+    const int per = 16, banks = 16;        // half-warp phases, bank pairs
     int total = 0;
-    for (int half = 0; half < 2; ++half) {
+    for (int ph = 0; ph * per < nlanes; ++ph) {
+        int cnt[32] = {};
         int worst = 0;
-        for (int b = 0; b < 16; ++b) {
-            int distinct[16], nd = 0;
-            for (int l = half * 16; l < std::min(nlanes, half * 16 + 16); ++l) {
-                if ((pos[l] & 15) != b) continue;
-                bool dup = false;
-                for (int q = 0; q < nd; ++q) dup |= distinct[q] == pos[l];
-                if (!dup) distinct[nd++] = pos[l];
-            }
-            worst = std::max(worst, nd);
-        }
+        for (int l = ph * per; l < std::min(nlanes, ph * per + per); ++l)
+            worst = std::max(worst, ++cnt[pos[l] & (banks - 1)]);
         total += worst;
     }
     return total;
@@ -315,33 +305,73 @@ static int warp_wavefronts(const int* pos, int nlanes, int esize) {
 // at runtime using the element positions given by Equation (6)"),
 // for both the staging store (input order) and the transposed read (output
 // order), on a sample of warps (cf. the 10 samples of P:L244).  Element
-// (c_i) sits at sum_i c_i * sm[i].
-static long smem_cost(const TileParams& tp, int esize, const int32_t* sm) {
+// (c_i) sits at sum_i c_i * sm[i].  The sampled lanes' tile coordinates do
+// not depend on the layout, so they are decoded once (SmemSample) and every
+// candidate layout costs one dot product per lane.
+struct SmemSample {
+    int a = 0, nacc = 0;
+    std::vector<int> nl;     // lanes per distinct access pattern
+    std::vector<int> wt;     // sampled accesses with that pattern
+    std::vector<int> coord;  // [pattern][lane][tile dim], relative to lane 0
+};
+
+// Adding the same offset to every lane's position permutes the banks, so an
+// access's wavefront count depends only on the lanes' coordinates relative to
+// lane 0: sampled accesses with equal relative patterns are merged (weighted).
+static SmemSample smem_sample(const TileParams& tp) {
+    SmemSample s;
+    s.a = tp.a;
     const int V = tp.V;
     const int nw = (V + 31) / 32;
     const int step = std::max(1, nw / 8);
-    long cost = 0;
-    int pos[32];
+    std::vector<int> cur(32 * tp.a);
     for (int w = 0; w < nw; w += step) {
         const int nl = std::min(32, V - w * 32);
-        // staging store: consecutive k in input order
-        for (int l = 0; l < nl; ++l) {
-            int kk = w * 32 + l, sp = 0;
-            for (int i = 0; i < tp.a; ++i) { sp += (kk % tp.tExt[i]) * sm[i]; kk /= tp.tExt[i]; }
-            pos[l] = sp;
-        }
-        cost += warp_wavefronts(pos, nl, esize);
-        // transposed read: consecutive k' in output order
-        for (int l = 0; l < nl; ++l) {
-            int kk = w * 32 + l, sp = 0;
-            for (int jj = 0; jj < tp.a; ++jj) {
-                const int t = tp.tOutOrder[jj];
-                sp += (kk % tp.tExt[t]) * sm[t];
-                kk /= tp.tExt[t];
+        for (int side = 0; side < 2; ++side) {  // 0: staging store (input order), 1: transposed read
+            int c0[kMaxDims] = {};
+            for (int l = 0; l < 32; ++l) {
+                int kk = w * 32 + l;
+                int c[kMaxDims] = {};
+                for (int jj = 0; jj < tp.a && l < nl; ++jj) {
+                    const int t = side == 0 ? jj : tp.tOutOrder[jj];
+                    c[t] = kk % tp.tExt[t];
+                    kk /= tp.tExt[t];
+                }
+                if (l == 0)
+                    for (int i = 0; i < tp.a; ++i) c0[i] = c[i];
+                for (int i = 0; i < tp.a; ++i) cur[l * tp.a + i] = l < nl ? c[i] - c0[i] : 0;
             }
-            pos[l] = sp;
+            bool merged = false;
+            for (int q = 0; q < s.nacc && !merged; ++q) {
+                if (s.nl[q] != nl) continue;
+                if (std::equal(cur.begin(), cur.end(), s.coord.begin() + (size_t)q * 32 * tp.a)) {
+                    ++s.wt[q];
+                    merged = true;
+                }
+            }
+            if (!merged) {
+                s.nl.push_back(nl);
+                s.wt.push_back(1);
+                s.coord.insert(s.coord.end(), cur.begin(), cur.end());
+                ++s.nacc;
+            }
         }
-        cost += warp_wavefronts(pos, nl, esize);
+    }
+    return s;
+}
+
+static long smem_cost(const SmemSample& s, int esize, const int32_t* sm, long bound = -1) {
+    long cost = 0;
+    int pos[32];
+    const int* c = s.coord.data();
+    for (int q = 0; q < s.nacc; ++q) {
+        if (bound >= 0 && cost >= bound) return cost;  // already no better than the incumbent
+        for (int l = 0; l < 32; ++l, c += s.a) {
+            int sp = 0;
+            for (int i = 0; i < s.a; ++i) sp += c[i] * sm[i];
+            pos[l] = sp + 4096;  // relative positions may be negative: keep the low bits' meaning
+        }
+        cost += (long)s.wt[q] * warp_wavefronts(pos, s.nl[q], esize);
     }
     return cost;
 }
@@ -365,12 +395,13 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
             const int64_t stride = ph == 0 ? tp.tSin[t] : tp.tSout[t];
             const int64_t before = ph == 0 ? tp.tCin[t] : tp.tCout[t];
             if (stride < (ph == 0 ? runIn : runOut) && before < 32) continue;
+            // slot fill ext / (C * RM) with C = ceil(ext / R) chunks: the
+            // largest R (fewest chunks) is best, smaller R never beats it
             const int ext = tp.tExt[t];
-            for (int R = std::min(RM, ext); R >= 1; --R) {
-                const int C = (ext + R - 1) / R;
-                const double eff = (double)ext / ((double)C * R) * ((double)R / RM);
-                if (eff > best.eff + 1e-9) { best.slot = t; best.R = R; best.C = C; best.eff = eff; }
-            }
+            const int R = std::min(RM, ext);
+            const int C = (ext + R - 1) / R;
+            const double eff = (double)ext / ((double)C * RM);
+            if (eff > best.eff + 1e-9) { best.slot = t; best.R = R; best.C = C; best.eff = eff; }
         }
         return best;
     };
@@ -414,15 +445,14 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
     return true;
 }
 
-// Build the tile of candidate run targets (Tin, Tout) in elements.
-static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
-                           const DeviceInfo& dev, int forceThreads, int maxR = 16, int forceR = 0,
-                           int VmaxSd = 0) {
-    TileCand c;
+// Tile extents for candidate run targets (Tin, Tout) in elements: need[i]
+// elements of input dim i (1 = a grid dim), and the split dim of each side.
+static void tile_need(const Problem& pr, int64_t Tin, int64_t Tout, int64_t* need, int& inSplit,
+                      int& outSplit) {
     const int n = pr.n;
-    int64_t need[kMaxDims];
     for (int i = 0; i < n; ++i) need[i] = 1;
-    int inSplit = -1, outSplit = -1;
+    inSplit = -1;
+    outSplit = -1;
     // input side: M_m = first input dims, last one possibly split
     {
         int64_t P = 1;
@@ -465,6 +495,14 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
             }
         }
     }
+}
+
+// Build the tile with extents need[] (from tile_need).
+static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSplit, int outSplit,
+                                int Vmax, const DeviceInfo& dev, int forceThreads, int maxR,
+                                int forceR, int VmaxSd) {
+    TileCand c;
+    const int n = pr.n;
     long double V = 1;
     for (int i = 0; i < n; ++i) V *= (long double)need[i];
     if (V > std::max(Vmax, VmaxSd)) return c;
@@ -665,6 +703,41 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
     return c;
 }
 
+// Build the tile of candidate run targets (Tin, Tout) in elements.
+static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax,
+                           const DeviceInfo& dev, int forceThreads, int maxR = 16, int forceR = 0,
+                           int VmaxSd = 0) {
+    int64_t need[kMaxDims];
+    int inSplit, outSplit;
+    tile_need(pr, Tin, Tout, need, inSplit, outSplit);
+    return build_tile_need(pr, need, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd);
+}
+
+// Many run-target pairs give the same tile (a dim is taken whole from one
+// target up): the searches of choose_plan evaluate each distinct tile once.
+struct TileMemo {
+    struct Entry {
+        int64_t key[kMaxDims + 3];
+        TileCand c;
+    };
+    std::vector<Entry> e;
+    const TileCand& get(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax, const DeviceInfo& dev,
+                        int forceThreads, int maxR, int forceR, int VmaxSd) {
+        Entry x;
+        int inSplit, outSplit;
+        tile_need(pr, Tin, Tout, x.key, inSplit, outSplit);
+        x.key[pr.n] = Vmax;
+        x.key[pr.n + 1] = VmaxSd;
+        x.key[pr.n + 2] = (int64_t)(inSplit + 1) * 64 + (outSplit + 1);
+        const size_t kb = sizeof(int64_t) * (pr.n + 3);
+        for (const Entry& y : e)
+            if (std::memcmp(x.key, y.key, kb) == 0) return y.c;
+        x.c = build_tile_need(pr, x.key, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd);
+        e.push_back(x);
+        return e.back().c;
+    }
+};
+
 // Shared-memory layout: per-dimension padded strides sm[i] = sm[i-1]*ext[i-1]
 // + pad[i] (the L x (L+1) padding of P:L123 generalised to every level of
 // the tile), chosen by coordinate descent on the conflict model, then by
@@ -687,7 +760,8 @@ static void choose_smem(TileParams& tp, int esize) {
     };
     const int64_t limit = std::min<int64_t>((65536 / esize) - 8, tp.V + tp.V / 4 + 64);
     strides(pad, sm);
-    long best = smem_cost(tp, esize, sm);
+    const SmemSample sample = smem_sample(tp);
+    long best = smem_cost(sample, esize, sm);
     const int ideal_per_warp = esize == 4 ? 2 : esize == 8 ? 4 : 8;  // store + read
     const int nw = (tp.V + 31) / 32;
     const long ideal = (long)((nw + std::max(1, nw / 8) - 1) / std::max(1, nw / 8)) * ideal_per_warp;
@@ -699,7 +773,7 @@ static void choose_smem(TileParams& tp, int esize) {
                 pad[i] = c;
                 const int64_t foot = strides(pad, sm);
                 if (foot > limit) continue;
-                const long cst = smem_cost(tp, esize, sm);
+                const long cst = smem_cost(sample, esize, sm, best);
                 if (cst < best) { best = cst; bestPad = c; }
             }
             pad[i] = bestPad;
@@ -1016,13 +1090,15 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     TileCand best;
     const int forceThreads = opts ? opts->threads : 0;
     const int forceR = opts ? opts->slots : 0;
+    TileMemo memo;
+    memo.e.reserve(256);
     auto search = [&](const std::vector<int64_t>& tin, const std::vector<int64_t>& tout, TileCand& b) {
         for (int64_t ti : tin) {
             for (int64_t to : tout) {
                 int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
                 int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-                TileCand c = build_tile(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                        VmaxSd);
+                const TileCand& c = memo.get(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                             VmaxSd);
                 if (!c.ok) continue;
                 if (!b.ok || c.cost_us < b.cost_us) b = c;
             }
@@ -1057,8 +1133,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         TileCand sx;
         for (int64_t ti : all)
             for (int64_t to : all) {
-                TileCand c = build_tile(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                        VmaxSdRule);
+                const TileCand& c = memo.get(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                             VmaxSdRule);
                 if (c.ok && (!sx.ok || c.cost_us < sx.cost_us)) sx = c;
             }
         const bool keepsOut = sx.ok && sx.runOut >= best.runOut &&
