@@ -10,7 +10,7 @@ NCCL_DIR  := $(shell $(PYTHON) -c "import nvidia.nccl; print(list(nvidia.nccl.__
 SRCS_CU   := $(wildcard $(CSRC)/*.cu)
 SRCS_CPP  := $(wildcard $(CSRC)/*.cpp)
 OBJS      := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(SRCS_CU)) $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(SRCS_CPP))
-HDRS      := $(wildcard $(CSRC)/*.h) include/tt.h
+HDRS      := $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh) include/tt.h
 NCCL_INC  := $(if $(NCCL_DIR),-I$(NCCL_DIR)/include,)
 NCCL_LNK  := $(if $(NCCL_DIR),-L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib,)
 CUDA_LIB  := /usr/local/cuda/lib64
