@@ -2,25 +2,49 @@
 """Benchmark of the B200 tensor-permutation hot path (arXiv 1705.01598, cuTT).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config s1|s2|s5local|s5redist]
+                    [--config s1|s2|s5local|s5batch|s5redist|s5p2p]
+                    [--suites default|full|none] [--verify full|none]
 
 One step = one pass of the whole hot path (plan already built: one
-tt_execute) over one tensor.  The default workload is BASELINE.json
-configs[1] (16384x16384 fp32, perm (1,0)); the metric is the paper's
-bandwidth 2*vol*E/D in GB/s (10^9), whole job.  At N > 1 every rank
-permutes its own tensor (independent units, weak scaling, no collective);
-``--config s5redist`` times the sharded NCCL redistribution instead.
+tt_execute, or one tt_execute_sharded) over one tensor.  The default workload
+is BASELINE.json configs[1] (16384x16384 fp32, perm (1,0)); the metric is the
+paper's bandwidth 2*vol*E/D in GB/s (10^9), whole job.
+
+Inputs are the seeded words of tt_workloads (host), uploaded to HBM before
+the timed region; after it the timed output is copied back and compared with
+the CPU oracle element by element (memcmp; "verified" in the JSON line).
+
+Multi-GPU (one process per GPU; `--gpus N` outside torchrun spawns its own N
+ranks through torch.distributed.run):
+  s1        every rank permutes its own tensor (independent units, weak scaling)
+  s5local   BASELINE configs[4], local case: the global tensor block-sharded
+            along its outermost dim, a 1/N slab per rank (strong scaling)
+  s5batch   8 independent S5 tensors, 8/N per rank (strong scaling)
+  s5redist  redistribution case: pack -> ncclAlltoAll -> unpack, with the
+            pack / all-to-all / unpack split and the NVLink fraction
+  s5p2p     the fused NVLink-P2P redistribution (f-1)
+
+At N = 1 the JSON line also carries `suites`: the rank 2-12 suites of
+BASELINE.json configs[2-3] (a fixed seeded set; `--suites full` = every case
+of S2 / S3 / Set 2 / S4), each case verified in full against the oracle,
+reported as worst / median / best fraction of a same-bytes device copy
+(P:L281), per-rank medians and plan time.
 
 ``--impl reference`` times the CPU oracle (oracle/) on the same workload
 (bounded sample per step) -- the deliberately slow baseline, not a target.
+``--dry-run`` runs the multi-process plumbing (spawn, gloo process group,
+offline sharded plans, max-over-ranks timing) without a GPU, for CPU tests.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
-import math
 import os
+import queue
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,19 +58,26 @@ import tt_workloads as wl  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 DTYPE_NAME = {4: "u32", 8: "u64"}
+NVLINK_GBS = 900.0        # NVLink 5 per direction per GPU (nominal)
+NVLINK_MEASURED = 770.0   # B200_PROFILING.md: measured peer copy per direction
+CONFIGS = ["s1", "s2", "s5local", "s5batch", "s5redist", "s5p2p"]
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="s1", choices=["s1", "s2", "s5local", "s5redist", "s5p2p"])
+    ap.add_argument("--config", default="s1", choices=CONFIGS)
+    ap.add_argument("--suites", default="default", choices=["default", "full", "none"])
+    ap.add_argument("--suites-out", default="", help="per-case JSONL of the suites")
+    ap.add_argument("--verify", default="full", choices=["full", "none"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true")
+    return ap.parse_args(argv)
 
 
 def workload(name: str):
@@ -56,8 +87,12 @@ def workload(name: str):
     if name == "s2":
         c = wl.s2_ttc()[30]
         return c, f"S2 TTC-style rank-{c.rank} fp64 case {c.name} dims {c.dims} perm {c.perm}"
-    if name in ("s5local", "s5redist", "s5p2p"):
-        c = wl.s5_sharded()[0 if name == "s5local" else 5]
+    if name in ("s5local", "s5batch"):
+        c = wl.s5_sharded()[0]
+        return c, (f"S5 {name[2:]} 112x112x112x104 fp64 perm {c.perm} (BASELINE.json configs[4])"
+                   + (", 8 independent tensors" if name == "s5batch" else ""))
+    if name in ("s5redist", "s5p2p"):
+        c = wl.s5_sharded()[5]
         return c, f"S5 {name[2:]} 112x112x112x104 fp64 perm {c.perm} (BASELINE.json configs[4])"
     raise ValueError(name)
 
@@ -71,6 +106,21 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args, argv) -> int:
+    """`--gpus N` outside torchrun: relaunch this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 class ClockSampler:
@@ -148,26 +198,31 @@ def traffic_from_profiles(kernel_key: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle baseline (the only bench leg that executes oracle/)
+# Verification leg: the timed output against the CPU oracle, in full.
+# (Test infrastructure inside the bench: never on the product path.)
 # ---------------------------------------------------------------------------
 
-def oracle_sample_time(case, words, budget_s: float, threads: int):
-    """Time the oracle on output ranges until ~budget_s of CPU work; returns
-    (GB/s, elements, seconds, description)."""
-    from oracle import oracle as orc
-    out = np.empty(case.vol, dtype=words.dtype)
-    # probe the rate on a small range, then size the sample
-    probe = min(case.vol, 1 << 20)
-    t0 = time.perf_counter()
-    _oracle_range_threaded(orc, case, words, out, 0, probe, threads)
-    dt = max(1e-6, time.perf_counter() - t0)
-    n = int(min(case.vol, max(probe, probe * budget_s / dt)))
-    t0 = time.perf_counter()
-    _oracle_range_threaded(orc, case, words, out, 0, n, threads)
-    dt = time.perf_counter() - t0
-    gbs = 2.0 * n * case.esize / dt / 1e9
-    return gbs, n, dt
+_libc = ctypes.CDLL(None)
+_libc.memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+_libc.memcmp.restype = ctypes.c_int
 
+
+def memcmp_equal(a: np.ndarray, b: np.ndarray) -> bool:
+    if a.nbytes != b.nbytes:
+        return False
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return _libc.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0
+
+
+def oracle_expected(case, words, threads=None):
+    from oracle import oracle as orc
+    return orc.permute_threaded(case.dims, case.perm, words, threads=threads)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample)
+# ---------------------------------------------------------------------------
 
 def _oracle_range_threaded(orc, case, words, out, begin, end, threads):
     bounds = [begin + (end - begin) * t // threads for t in range(threads + 1)]
@@ -180,6 +235,35 @@ def _oracle_range_threaded(orc, case, words, out, begin, end, threads):
         t.join()
 
 
+def oracle_sample_time(case, words, budget_s: float, threads: int):
+    """Time the oracle on output ranges until ~budget_s of CPU work; returns
+    (GB/s, elements, seconds)."""
+    from oracle import oracle as orc
+    out = np.empty(case.vol, dtype=words.dtype)
+    probe = min(case.vol, 1 << 20)
+    t0 = time.perf_counter()
+    _oracle_range_threaded(orc, case, words, out, 0, probe, threads)
+    dt = max(1e-6, time.perf_counter() - t0)
+    n = int(min(case.vol, max(probe, probe * budget_s / dt)))
+    t0 = time.perf_counter()
+    _oracle_range_threaded(orc, case, words, out, 0, n, threads)
+    dt = time.perf_counter() - t0
+    return 2.0 * n * case.esize / dt / 1e9, n, dt
+
+
+def cpu_baseline(case, words):
+    """The oracle on all host threads (bounded sample) and on one thread
+    (smaller sample), as it stands."""
+    threads = len(os.sched_getaffinity(0))
+    gbs, n, dt = oracle_sample_time(case, words, 10.0, threads)
+    g1, n1, d1 = oracle_sample_time(case, words, 4.0, 1)
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"output elements [0, {n}) of {case.vol} ({dt:.1f} s, {threads} threads, "
+                      f"C gather odometer)",
+            "single_thread": {"value": round(g1, 3), "unit": "GB/s", "cores": 1,
+                              "sample": f"output elements [0, {n1}) ({d1:.1f} s, 1 thread)"}}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -189,7 +273,7 @@ def run_reference(args):
     words = case.words()
     from oracle import oracle as orc
     out = np.empty(case.vol, dtype=words.dtype)
-    # size one step as a bounded sample: ~ (budget / steps) seconds of CPU work
+    # one step = a bounded sample: ~ (budget / steps) seconds of CPU work
     probe = min(case.vol, 1 << 20)
     t0 = time.perf_counter()
     _oracle_range_threaded(orc, case, words, out, 0, probe, threads)
@@ -212,8 +296,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE_NAME[case.esize], "data": "synthetic",
-        "config": {"workload": desc, "dims": list(case.dims), "perm": list(case.perm),
-                   "elem_bytes": case.esize, "parallelism": "host threads"},
+        "config": config_dict(args, case, desc, args.gpus, sharded=False),
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads,
                          "kind": "oracle", "sample": sample},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -224,9 +307,182 @@ def run_reference(args):
     return 0
 
 
+def config_dict(args, case, desc, world, sharded, plan_desc=None):
+    c = {"workload": desc, "dims": list(case.dims), "perm": list(case.perm), "elem_bytes": case.esize,
+         "global_batch": (8 if args.config == "s5batch" else (1 if sharded else world)),
+         "parallelism": {"s1": "independent tensor per GPU" if world > 1 else "single GPU",
+                         "s2": "independent tensor per GPU" if world > 1 else "single GPU",
+                         "s5local": f"sharded along the outermost dim, 1/{world} slab per GPU",
+                         "s5batch": f"8 independent tensors, {8 // max(1, world)} per GPU",
+                         "s5redist": "sharded, pack -> ncclAlltoAll -> unpack",
+                         "s5p2p": "sharded, fused NVLink-P2P redistribution"}[args.config],
+         "l2": "inputs larger than L2 (126 MB); no flush"}
+    if plan_desc:
+        c["plan"] = {k: plan_desc.get(k) for k in ("kernel", "threads", "grid", "smem", "nreg", "stages")}
+        c["tile"] = {k: plan_desc.get("tile", {}).get(k) for k in ("ext", "V", "sm")}
+    return c
+
+
+# ---------------------------------------------------------------------------
+# suites (rank 2-12, BASELINE.json configs[2-3]), N = 1
+# ---------------------------------------------------------------------------
+
+def suite_cases(which: str):
+    if which == "full":
+        s2 = wl.s2_ttc()
+        s3 = [c for c in wl.s3_random(per_cell=20, set2_random=0) if c.tags[0] == "S3"]
+        st = [c for c in wl.s3_random(per_cell=0, set2_random=50) if c.tags[0] == "SET2"]
+    else:
+        s2 = wl.s2_ttc()
+        s3 = [c for c in wl.s3_random(per_cell=2, set2_random=0) if c.tags[0] == "S3"]
+        st = [c for c in wl.s3_random(per_cell=0, set2_random=10) if c.tags[0] == "SET2"]
+    return {"S2": s2, "S3": s3, "SET2": st, "S4": wl.s4_alignment()}
+
+
+def _event_median(fn, reps, stream):
+    import torch
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def run_suites(tt, dev, which, reps, out_path=""):
+    """Every case: seeded words uploaded to HBM, plan time, median of `reps`
+    event-timed executes, same-bytes device copy, full memcmp against the
+    oracle.  Words and oracle output of the next cases are prepared on host
+    threads while the GPU works."""
+    import torch
+    groups = suite_cases(which)
+    cases = [(g, c) for g, cs in groups.items() for c in cs]
+    q: "queue.Queue" = queue.Queue(maxsize=2)
+
+    def producer():
+        for g, c in cases:
+            w = c.words()
+            q.put((g, c, w, oracle_expected(c, w)))
+        q.put(None)
+
+    th = threading.Thread(target=producer, daemon=True)
+    t_start = time.perf_counter()
+    th.start()
+    stream = torch.cuda.Stream(device=dev)
+    memcpy_ms = {}
+    rows = []
+    fout = open(out_path, "w") if out_path else None
+    while True:
+        item = q.get()
+        if item is None:
+            break
+        g, c, words, want = item
+        nd = np.int32 if c.esize == 4 else np.int64
+        x = torch.from_numpy(words.view(nd)).to(dev)
+        y = torch.empty_like(x)
+        t0 = time.perf_counter()
+        plan = tt.Plan(c.dims, c.perm, c.esize, stream=stream)
+        plan_first = (time.perf_counter() - t0) * 1e6
+        warm = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            p2 = tt.Plan(c.dims, c.perm, c.esize, stream=stream)
+            warm.append((time.perf_counter() - t0) * 1e6)
+            p2.destroy()
+        with torch.cuda.stream(stream):
+            ms = _event_median(lambda: plan.execute(x, y), reps, stream)
+            if c.nbytes not in memcpy_ms:
+                z = torch.empty_like(x)
+                memcpy_ms[c.nbytes] = _event_median(lambda: z.copy_(x), reps, stream)
+                del z
+        stream.synchronize()
+        got = y.cpu().numpy().view(words.dtype)
+        ok = memcmp_equal(got, want)
+        d = plan.describe()
+        plan.destroy()
+        r = {"suite": g, "case": c.name, "rank": c.rank, "esize": c.esize, "dims": list(c.dims),
+             "perm": list(c.perm), "kernel": d["kernel"], "vg": "vg" in d.get("tile", {}),
+             "sd": "sd" in d.get("tile", {}), "ms": round(ms, 5),
+             "gbs": round(2 * c.nbytes / ms / 1e6, 1), "frac_memcpy": round(memcpy_ms[c.nbytes] / ms, 4),
+             "plan_us": round(statistics.median(warm), 1), "plan_us_first": round(plan_first, 1),
+             "verified": ok, "elements": c.vol}
+        rows.append(r)
+        if fout:
+            fout.write(json.dumps(r) + "\n")
+            fout.flush()
+        del x, y, got, want, words
+        torch.cuda.empty_cache()
+    th.join()
+    if fout:
+        fout.close()
+    out = {}
+    for g in groups:
+        rs = [r for r in rows if r["suite"] == g]
+        if not rs:
+            continue
+        f = sorted(r["frac_memcpy"] for r in rs)
+        gb = sorted(r["gbs"] for r in rs)
+        per_rank = {}
+        for r in rs:
+            per_rank.setdefault(r["rank"], []).append(r["frac_memcpy"])
+        med = {str(k): round(statistics.median(v), 4) for k, v in sorted(per_rank.items())}
+        pu = sorted(r["plan_us"] for r in rs)
+        out[g] = {"n": len(rs), "worst_frac": f[0], "median_frac": round(statistics.median(f), 4),
+                  "best_frac": f[-1], "worst_gbs": gb[0], "median_gbs": statistics.median(gb),
+                  "best_gbs": gb[-1], "per_rank_median_frac": med,
+                  "rank_max_over_min": round(max(med.values()) / max(1e-9, min(med.values())), 3),
+                  "plan_us_median": statistics.median(pu), "plan_us_max": pu[-1],
+                  "verified": f"{sum(r['verified'] for r in rs)}/{len(rs)} cases, full memcmp vs oracle, "
+                              f"{sum(r['elements'] for r in rs)} elements",
+                  "all_verified": all(r["verified"] for r in rs)}
+    allr = [r for r in rows if r["suite"] in ("S2", "S3", "SET2")]
+    if allr:
+        f = sorted(r["frac_memcpy"] for r in allr)
+        out["rank2_12"] = {"n": len(allr), "worst_frac": f[0], "median_frac": round(statistics.median(f), 4),
+                           "best_frac": f[-1], "all_verified": all(r["verified"] for r in allr)}
+    out["wall_s"] = round(time.perf_counter() - t_start, 1)
+    out["reps"] = reps
+    out["which"] = which
+    return out
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+
+def run_dry(args):
+    """Multi-process plumbing on CPU: gloo group, offline sharded plans of
+    this rank, max-over-ranks reduction and the JSON line -- no kernels."""
+    import torch
+    import torch.distributed as dist
+    import paper_1705_01598_b200 as tt
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    case, desc = workload(args.config)
+    if args.config in ("s5local", "s5redist"):
+        d = tt.plan_sharded_offline(world, rank, case.dims, case.perm, case.esize)
+    elif args.config == "s5p2p":
+        d = tt.plan_sharded_p2p_offline(world, rank, case.dims, case.perm, case.esize)
+    else:
+        d = tt.plan_offline(case.dims, case.perm, case.esize)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "config": args.config,
+                          "max_over_ranks": float(t.item()), "mode": d.get("mode", d.get("kernel")),
+                          "plan": d}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
 
 def run_ours(args):
     import torch
@@ -234,9 +490,6 @@ def run_ours(args):
     import paper_1705_01598_b200 as tt
 
     world, rank, local = dist_env()
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus > 1 must be launched with torch.distributed.run (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -244,23 +497,38 @@ def run_ours(args):
 
     case, desc = workload(args.config)
     E = case.esize
-    tdt = torch.int32 if E == 4 else torch.int64
-    # s5p2p: the fused redistribution (f-1); on one GPU the redistribution is
-    # forced with a one-rank communicator (registration + both barriers run)
+    nd = np.int32 if E == 4 else np.int64
     p2p = args.config == "s5p2p"
+    redist = args.config in ("s5redist", "s5p2p")
+    sharded = args.config in ("s5local", "s5redist", "s5p2p")
+    batch = args.config == "s5batch"
     if p2p and world == 1:
+        # one-rank communicator: the fused path with registration + both barriers
         os.environ["TT_SHARD_FORCE_REDIST"] = "1"
-    sharded = (args.config == "s5redist" and world > 1) or p2p
-    local_vol = case.vol // world if sharded else case.vol
 
-    # seeded input, resident in HBM before timing (rank-specific seed).
-    # Allocated BEFORE the plan's stream is created: creating a stream before
-    # the first device allocation measured ~4 % slower for S1 with the same
-    # kernel (tools/stream_exp3.py; profiles/round1_summary.md).
-    g = torch.Generator(device=dev)
-    g.manual_seed(case.seed + rank)
-    x = torch.randint(-(2 ** 31), 2 ** 31 - 1, (local_vol,), dtype=tdt, device=dev, generator=g)
-    y = torch.empty_like(x)
+    # seeded input, uploaded before timing.  Allocated BEFORE the plan's
+    # stream is created (tools/stream_exp3.py: ~4 % on S1 otherwise).
+    if sharded:
+        words_all = case.words()
+        slab = case.vol // world
+        words = words_all[rank * slab:(rank + 1) * slab]   # input slab r (outermost dim)
+        nbatch = 1
+    elif batch:
+        nbatch = max(1, 8 // world)
+        words_all = None
+        words = None
+    else:
+        words = wl.random_words(case.vol, E, case.seed + rank)
+        nbatch = 1
+    if batch:
+        xs = [torch.from_numpy(wl.random_words(case.vol, E, case.seed + 8 * rank + b).view(nd)).to(dev)
+              for b in range(nbatch)]
+        ys = [torch.empty_like(x) for x in xs]
+        x, y = xs[0], ys[0]
+    else:
+        x = torch.from_numpy(np.ascontiguousarray(words).view(nd)).to(dev)
+        y = torch.empty_like(x)
+    local_vol = x.numel()
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=dev)
 
@@ -269,16 +537,24 @@ def run_ours(args):
         plan = tt.P2PShardedPlan(comm, case.dims, case.perm, E, stream=stream)
         plan.register_output(y)
         execute = plan.execute
-        units_per_step_all = case.vol  # global tensor per step
+        units_all = case.vol
     elif sharded:
-        comm = tt.Comm.from_process_group()
+        comm = tt.Comm.from_process_group() if world > 1 else tt.Comm(tt.unique_id(), 1, 0)
         plan = tt.ShardedPlan(comm, case.dims, case.perm, E, stream=stream)
         execute = plan.execute
-        units_per_step_all = case.vol  # global tensor per step
+        units_all = case.vol
     else:
+        t0 = time.perf_counter()
         plan = tt.Plan(case.dims, case.perm, E, stream=stream)
-        execute = plan.execute
-        units_per_step_all = case.vol * world
+        plan_us = (time.perf_counter() - t0) * 1e6
+        if batch:
+            def execute(_x, _y):
+                for xb, yb in zip(xs, ys):
+                    plan.execute(xb, yb)
+            units_all = case.vol * nbatch * world
+        else:
+            execute = plan.execute
+            units_all = case.vol * world
     desc_plan = plan.describe()
     if desc_plan.get("sharded"):  # report the dominant sub-plan (fused / local / pack)
         for key in ("fused", "local", "pack"):
@@ -315,9 +591,50 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    bytes_step_all = 2.0 * units_per_step_all * E
-    value = bytes_step_all / (ms_step * 1e-3) / 1e9
+    value = 2.0 * units_all * E / (ms_step * 1e-3) / 1e9
     clocks = sampler.summary(h0, h1)
+
+    # sharded split (pack / all-to-all / unpack, or barriers / fused / barrier)
+    split = None
+    if sharded:
+        with torch.cuda.stream(stream):
+            execute(x, y)
+        sp = torch.tensor(list(plan.timings()), dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(sp, op=dist.ReduceOp.MAX)
+        sp = [float(v) for v in sp.tolist()]
+        shard_bytes = local_vol * E
+        nv_bytes = (world - 1) / world * shard_bytes
+        keys = ("entry_barrier_ms", "fused_ms", "exit_barrier_ms") if p2p else ("pack_ms", "alltoall_ms", "unpack_ms")
+        split = dict(zip(keys, [round(v, 4) for v in sp]))
+        split["nvlink_bytes_per_gpu_per_direction"] = int(nv_bytes)
+        if redist and world > 1:
+            t_x = sp[1] if not p2p else ms_step
+            split["nvlink_frac"] = round(nv_bytes / (t_x * 1e-3) / 1e9 / NVLINK_GBS, 4)
+            split["nvlink_frac_of_measured"] = round(nv_bytes / (t_x * 1e-3) / 1e9 / NVLINK_MEASURED, 4)
+            split["nvlink_note"] = ("(P-1)/P * shard bytes over the " + ("all-to-all" if not p2p else "whole step")
+                                    + f" time, vs {NVLINK_GBS:.0f} GB/s nominal / {NVLINK_MEASURED:.0f} measured")
+
+    # verification leg: the timed output, in full, against the oracle
+    verified = None
+    if args.verify == "full" and not batch:
+        stream.synchronize()
+        got = y.cpu().numpy().view(np.uint32 if E == 4 else np.uint64)
+        if sharded:
+            # the global output, block-sharded along its outermost output dim
+            threads = max(1, len(os.sched_getaffinity(0)) // world)
+            want = oracle_expected(case, words_all, threads)
+            slab = case.vol // world
+            ok = memcmp_equal(got, want[rank * slab:(rank + 1) * slab])
+        else:
+            threads = max(1, len(os.sched_getaffinity(0)) // world)
+            ok = memcmp_equal(got, oracle_expected(case, words, threads))
+        okt = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        if world > 1:
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        verified = {"ok": bool(okt.item()), "how": f"full memcmp of every rank's timed output vs the CPU oracle",
+                    "elements": int(case.vol if sharded else case.vol * world)}
+        del got
 
     # memcpy roofline of the same bytes on the same stream (P:L252 GPU-STREAM analogue)
     z = torch.empty_like(x)
@@ -338,10 +655,10 @@ def run_ours(args):
 
     # end-to-end through the C ABI with pinned host buffers (H2D + kernel + D2H)
     e2e = None
-    if not sharded and not args.no_e2e:
+    if not sharded and not batch and not args.no_e2e:
         e2e_steps = args.e2e_steps or min(args.steps, 20)
-        hin = torch.empty(local_vol, dtype=tdt).pin_memory()
-        hin.copy_(x.cpu())
+        hin = torch.empty(local_vol, dtype=x.dtype).pin_memory()
+        hin.copy_(torch.from_numpy(words.view(nd)))
         hout = torch.empty_like(hin).pin_memory()
         plan.execute_host(hin, hout, x, y)
         stream.synchronize()
@@ -360,65 +677,73 @@ def run_ours(args):
         e2e = {"value": round(2.0 * local_vol * E * world / (float(te.item()) * 1e-3) / 1e9, 3),
                "unit": "GB/s", "h2d_bytes_per_step": local_vol * E, "d2h_bytes_per_step": local_vol * E,
                "ms_per_step": round(float(te.item()), 4), "steps": e2e_steps,
-               "note": "tt_execute_host: pinned H2D + permute + D2H on the plan stream"}
+               "note": "tt_execute_host: pinned H2D + permute + D2H on the plan stream",
+               "verified": bool(memcmp_equal(hout.numpy().view(np.uint32 if E == 4 else np.uint64),
+                                             oracle_expected(case, words)))
+               if args.verify == "full" and rank == 0 else None}
         del hin, hout
 
-    # CPU oracle baseline (rank 0, N=1 only), bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        words = case.words()
-        gbs, n, dt = oracle_sample_time(case, words, 15.0, threads)
-        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
-               "sample": f"output elements [0, {n}) of {case.vol} ({dt:.1f} s, {threads} threads, "
-                         f"C gather odometer)"}
-        del words
+    suites = None
+    if rank == 0 and world == 1:
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline(case, words if words is not None else case.words())
+        if args.suites != "none":
+            plan.destroy()
+            del x, y
+            torch.cuda.empty_cache()
+            suites = run_suites(tt, dev, args.suites, 10 if args.suites == "full" else 20, args.suites_out)
+            plan = None
 
     if rank == 0:
         peak, peak_src = peak_hbm()
-        achieved = 2.0 * local_vol * E / (ms_step * 1e-3) / 1e9  # per GPU, dominant kernel
+        achieved = 2.0 * local_vol * E * nbatch / (ms_step * 1e-3) / 1e9  # per GPU
         kernel_key = f"{args.config}:{desc_plan.get('kernel')}"
-        traffic = traffic_from_profiles(kernel_key)
-        launches_per_step = plan.launches
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": DTYPE_NAME[E], "data": "synthetic",
-            "config": {
-                "workload": desc, "dims": list(case.dims), "perm": list(case.perm),
-                "elem_bytes": E, "global_batch": world if not sharded else 1,
-                "parallelism": ("sharded, fused P2P redistribution" if p2p else
-                                "sharded all-to-all" if sharded else
-                                ("independent tensor per GPU" if world > 1 else "single GPU")),
-                "l2": "inputs larger than L2 (%.0f MB per tensor > 126 MB L2); no flush" % (local_vol * E / 1e6),
-                "plan": {k: desc_plan.get(k) for k in ("kernel", "threads", "grid", "smem", "nreg")},
-                "tile": {k: desc_plan.get("tile", {}).get(k) for k in ("ext", "V", "sm")},
-            },
+            "higher_is_better": True,
+            "scaling": "strong" if args.config in ("s5local", "s5batch", "s5redist", "s5p2p") else "weak",
+            "vs_baseline": None, "dtype": DTYPE_NAME[E], "data": "synthetic",
+            "config": config_dict(args, case, desc, world, sharded, desc_plan),
+            "verified": verified,
             "memcpy_gbs_per_gpu": round(memcpy_gbs, 2),
             "frac_of_memcpy": round(achieved / memcpy_gbs, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(kernel_key),
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": 2 * local_vol * E,
                          "kernel": desc_plan.get("kernel")},
             "clocks": clocks,
-            "gpu_launches": args.steps * launches_per_step,
+            "gpu_launches": args.steps * (plan.launches if plan is not None else 1) * nbatch,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if not sharded:
+            line["plan_us"] = round(plan_us, 1)
+        if split:
+            line["sharded"] = split
+        if suites:
+            line["suites"] = suites
         print(json.dumps(line), flush=True)
-    plan.destroy()
+    if plan is not None:
+        plan.destroy()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    world, _, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args, argv)
     if args.impl == "reference":
         return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
     return run_ours(args)
 
 

@@ -103,6 +103,8 @@ typedef struct {
     int slot_dims;       /* TILE: 1 = slot-dim thread map when it applies, -1 = never, 0 = planner */
     int sd_vmax;         /* TILE: largest slot-dim tile searched by the model, elements
                             (<= 8192 for 4-byte, 6144 for 8-byte words); 0 = planner's default */
+    int vector_gather;   /* TILE: 1 = load input runs as 16-byte chunks of their aligned superset
+                            (tile_vg_kernel; stages 3/4, default 4), -1 = never, 0 = planner */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

@@ -46,7 +46,8 @@ class PlanOptions(ctypes.Structure):
                 ("no_fusion", ctypes.c_int), ("grid_order", ctypes.c_int),
                 ("no_widen", ctypes.c_int), ("stages", ctypes.c_int),
                 ("accumulate", ctypes.c_int), ("slots", ctypes.c_int),
-                ("slot_dims", ctypes.c_int), ("sd_vmax", ctypes.c_int)]
+                ("slot_dims", ctypes.c_int), ("sd_vmax", ctypes.c_int),
+                ("vector_gather", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -126,10 +127,11 @@ def _arrays(dims, perm):
 
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
              grid_order=0, no_widen=False, stages=0, accumulate=False, slots=0, slot_dims=0,
-             sd_vmax=0):
+             sd_vmax=0, vector_gather=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
                        1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
-                       1 if accumulate else 0, int(slots), int(slot_dims), int(sd_vmax))
+                       1 if accumulate else 0, int(slots), int(slot_dims), int(sd_vmax),
+                       int(vector_gather))
 
 
 def _ptr(x) -> int:

@@ -449,6 +449,16 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
             vars.push_back(o);
         }
 
+    // the heuristic tile with the vector-gather load phase (16-byte chunks of
+    // the aligned superset of every input run, 3- or 4-stage cp.async ring)
+    if (hp.n >= 2)
+        for (int st : {4, 3}) {
+            tt_plan_options_t o = opt(TT_KERNEL_TILE, 0, 0, 0, 0, 0);
+            o.vector_gather = 1;
+            o.stages = st;
+            vars.push_back(o);
+        }
+
     std::vector<Plan*> cands{heur};
     std::vector<std::string> keys{describe_json(*heur)};
     for (const auto& o : vars) {

@@ -318,7 +318,7 @@ struct SmemSample {
 // Adding the same offset to every lane's position permutes the banks, so an
 // access's wavefront count depends only on the lanes' coordinates relative to
 // lane 0: sampled accesses with equal relative patterns are merged (weighted).
-static SmemSample smem_sample(const TileParams& tp) {
+static SmemSample smem_sample(const TileParams& tp, int sides = 3) {
     SmemSample s;
     s.a = tp.a;
     const int V = tp.V;
@@ -328,6 +328,7 @@ static SmemSample smem_sample(const TileParams& tp) {
     for (int w = 0; w < nw; w += step) {
         const int nl = std::min(32, V - w * 32);
         for (int side = 0; side < 2; ++side) {  // 0: staging store (input order), 1: transposed read
+            if (!(sides & (1 << side))) continue;
             int c0[kMaxDims] = {};
             for (int l = 0; l < 32; ++l) {
                 int kk = w * 32 + l;
@@ -784,6 +785,87 @@ static void choose_smem(TileParams& tp, int esize) {
     tp.sbuf = (int32_t)((foot + 3) / 4 * 4);
 }
 
+// Vector-gather layout (kernels_vg.cu tile_vg_kernel) of a chosen generic
+// tile: the run dims (the tile's first dims that are dense in the input),
+// a run slot of 16-byte chunks holding the 16-byte-aligned superset of a run
+// (worst-case shift 16/E - 1 elements), padded slot strides for the other
+// tile dims (multiples of 16 bytes so every slot stays 16-byte aligned),
+// chosen on the transposed read's bank-conflict cost, and the run
+// table behind the S staging buffers.  False when the runs are shorter than
+// `minRunBytes` or the footprint exceeds `maxSmem`.
+static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int minRunBytes,
+                     int& threads, int& nreg, int& smem) {
+    const int E = pr.esize;
+    if ((E != 4 && E != 8) || !pr.dense || pr.span >= (int64_t(1) << 31)) return false;
+    const int VPC = 16 / E;
+    int M = 0;
+    int64_t L = 1;
+    while (M < tp.a && tp.tSin[M] == L) L *= tp.tExt[M++];
+    if (M == 0 || L * E < minRunBytes || M == tp.a) return false;  // M == a: a plain copy
+    tp.vgM = M;
+    tp.vgL = (int32_t)L;
+    tp.vgLtail = (int32_t)L;
+    tp.vgRunBit = 0;
+    for (int s = 0; s < tp.nSplit; ++s)
+        if (tp.splitTile[s] == M - 1 && tp.splitTail[s] != tp.splitChunk[s]) {
+            tp.vgRunBit = 1 << s;
+            tp.vgLtail = (int32_t)(L / tp.tExt[M - 1] * tp.splitTail[s]);
+        }
+    tp.vgNR = (int32_t)(tp.V / L);
+    const int64_t nch = (L + VPC - 1 + VPC - 1) / VPC;  // 16-byte chunks of a run at worst shift
+    int g = 1;
+    while (g < 32 && g < nch) g *= 2;
+    tp.vgG = g;
+    // slot strides: tile dims < M dense (the run), the rest padded
+    int32_t pad[kMaxDims] = {};
+    int32_t sm[kMaxDims];
+    auto strides = [&]() -> int64_t {
+        int64_t acc = 1;
+        for (int t = 0; t < tp.a; ++t) {
+            if (t == M) acc = nch * VPC;
+            acc += pad[t];
+            sm[t] = (int32_t)acc;
+            acc *= tp.tExt[t];
+        }
+        int64_t last = 0;
+        for (int t = M; t < tp.a; ++t) last += (int64_t)(tp.tExt[t] - 1) * sm[t];
+        return last + nch * VPC;
+    };
+    const SmemSample sample = smem_sample(tp, 2);  // the transposed read only
+    strides();
+    long best = smem_cost(sample, E, sm);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int t = M; t < tp.a; ++t) {
+            int32_t bestPad = pad[t];
+            for (int c = 0; c < 32; c += VPC) {
+                pad[t] = c;
+                if (strides() * E > 65536 * 2) continue;
+                const long cst = smem_cost(sample, E, sm, best);
+                if (cst < best) { best = cst; bestPad = c; }
+            }
+            pad[t] = bestPad;
+        }
+    const int64_t foot = strides();
+    for (int t = 0; t < tp.a; ++t) tp.tSm[t] = sm[t];
+    tp.sbuf = (int32_t)((foot + VPC - 1) / VPC * VPC);
+    tp.vgTab = S * tp.sbuf * E;
+    tp.vgInBytes = pr.span * E;
+    smem = tp.vgTab + 8 * tp.vgNR;
+    if (smem > maxSmem || (int64_t)(foot + 8) * E >= (int64_t(1) << 24)) return false;
+    // store phase: NT threads x NREG slots cover the tile
+    threads = 0;
+    for (int R : {8, 4, 16}) {
+        int T = (int)((tp.V + R - 1) / R);
+        T = (T + 31) / 32 * 32;
+        if (T < 64) T = 64;
+        if (T > (R >= 16 ? 256 : 1024)) continue;  // kernels_vg.cu launch bounds
+        threads = T;
+        nreg = R;
+        break;
+    }
+    return threads > 0;
+}
+
 // Vectorised 2-D tiled kernel (TT_KERNEL_TILED2D): A = input dim 0, B = p[0].
 // Returns false if the problem is not of that class or the vector width
 // would be 1.  TA = 16*VW, TB = 16*VW*R with (VW, R) = (4,1) | (2,2) for 4-byte
@@ -1229,6 +1311,30 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
             kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
         }
     }
+    // vector-gather load phase (tile_vg_kernel): 16-byte cp.async chunks of
+    // the aligned superset of every input run, S-stage ring
+    const int vgOpt = opts ? opts->vector_gather : 0;
+    if (vgOpt > 0 && !acc && !kc.idx64) {
+        TileParams vt = plan.tile;
+        vt.sdSlot[0] = vt.sdSlot[1] = -1;
+        const int S = opts && opts->stages >= 3 ? std::min(4, opts->stages) : 4;
+        int thr = 0, nr = 0, sm = 0;
+        if (build_vg(vt, pr, S, dev.max_smem_per_block, 32, thr, nr, sm)) {
+            plan.tile = vt;
+            kc.vg = 1;
+            kc.sdq = kc.sdr = 0;
+            kc.stages = S;
+            kc.threads = thr;
+            kc.nreg = nr;
+            kc.smem = sm;
+            OccQuery qv{TT_KERNEL_TILE, E, nr, S, thr, sm, false, 0, 0, 0, 0, 0, 1};
+            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qv, dev) : 0);
+            if (per <= 0)
+                per = std::max(1, std::min({dev.max_smem_per_sm / (sm + 1024), dev.max_threads_per_sm / thr,
+                                            dev.regs_per_sm / (thr * 64)}));
+            kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
+        }
+    }
     kc.fb_threads = kc.threads;
     kc.fb_grid = kc.grid;
     kc.fb_smem = kc.smem;
@@ -1395,6 +1501,9 @@ std::string describe_json(const Plan& plan) {
         arr(o, t.gSin, t.h);
         o << ",\"grid_sout\":";
         arr(o, t.gSout, t.h);
+        if (kc.vg)
+            o << ",\"vg\":{\"M\":" << t.vgM << ",\"L\":" << t.vgL << ",\"Ltail\":" << t.vgLtail
+              << ",\"runs\":" << t.vgNR << ",\"group\":" << t.vgG << ",\"stages\":" << kc.stages << "}";
         if (kc.sdq) {
             o << ",\"sd\":{\"q\":" << kc.sdq << ",\"r\":" << kc.sdr << ",\"slot\":";
             arr(o, t.sdSlot, 2);

@@ -83,6 +83,19 @@ struct TileParams {
     int32_t sdC[2];     // chunks of the slot dim, ceil(ext / sdR)
     int32_t sdU[2];     // thread-space size: V / ext * chunks
     int32_t sdQ[2];     // passes, ceil(sdU / threads)
+    // vector-gather variant (tile_vg_kernel, kernels_vg.cu): the load phase
+    // copies the 16-byte-aligned superset of every input run (the tile's
+    // first vgM dims, contiguous in the input) in 16-byte cp.async chunks.
+    // Run r of a tile sits in shared memory at a 16-byte-aligned slot; its
+    // elements are shifted by the run start's offset inside its 16-byte chunk.
+    int32_t vgM;        // run dims: tile dims 0 .. vgM-1 (tile-input order)
+    int32_t vgL;        // run length (elements) of a full run
+    int32_t vgLtail;    // run length when the run's split dim is at its ragged tail
+    int32_t vgRunBit;   // need bit (1 or 2) of that split dim; 0 if the run is never ragged
+    int32_t vgNR;       // runs per tile
+    int32_t vgG;        // lanes per run group (power of two <= 32)
+    int32_t vgTab;      // byte offset of the run table (uint2 per run) in dynamic shared memory
+    int64_t vgInBytes;  // bytes of the input tensor (chunks are clipped to [in, in + vgInBytes))
 };
 
 // Row-copy (fastest dim unchanged, long rows; TiledCopy class P:L141): each
@@ -132,6 +145,7 @@ struct KernelChoice {
     int stages = 0;                // generic tile: 0 = register double buffer, >= 3 = cp.async ring
     int acc = 0;                   // accumulate plan (f-3): generic tile with alpha/beta
     int sdq = 0, sdr = 0;          // generic tile, slot-dim variant: passes x slots (0 = classic)
+    int vg = 0;                    // generic tile, vector-gather variant (tile_vg_kernel)
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
     // model features of the generic tile (describe "model"; calibration)
@@ -156,6 +170,7 @@ struct OccQuery {
     int ta, tb;  // TILED2D tile
     int acc;     // TILE accumulate variant
     int sdq, sdr;  // TILE slot-dim variant (passes, slots); 0 = classic; TILED2D: sdq = cp.async stages
+    int vg;        // TILE vector-gather variant (nreg = slots, vec = stages)
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 

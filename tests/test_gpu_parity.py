@@ -260,6 +260,45 @@ def test_slot_dim_async_ring(esize, stages):
     assert used >= 8
 
 
+VG_SHAPES = RANDOM_SHAPES[:11] + [
+    ((37, 29, 11), (2, 0, 1)), ((5, 3, 2, 4, 35, 33), (5, 4, 3, 2, 1, 0)),
+    ((46, 46, 46, 7), (3, 1, 0, 2)), ((3, 5, 7, 11, 13, 2), (4, 2, 0, 5, 3, 1)),
+    ((5, 5, 5, 5, 5, 5, 5, 5), (0, 6, 3, 7, 1, 4, 2, 5)), ((9, 7, 5, 3, 5, 7, 9), (6, 4, 2, 0, 1, 3, 5)),
+    ((1025, 3, 2), (2, 1, 0)), ((3, 6, 6, 6, 6, 6, 6), (0, 5, 2, 3, 6, 1, 4)), ((6, 7), (1, 0))]
+
+
+@pytest.mark.parametrize("esize", [4, 8])
+@pytest.mark.parametrize("stages", [3, 4])
+def test_vector_gather(esize, stages):
+    """The vector-gather load phase (tile_vg_kernel): runs copied as 16-byte
+    chunks of their aligned superset.  Ragged run tails and ragged non-run
+    splits, runs shorter than a chunk, forced tiles, pointers at every
+    element offset inside a 16-byte chunk (the shift logic, and the chunks
+    that cross the start and the end of the input are clipped)."""
+    used = 0
+    for dims, perm in VG_SHAPES:
+        vol = int(np.prod(dims))
+        if vol > 2_000_000:
+            dims = wl.scaled(wl.Case("x", dims, perm, esize, 3), 1_000_000).dims
+        try:
+            j = tt.Plan(dims, perm, esize, vector_gather=1, stages=stages, no_widen=True).describe()
+        except tt.TTError:
+            continue
+        if "vg" not in j.get("tile", {}):
+            continue
+        used += 1
+        check(dims, perm, esize, vector_gather=1, stages=stages, no_widen=True)
+        words = wl.random_words(int(np.prod(dims)), esize, 17)
+        want = orc.permute(dims, perm, words)
+        for off in range(1, 16 // esize):
+            got = run_gpu(dims, perm, words, offset=off, vector_gather=1, stages=stages, no_widen=True)
+            np.testing.assert_array_equal(got, want, err_msg=f"{dims} {perm} offset {off}")
+    assert used >= 12
+    for run in [(8, 3), (32, 32), (64, 16), (16, 256)]:
+        for dims, perm in [((37, 29, 11), (2, 0, 1)), ((9, 8, 7, 6, 5), (3, 4, 0, 2, 1))]:
+            check(dims, perm, esize, run_in=run[0], run_out=run[1], vector_gather=1, stages=stages)
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)

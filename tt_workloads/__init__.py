@@ -35,19 +35,46 @@ def case_seed(index: int, suite_seed: int = SUITE_SEED) -> int:
     return splitmix64(suite_seed ^ int(index))
 
 
+_CHUNK = 1 << 22  # 64-bit draws per generator stream
+
+
+def _raw64(count: int, seed: int) -> np.ndarray:
+    """``count`` 64-bit draws: stream c of 2^22 draws comes from
+    PCG64(seed) jumped c times (stream 0 is PCG64(seed) itself), so the
+    streams fill disjoint chunks in parallel host threads (numpy releases
+    the GIL while drawing) and the result does not depend on the thread
+    count."""
+    if count <= _CHUNK:
+        return np.random.PCG64(seed).random_raw(count).astype(np.uint64, copy=False)
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    out = np.empty(count, dtype=np.uint64)
+    nch = (count + _CHUNK - 1) // _CHUNK
+
+    def fill(c):
+        bg = np.random.PCG64(seed)
+        if c:
+            bg = bg.jumped(c)
+        m = min(_CHUNK, count - c * _CHUNK)
+        out[c * _CHUNK:c * _CHUNK + m] = bg.random_raw(m)
+
+    with ThreadPoolExecutor(max(1, min(16, len(os.sched_getaffinity(0))))) as ex:
+        list(ex.map(fill, range(nch)))
+    return out
+
+
 def random_words(n: int, esize: int, seed: int) -> np.ndarray:
-    """n random 4- or 8-byte words (uint32/uint64) from PCG64(seed).
+    """n random 4- or 8-byte words (uint32/uint64) from seeded PCG64 streams.
 
     Every bit pattern is equally likely, so NaN payloads, infinities,
     subnormals and -0.0 all occur when the words are viewed as floats.
     """
     n = int(n)
-    bg = np.random.PCG64(int(seed) & _MASK64)
+    seed = int(seed) & _MASK64
     if esize == 8:
-        return bg.random_raw(n).astype(np.uint64, copy=False)
+        return _raw64(n, seed)
     if esize == 4:
-        raw = bg.random_raw((n + 1) // 2).astype(np.uint64, copy=False)
-        return raw.view(np.uint32)[:n]
+        return _raw64((n + 1) // 2, seed).view(np.uint32)[:n]
     raise ValueError("esize must be 4 or 8")
 
 
