@@ -502,9 +502,6 @@ def run_ours(args):
     redist = args.config in ("s5redist", "s5p2p")
     sharded = args.config in ("s5local", "s5redist", "s5p2p")
     batch = args.config == "s5batch"
-    if p2p and world == 1:
-        # one-rank communicator: the fused path with registration + both barriers
-        os.environ["TT_SHARD_FORCE_REDIST"] = "1"
 
     # seeded input, uploaded before timing.  Allocated BEFORE the plan's
     # stream is created (tools/stream_exp3.py: ~4 % on S1 otherwise).
@@ -534,7 +531,8 @@ def run_ours(args):
 
     if p2p:
         comm = tt.Comm.from_process_group() if world > 1 else tt.Comm(tt.unique_id(), 1, 0)
-        plan = tt.P2PShardedPlan(comm, case.dims, case.perm, E, stream=stream)
+        # one rank: force the fused path (registration + both barriers run)
+        plan = tt.P2PShardedPlan(comm, case.dims, case.perm, E, stream=stream, force_redistribute=world == 1)
         plan.register_output(y)
         execute = plan.execute
         units_all = case.vol

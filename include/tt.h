@@ -51,7 +51,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define TT_VERSION 1
+#define TT_VERSION 2
 #define TT_MAX_RANK 32          /* the warp-parallel decode handles h <= 32 terms */
 #define TT_NCCL_UNIQUE_ID_BYTES 128
 
@@ -105,6 +105,12 @@ typedef struct {
                             (<= 8192 for 4-byte, 6144 for 8-byte words); 0 = planner's default */
     int vector_gather;   /* TILE: 1 = load input runs as 16-byte chunks of their aligned superset
                             (tile_vg_kernel; stages 3/4, default 4), -1 = never, 0 = planner */
+    int t2d_vec2;        /* TILED2D: 2-element vectors where the extents allow only those:
+                            1 = always, -1 = never (scalar kernel), 0 = planner's measured rule */
+    int force_redistribute; /* sharded plans (tt_plan_sharded_ex / _p2p_ex): take the
+                            redistribution path even with one rank (single-GPU tests) */
+    int vg_policy;       /* vector-gather loads, calibration: 0 = cp.async.cg, 1 = .ca,
+                            2 = .cg with an L2 evict_last hint, 3 = evict_normal hint */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */
@@ -277,6 +283,12 @@ tt_status_t tt_comm_destroy(tt_comm_t comm);
 tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int rank, const int64_t* global_dims,
                             const int* perm, size_t elem_size, tt_stream_t stream);
 
+/* tt_plan_sharded with options (NULL = tt_plan_sharded); only
+ * force_redistribute is read. */
+tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int rank, const int64_t* global_dims,
+                               const int* perm, size_t elem_size, tt_stream_t stream,
+                               const tt_plan_options_t* opts);
+
 /*
  * tt_plan_sharded_offline -- the same geometry and sub-plans for process
  * `proc` of `nranks` without a communicator or GPU (describe only; executing
@@ -326,6 +338,13 @@ tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3);
 tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int rank,
                                 const int64_t* global_dims, const int* perm, size_t elem_size,
                                 tt_stream_t stream);
+
+/* tt_plan_sharded_p2p with options (NULL = tt_plan_sharded_p2p); only
+ * force_redistribute is read (the fused path with one rank: registration and
+ * both barriers run on a single GPU). */
+tt_status_t tt_plan_sharded_p2p_ex(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int rank,
+                                   const int64_t* global_dims, const int* perm, size_t elem_size,
+                                   tt_stream_t stream, const tt_plan_options_t* opts);
 
 /* tt_plan_sharded_p2p geometry without a GPU (describe only): "mode" "p2p",
  * "fused" (the strided sub-box plan), "in_step" / "out_offset" (elements),

@@ -47,7 +47,8 @@ class PlanOptions(ctypes.Structure):
                 ("no_widen", ctypes.c_int), ("stages", ctypes.c_int),
                 ("accumulate", ctypes.c_int), ("slots", ctypes.c_int),
                 ("slot_dims", ctypes.c_int), ("sd_vmax", ctypes.c_int),
-                ("vector_gather", ctypes.c_int)]
+                ("vector_gather", ctypes.c_int), ("t2d_vec2", ctypes.c_int),
+                ("force_redistribute", ctypes.c_int), ("vg_policy", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -84,6 +85,8 @@ def _load():
         "tt_comm_init": [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int],
         "tt_comm_destroy": [vp],
         "tt_plan_sharded": [ctypes.POINTER(vp), vp, ctypes.c_int, i64p, ip, ctypes.c_size_t, vp],
+        "tt_plan_sharded_ex": [ctypes.POINTER(vp), vp, ctypes.c_int, i64p, ip, ctypes.c_size_t, vp,
+                               ctypes.POINTER(PlanOptions)],
         "tt_plan_sharded_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     i64p, ip, ctypes.c_size_t],
         "tt_sharded_timings": [vp, ctypes.POINTER(ctypes.c_float)],
@@ -91,6 +94,8 @@ def _load():
         "tt_plan_shard_dims": [vp, i64p, i64p],
         "tt_plan_sharded_p2p": [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 i64p, ip, ctypes.c_size_t, vp],
+        "tt_plan_sharded_p2p_ex": [ctypes.POINTER(vp), vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   i64p, ip, ctypes.c_size_t, vp, ctypes.POINTER(PlanOptions)],
         "tt_plan_sharded_p2p_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         i64p, ip, ctypes.c_size_t],
         "tt_sharded_register_output": [vp, vp],
@@ -127,11 +132,12 @@ def _arrays(dims, perm):
 
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
              grid_order=0, no_widen=False, stages=0, accumulate=False, slots=0, slot_dims=0,
-             sd_vmax=0, vector_gather=0):
+             sd_vmax=0, vector_gather=0, t2d_vec2=0, force_redistribute=False,
+             vg_policy=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
                        1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
                        1 if accumulate else 0, int(slots), int(slot_dims), int(sd_vmax),
-                       int(vector_gather))
+                       int(vector_gather), int(t2d_vec2), 1 if force_redistribute else 0, int(vg_policy))
 
 
 def _ptr(x) -> int:

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes
 
-from . import lib, _check, _arrays, _stream_handle, _describe, _ptr, NCCL_UNIQUE_ID_BYTES
+from . import lib, _check, _arrays, _stream_handle, _describe, _ptr, _options, NCCL_UNIQUE_ID_BYTES
 
 
 def unique_id() -> bytes:
@@ -57,13 +57,17 @@ class ShardedPlan:
     (slab ``rank`` of ``global_dims[-1] / nranks``) into the output
     block-sharded along its outermost output dim."""
 
-    def __init__(self, comm: Comm, global_dims, perm, elem_size: int, stream=None):
+    def __init__(self, comm: Comm, global_dims, perm, elem_size: int, stream=None,
+                 force_redistribute: bool = False):
+        """``force_redistribute``: the pack / all-to-all / unpack path even
+        with one rank (single-GPU tests)."""
         n, d, p = _arrays(global_dims, perm)
         self.comm = comm
         self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
         h = ctypes.c_void_p()
-        _check(lib.tt_plan_sharded(ctypes.byref(h), comm._h, n, d, p, self.elem_size,
-                                   _stream_handle(stream)), "tt_plan_sharded")
+        o = _options(force_redistribute=force_redistribute)
+        _check(lib.tt_plan_sharded_ex(ctypes.byref(h), comm._h, n, d, p, self.elem_size,
+                                      _stream_handle(stream), ctypes.byref(o)), "tt_plan_sharded")
         self._h = h
         a = (ctypes.c_int64 * n)()
         b = (ctypes.c_int64 * n)()
@@ -113,7 +117,7 @@ class P2PShardedPlan(ShardedPlan):
     every rank's output slab as a device tensor (no barriers)."""
 
     def __init__(self, comm, global_dims, perm, elem_size: int, stream=None, nranks=None,
-                 proc=None):
+                 proc=None, force_redistribute: bool = False):
         n, d, p = _arrays(global_dims, perm)
         self.comm = comm
         if comm is not None:
@@ -123,9 +127,10 @@ class P2PShardedPlan(ShardedPlan):
         self.nranks, self.proc = int(nranks), int(proc)
         self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
         h = ctypes.c_void_p()
-        _check(lib.tt_plan_sharded_p2p(ctypes.byref(h), comm._h if comm is not None else None,
-                                       self.nranks, self.proc, n, d, p, self.elem_size,
-                                       _stream_handle(stream)), "tt_plan_sharded_p2p")
+        o = _options(force_redistribute=force_redistribute)
+        _check(lib.tt_plan_sharded_p2p_ex(ctypes.byref(h), comm._h if comm is not None else None,
+                                          self.nranks, self.proc, n, d, p, self.elem_size,
+                                          _stream_handle(stream), ctypes.byref(o)), "tt_plan_sharded_p2p")
         self._h = h
         a = (ctypes.c_int64 * n)()
         b = (ctypes.c_int64 * n)()

@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <mutex>
+#include <unordered_set>
 
 #include "tt_internal.h"
 
@@ -17,10 +19,31 @@ using namespace tt;
 
 namespace tt {
 
+static std::mutex g_handles_mu;
+static std::unordered_set<const void*> g_handles;
+
+void* publish_handle(void* h) {
+    if (h != nullptr) {
+        std::lock_guard<std::mutex> g(g_handles_mu);
+        g_handles.insert(h);
+    }
+    return h;
+}
+
+bool handle_live(const void* h) {
+    if (h == nullptr) return false;
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    return g_handles.count(h) != 0;
+}
+
+bool retire_handle(const void* h) {
+    if (h == nullptr) return false;
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    return g_handles.erase(h) != 0;
+}
+
 Plan* as_plan(tt_plan_t h) {
-    Plan* p = reinterpret_cast<Plan*>(h);
-    if (p == nullptr || p->magic != 0x54545054u) return nullptr;
-    return p;
+    return handle_live(h) ? reinterpret_cast<Plan*>(h) : nullptr;
 }
 
 tt_status_t query_device(DeviceInfo& dev) {
@@ -141,37 +164,6 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
-    // 8-byte elements on the generic tile: the slot-dim map with a 4-stage
-    // cp.async ring (tile_sd_async_kernel) when that plan runs at one CTA per
-    // SM.  Same-box A/B over the suites' fp64 generic-tile cases
-    // (profiles/round1_ab_sd_async8.txt): 18 of 20 such cases faster, median
-    // 1.10x, none slower; at 2+ CTAs per SM it was a wash.  Planner-chosen
-    // plans only (no options); TT_KNOB_SD_RING8=0 turns it off.
-    static const tt_plan_options_t zero{};
-    const bool noOpts = opts == nullptr || std::memcmp(opts, &zero, sizeof(zero)) == 0;
-    const char* kv = std::getenv("TT_KNOB_SD_RING8");
-    // also 8-byte words widened from 4-byte elements (A/B: 5 of 5 faster,
-    // 0.93-0.99x time, profiles/round1_ab_sd_async8.txt); TT_KNOB_SD_RING8W=0
-    // keeps those on the register pipeline
-    const char* kw = std::getenv("TT_KNOB_SD_RING8W");
-    const bool word8 = elem_size == 8 ? p->widen == 1
-                                      : (!(kw && *kw && std::atoi(kw) == 0) && p->prob.esize == 8);
-    if (noOpts && !(kv && *kv && std::atoi(kv) == 0) && word8 &&
-        p->kc.kernel == TT_KERNEL_TILE && !p->kc.idx64) {
-        Plan alt;
-        alt.device = p->device;
-        alt.stream = p->stream;
-        alt.rank = rank;
-        alt.prob = p->prob;
-        tt_plan_options_t o{};
-        o.slot_dims = 1;
-        o.stages = 4;
-        if (choose_plan(alt, dev, &o, occ) == TT_SUCCESS && alt.kc.kernel == TT_KERNEL_TILE &&
-            alt.kc.sdq && alt.kc.stages == 4 && alt.kc.grid <= dev.num_sms) {
-            p->tile = alt.tile;
-            p->kc = alt.kc;
-        }
-    }
     *out = p;
     return TT_SUCCESS;
 }
@@ -210,13 +202,11 @@ static tt_status_t build_pipe(Plan& p) {
     if (dt < 2) return TT_UNSUPPORTED;
     // chunks of >= 16 MB, at most 32 (S1 e2e: 4 / 8 / 16 / 32 chunks =
     // 82 / 88 / 90 / 92 GB/s -- both PCIe directions near their limit; more
-    // chunks shorten the pipeline's fill and drain); knob for calibration
-    const char* kn = std::getenv("TT_KNOB_PIPE_CHUNKS");
+    // chunks shorten the pipeline's fill and drain)
     int64_t volAll = 1;
     for (int64_t x : p.dims) volAll *= x;
     const int64_t bytesAll = volAll * (p.prob.esize / p.widen);
-    const int want = kn && *kn ? std::max(2, std::atoi(kn))
-                               : (int)std::max<int64_t>(2, std::min<int64_t>(32, bytesAll >> 24));
+    const int want = (int)std::max<int64_t>(2, std::min<int64_t>(32, bytesAll >> 24));
     const int nch = (int)std::min<int64_t>(dt, want);
     HostPipe* hp = new (std::nothrow) HostPipe();
     if (!hp) return TT_INTERNAL_ERROR;
@@ -314,7 +304,6 @@ void destroy_plan(Plan* p) {
     if (p == nullptr) return;
     if (p->shard) destroy_shard(p->shard);
     p->shard = nullptr;
-    p->magic = 0;
     delete p;
 }
 
@@ -325,7 +314,7 @@ static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, cons
                              const tt_plan_options_t* opts, OccupancyFn occ) {
     Plan* p = nullptr;
     tt_status_t st = create_plan(&p, rank, dims, perm, elem_size, stream, dev, opts, occ);
-    if (out) *out = reinterpret_cast<tt_plan_t>(p);
+    if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
 
@@ -505,7 +494,7 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
     p->measured_ms = bestMs;
     p->heuristic_ms = heurMs;
     p->n_candidates = (int)cands.size();
-    *plan = reinterpret_cast<tt_plan_t>(p);
+    *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return TT_SUCCESS;
 }
 
@@ -547,7 +536,7 @@ tt_status_t tt_plan_strided(tt_plan_t* plan, int rank, const int64_t* dims, cons
     Plan* p = nullptr;
     st = create_plan_s(&p, rank, dims, perm, elem_size, stream, dev, nullptr, &cuda_occupancy,
                        in_strides, out_strides);
-    *plan = reinterpret_cast<tt_plan_t>(p);
+    *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
 
@@ -562,7 +551,7 @@ tt_status_t tt_plan_strided_offline(tt_plan_t* plan, int rank, const int64_t* di
     Plan* p = nullptr;
     tt_status_t st = create_plan_s(&p, rank, dims, perm, elem_size, nullptr, dev, opts, nullptr,
                                    in_strides, out_strides);
-    *plan = reinterpret_cast<tt_plan_t>(p);
+    *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
 
@@ -647,9 +636,8 @@ int tt_plan_launches(tt_plan_t plan) {
 }
 
 tt_status_t tt_destroy(tt_plan_t plan) {
-    Plan* p = as_plan(plan);
-    if (p == nullptr) return TT_INVALID_PLAN;
-    destroy_plan(p);
+    if (!retire_handle(plan)) return TT_INVALID_PLAN;  // NULL, never issued, or already destroyed
+    destroy_plan(reinterpret_cast<Plan*>(plan));
     return TT_SUCCESS;
 }
 

@@ -44,7 +44,6 @@ struct Operand {
 };
 
 struct Contract {
-    uint32_t magic = 0x54544354u;  // "TTCT"
     int device = -1;
     void* stream = nullptr;
     int esize = 8;
@@ -75,7 +74,6 @@ static void destroy_contract(Contract* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->blas) cublasDestroy(c->blas);
-    c->magic = 0;
     delete c;
 }
 
@@ -269,9 +267,7 @@ static std::string describe_contract(const Contract& c) {
 using namespace tt;
 
 static Contract* as_contract(tt_contract_t h) {
-    Contract* c = reinterpret_cast<Contract*>(h);
-    if (c == nullptr || c->magic != 0x54544354u) return nullptr;
-    return c;
+    return handle_live(h) ? reinterpret_cast<Contract*>(h) : nullptr;
 }
 
 extern "C" {
@@ -285,7 +281,7 @@ tt_status_t tt_contract_plan(tt_contract_t* plan, int rank_d, const int* modes_d
     Contract* c = nullptr;
     tt_status_t st = build_contract(&c, rank_d, modes_d, rank_l, dims_l, modes_l, rank_r, dims_r,
                                     modes_r, elem_size, stream, true);
-    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_contract_t>(c);
+    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_contract_t>(publish_handle(c));
     return st;
 }
 
@@ -297,7 +293,7 @@ tt_status_t tt_contract_plan_offline(tt_contract_t* plan, int rank_d, const int*
     Contract* c = nullptr;
     tt_status_t st = build_contract(&c, rank_d, modes_d, rank_l, dims_l, modes_l, rank_r, dims_r,
                                     modes_r, elem_size, nullptr, false);
-    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_contract_t>(c);
+    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_contract_t>(publish_handle(c));
     return st;
 }
 
@@ -396,9 +392,8 @@ tt_status_t tt_contract_describe(tt_contract_t plan, char* buf, size_t len) {
 }
 
 tt_status_t tt_contract_destroy(tt_contract_t plan) {
-    Contract* c = as_contract(plan);
-    if (c == nullptr) return TT_INVALID_PLAN;
-    destroy_contract(c);
+    if (!retire_handle(plan)) return TT_INVALID_PLAN;  // NULL or already destroyed
+    destroy_contract(reinterpret_cast<Contract*>(plan));
     return TT_SUCCESS;
 }
 

@@ -53,7 +53,6 @@ namespace tt {
 static int64_t ceil_div_i64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct tt_comm_impl {
-    uint32_t magic = 0x5454434du;  // "TTCM"
     ncclComm_t nccl = nullptr;
     int nranks = 0, rank = 0, device = -1;
 };
@@ -155,7 +154,8 @@ std::string describe_shard_json(const Plan& plan) {
 // Geometry + sub-plans; comm may be null (offline).
 static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int rank, int n,
                                  const int64_t* gd, const int* perm, size_t esize, void* stream,
-                                 const DeviceInfo& dev, OccupancyFn occ, bool p2p = false) {
+                                 const DeviceInfo& dev, OccupancyFn occ, bool p2p = false,
+                                 bool forceRedist = false) {
     *out = nullptr;
     tt_status_t st = validate(n, gd, perm, esize);
     if (st != TT_SUCCESS) return st;
@@ -163,10 +163,9 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
     const int P = nranks;
     const int t = perm[n - 1];
     if (gd[n - 1] % P != 0) return TT_UNSUPPORTED;
-    // TT_SHARD_FORCE_REDIST=1 (tests): take the pack / all-to-all / unpack path
-    // even with one rank, so the NCCL path runs on a single-GPU box
-    const char* force = std::getenv("TT_SHARD_FORCE_REDIST");
-    const bool redist = (t != n - 1) && (P > 1 || (force && force[0] == '1'));
+    // forceRedist (option force_redistribute, tests): take the redistribution
+    // path even with one rank, so the NCCL / P2P machinery runs on one GPU
+    const bool redist = (t != n - 1) && (P > 1 || forceRedist);
     if (redist && gd[t] % P != 0) return TT_UNSUPPORTED;
 
     ShardInfo* s = new (std::nothrow) ShardInfo();
@@ -394,9 +393,7 @@ static_assert(sizeof(RegRecord) == 256, "registration record");
 using namespace tt;
 
 static tt_comm_impl* as_comm(tt_comm_t c) {
-    tt_comm_impl* p = reinterpret_cast<tt_comm_impl*>(c);
-    if (p == nullptr || p->magic != 0x5454434du) return nullptr;
-    return p;
+    return handle_live(c) ? reinterpret_cast<tt_comm_impl*>(c) : nullptr;
 }
 
 extern "C" {
@@ -429,21 +426,26 @@ tt_status_t tt_comm_init(tt_comm_t* comm, const void* id, int nranks, int rank) 
     }
     c->nranks = nranks;
     c->rank = rank;
-    *comm = reinterpret_cast<tt_comm_t>(c);
+    *comm = reinterpret_cast<tt_comm_t>(publish_handle(c));
     return TT_SUCCESS;
 }
 
 tt_status_t tt_comm_destroy(tt_comm_t comm) {
-    tt_comm_impl* c = as_comm(comm);
-    if (c == nullptr) return TT_INVALID_PARAMETER;
+    if (!retire_handle(comm)) return TT_INVALID_PARAMETER;  // NULL or already destroyed
+    tt_comm_impl* c = reinterpret_cast<tt_comm_impl*>(comm);
     ncclResult_t r = ncclCommDestroy(c->nccl);
-    c->magic = 0;
     delete c;
     return r == ncclSuccess ? TT_SUCCESS : TT_NCCL_ERROR;
 }
 
 tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int ndims, const int64_t* global_dims,
                             const int* perm, size_t elem_size, tt_stream_t stream) {
+    return tt_plan_sharded_ex(plan, comm, ndims, global_dims, perm, elem_size, stream, nullptr);
+}
+
+tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int ndims, const int64_t* global_dims,
+                               const int* perm, size_t elem_size, tt_stream_t stream,
+                               const tt_plan_options_t* opts) {
     if (plan == nullptr) return TT_INVALID_PARAMETER;
     *plan = nullptr;
     tt_comm_impl* c = as_comm(comm);
@@ -456,7 +458,7 @@ tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int ndims, const in
     if (dev.device != c->device) return TT_INVALID_DEVICE;
     Plan* p = nullptr;
     st = build_shard_n(&p, c, c->nranks, rank, ndims, global_dims, perm, elem_size, stream, dev,
-                       &cuda_occupancy);
+                       &cuda_occupancy, false, opts && opts->force_redistribute);
     if (st != TT_SUCCESS) return st;
     ShardInfo* s = p->shard;
     if (s->redistribute) {
@@ -474,7 +476,7 @@ tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int ndims, const in
             return TT_CUDA_ERROR;
         }
     }
-    *plan = reinterpret_cast<tt_plan_t>(p);
+    *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return TT_SUCCESS;
 }
 
@@ -488,7 +490,7 @@ tt_status_t tt_plan_sharded_offline(tt_plan_t* plan, int nranks, int rank, int n
     Plan* p = nullptr;
     tt_status_t st = build_shard_n(&p, nullptr, nranks, rank, ndims, global_dims, perm, elem_size,
                                    nullptr, dev, nullptr);
-    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(p);
+    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
 
@@ -572,6 +574,13 @@ tt_status_t tt_plan_shard_dims(tt_plan_t plan, int64_t* local_in_dims, int64_t* 
 tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int ndims,
                                 const int64_t* global_dims, const int* perm, size_t elem_size,
                                 tt_stream_t stream) {
+    return tt_plan_sharded_p2p_ex(plan, comm, nranks, proc, ndims, global_dims, perm, elem_size, stream,
+                                  nullptr);
+}
+
+tt_status_t tt_plan_sharded_p2p_ex(tt_plan_t* plan, tt_comm_t comm, int nranks, int proc, int ndims,
+                                   const int64_t* global_dims, const int* perm, size_t elem_size,
+                                   tt_stream_t stream, const tt_plan_options_t* opts) {
     if (plan == nullptr || ndims < 1) return TT_INVALID_PARAMETER;
     *plan = nullptr;
     tt_comm_impl* c = nullptr;
@@ -586,7 +595,7 @@ tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int
     if (c && dev.device != c->device) return TT_INVALID_DEVICE;
     Plan* p = nullptr;
     st = build_shard_n(&p, c, nranks, proc, ndims, global_dims, perm, elem_size, stream, dev,
-                       &cuda_occupancy, true);
+                       &cuda_occupancy, true, opts && opts->force_redistribute);
     if (st != TT_SUCCESS) return st;
     ShardInfo* s = p->shard;
     for (auto& e : s->ev) {
@@ -596,7 +605,7 @@ tt_status_t tt_plan_sharded_p2p(tt_plan_t* plan, tt_comm_t comm, int nranks, int
             return TT_CUDA_ERROR;
         }
     }
-    *plan = reinterpret_cast<tt_plan_t>(p);
+    *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return TT_SUCCESS;
 }
 
@@ -611,7 +620,7 @@ tt_status_t tt_plan_sharded_p2p_offline(tt_plan_t* plan, int nranks, int proc, i
     Plan* p = nullptr;
     tt_status_t st = build_shard_n(&p, nullptr, nranks, proc, ndims, global_dims, perm, elem_size,
                                    nullptr, dev, nullptr, true);
-    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(p);
+    if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
 

@@ -13,6 +13,6 @@ const void* pick_tile_sd(int esize, int q, int r, int stages);
 const void* pick_rowcopy(int esize, bool idx64);
 const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64);
 const void* pick_tiled2d_async(int esize, int ta, int tb, int stages);
-const void* pick_tile_vg(int esize, int nreg, int stages);
+const void* pick_tile_vg(int esize, int nreg, int items, int stages);
 
 }  // namespace tt

@@ -2,224 +2,300 @@
 //
 // Citations: P:Lnn = PAPER.md line nn (arXiv 1705.01598).
 //
-// The tile, grid walk and store phase are the generic tile's (Packed /
+// The tile, its grid and its store phase are the generic tile's (Packed /
 // PackedSplit classes; Eqs. 4-6; Algorithm 1,
-// P:L84-103).  What changes is how the input side reaches shared memory.
-// Inside a tile the input is a set of contiguous RUNS: the tile's first vgM
-// dims are the first input dims (M_m of P:L66), so run r -- one coordinate of
-// the remaining tile dims -- is vgL consecutive input elements.  Runs start at
-// arbitrary element offsets, so 4- and 8-byte gathers classically move one
-// element per instruction and per in-flight register (the loads-in-flight
-// limit of section 11 in DESIGN.md).  Here every run is copied as the
-// 16-byte-aligned superset of its bytes: ceil((shift + vgL*E) / 16) chunks
-// of 16 bytes, each one cp.async.cg (LDGSTS.128) into the run's 16-byte-
-// aligned shared-memory slot.  The run's elements then sit `shift` bytes into
-// the slot (shift = the run start's offset inside its 16-byte chunk, which
-// depends on the tile base and the run's offset); the store phase adds it
-// back when it reads the staged tile in output order (Eq. 6) and writes
-// coalesced runs (Eq. 5).  The superset never leaves the run's 32-byte
-// sectors, so DRAM traffic is unchanged; chunks that would cross the ends of
-// the input tensor are copied element by element.  No data registers: S-1
-// tiles are in flight per CTA (an S-stage ring).
+// P:L84-103).  What changes is how the input reaches shared memory and how
+// little work each element costs.
 //
-// Shared memory: S stages of p.sbuf elements, then the run table (uint2 per
-// run: {run offset in elements from the tile base, staging byte offset |
-// validity bits << 24}), built once per CTA.
+// Load phase.  Inside a tile the input is a set of contiguous RUNS: the
+// tile's first vgM dims are the first input dims (M_m of P:L66), so run r --
+// one coordinate of the remaining tile dims -- is vgL consecutive input
+// elements.  Runs start at arbitrary element offsets, so a 4- or 8-byte
+// gather classically moves one element per instruction and per in-flight
+// register.  Here every run is copied as the 16-byte-aligned superset of its
+// bytes: chunk c of run r is one cp.async.cg of 16 bytes (LDGSTS.128) when
+// 16c < shift + run bytes, where shift = the run start's offset inside its
+// 16-byte chunk.  The superset never leaves the run's 32-byte sectors, so
+// DRAM traffic is unchanged.  Chunks of tiles touching the first or last 32
+// bytes of the input are copied element by element (no read outside the
+// tensor).  No data registers: S-1 tiles are in flight per CTA.
+//
+// Shift folding.  shift_r = (sh + q_r) mod 16 with sh = the tile base's
+// offset inside its chunk and q_r = the run offset's (both multiples of E).
+// The load places chunk 0 of run r at slot_r + 16 w_r, w_r = [sh + q_r >= 16]
+// (equivalently shift_r < q_r), so element i of run r is ALWAYS at
+// slot_r + q_r + i*E + sh: the store phase adds one per-tile constant.
+//
+// Per-element cost.  Each thread owns K fixed (run, chunk) load items and
+// NREG fixed output-order store slots (tables computed once); the tile bases
+// (Algorithm 1) are decoded 32 tiles at a time by one warp into a shared
+// ring, so a tile costs every warp one 16-byte shared load.  A store slot is
+// LDS + IMAD.WIDE + STG + one add; ragged tiles predicate the STG
+// per slot instead of branching.
+//
+// Shared memory: S stages of p.sbuf elements, then the tile-base ring (64 x
+// uint4: input offset, output offset, ragged state | interior << 2).
 #include "kern_common.cuh"
 #include "kern_pick.h"
 
 namespace tt {
 
-template <typename W, int NREG, int S>
-__global__ void __launch_bounds__(NREG >= 16 ? 256 : 1024, NREG >= 16 ? 2 : 1)
+__device__ __forceinline__ void stg_pred(uint32_t* p, uint32_t v, bool ok) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.global.b32 [%0], %1; }" ::"l"(p), "r"(v),
+                 "r"((uint32_t)ok)
+                 : "memory");
+}
+__device__ __forceinline__ void stg_pred(uint64_t* p, uint64_t v, bool ok) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.global.b64 [%0], %1; }" ::"l"(p), "l"(v),
+                 "r"((uint32_t)ok)
+                 : "memory");
+}
+// cache flavour of the 16-byte chunk copies (p.vgPolicy, calibration):
+// 0 = .cg (L2 only), 1 = .ca (L1 and L2), 2 = .cg with an L2 evict_last hint,
+// 3 = .cg with an L2 evict_normal hint
+template <int POL>
+__device__ __forceinline__ void cp_async16_pred(uint32_t saddr, const void* g, bool ok, uint64_t pol) {
+    if constexpr (POL == 0)
+        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(saddr),
+                     "l"(g), "r"((uint32_t)ok));
+    else if constexpr (POL == 1)
+        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.ca.shared.global [%0], [%1], 16; }" ::"r"(saddr),
+                     "l"(g), "r"((uint32_t)ok));
+    else
+        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3; }"
+                     ::"r"(saddr), "l"(g), "r"((uint32_t)ok), "l"(pol));
+}
+
+// Tile-base entry of one tile (Algorithm 1 over the grid dims, one lane):
+// x = input offset, y = output offset, z = ragged state (2 bits) | interior
+// (the tile's 16-byte chunks stay >= 32 bytes inside the input) << 2.
+__device__ __forceinline__ uint4 vg_tile_entry(const TileParams& p, uint32_t t) {
+    uint32_t vin = 0, vout = 0, need = 0;
+    for (int g = 0; g < p.h; ++g) {
+        const uint32_t q1 = fast_div(t, p.gMC[g], p.gLC[g]);
+        const uint32_t x = q1 - fast_div(q1, p.gMD[g], p.gLD[g]) * (uint32_t)p.gD[g];
+        vin += x * (uint32_t)p.gSin[g];
+        vout += x * (uint32_t)p.gSout[g];
+        if (x == (uint32_t)p.gD[g] - 1) {
+            if (p.nSplit > 0 && g == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) need |= 1u;
+            if (p.nSplit > 1 && g == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]) need |= 2u;
+        }
+    }
+    const int64_t lo = (int64_t)vin * p.vgE;
+    const int64_t hi = ((int64_t)vin + p.vgSpanIn) * p.vgE;
+    const uint32_t interior = (lo >= 32 && hi + 32 <= p.vgInBytes) ? 4u : 0u;
+    return make_uint4(vin, vout, need | interior, 0u);
+}
+
+template <typename W, int NREG, int K, int S>
+__global__ void __launch_bounds__(NREG >= 16 ? 512 : 1024, 1)
 tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
+    constexpr uint32_t E = sizeof(W);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sbytes = (uint32_t)p.sbuf * (uint32_t)sizeof(W);
+    const uint32_t sbytes = (uint32_t)p.sbuf * E;
+    uint4* const ring = reinterpret_cast<uint4*>(smem_raw + p.vgTab);
     const int tid = threadIdx.x;
     const int NT = blockDim.x;
-    const int lane = tid & 31;
     const int M = p.vgM;
-    const int NR = p.vgNR;
-    uint2* const tab = reinterpret_cast<uint2*>(smem_raw + p.vgTab);
+    const uint32_t nch = (uint32_t)p.vgNch;
 
-    // run table: offset (Eq. 4 over the non-run tile dims) and staging slot
-    // (Eq. 6 with the padded strides) of every run; validity per ragged state
-    for (int r = tid; r < NR; r += NT) {
-        int rem = r;
-        uint32_t off = 0, smb = 0, bad = 0;
-        for (int t = M; t < p.a; ++t) {
-            const int c = rem % p.tExt[t];
-            rem /= p.tExt[t];
-            off += (uint32_t)c * (uint32_t)p.tSin[t];
-            smb += (uint32_t)c * (uint32_t)p.tSm[t];
-            if (p.nSplit > 0 && t == p.splitTile[0] && c >= p.splitTail[0]) bad |= 1u;
-            if (p.nSplit > 1 && t == p.splitTile[1] && c >= p.splitTail[1]) bad |= 2u;
+    // --- load items: item k = (run r, chunk c), u = tid + k*NT -----------------
+    // roff = run offset in bytes from the tile base (Eq. 4 over the non-run
+    // dims); pk = slot byte offset + 16c (bits 0-17) | validity in the four
+    // ragged states (18-21) | q_r / 4 (22-23) | c (24-31)
+    uint32_t roff[K], pk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        roff[k] = 0;
+        pk[k] = 0;
+        const uint32_t u = (uint32_t)tid + (uint32_t)k * (uint32_t)NT;
+        if (u < (uint32_t)p.vgNR * nch) {
+            const uint32_t r = u / nch, c = u - r * nch;
+            uint32_t rem = r, off = 0, smb = 0, bad = 0;
+            for (int t = M; t < p.a; ++t) {
+                const uint32_t x = rem % (uint32_t)p.tExt[t];
+                rem /= (uint32_t)p.tExt[t];
+                off += x * (uint32_t)p.tSin[t];
+                smb += x * (uint32_t)p.tSm[t];
+                if (p.nSplit > 0 && t == p.splitTile[0] && x >= (uint32_t)p.splitTail[0]) bad |= 1u;
+                if (p.nSplit > 1 && t == p.splitTile[1] && x >= (uint32_t)p.splitTail[1]) bad |= 2u;
+            }
+            uint32_t valid = 0;
+            for (uint32_t n = 0; n < 4; ++n)
+                if ((bad & n) == 0) valid |= 1u << n;
+            roff[k] = off * E;
+            pk[k] = (smb * E + 16u * c) | (valid << 18) | ((((off * E) & 15u) >> 2) << 22) | (c << 24);
         }
-        uint32_t valid = 0;
-        for (uint32_t n = 0; n < 4; ++n)
-            if ((bad & n) == 0) valid |= 1u << n;
-        tab[r] = make_uint2(off, smb * (uint32_t)sizeof(W) | (valid << 24));
     }
 
-    // store-phase slot tables: element k' = tid + r*NT in tile-output order;
-    // gout = Eq. (5) offset, spk = staging byte offset (run slot + in-run
-    // index) | run offset mod 16 bytes << 24, validity bits as build_slots
+    // --- store slots: element k' = tid + r*NT in tile-output order ---------------
+    // gout = Eq. (5) offset; spk = slot_r + q_r + in-run index * E (Eq. 6 with
+    // the run layout and the folded shift); m<n> = slots valid in state n
     uint32_t gout[NREG], spk[NREG];
-    uint32_t fl = 0;  // 2 bits per slot: element inside the ragged chunk of split 0 / 1
-    const int nmine = (p.V > tid) ? min(NREG, (p.V - tid + NT - 1) / NT) : 0;
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
 #pragma unroll
     for (int r = 0; r < NREG; ++r) {
         gout[r] = 0;
         spk[r] = 0;
-        if (r < nmine) {
-            int rem = tid + r * NT;
-            uint32_t go = 0, inrun = 0, smb = 0, roff = 0, f = 0;
+        const int kk = tid + r * NT;
+        if (kk < p.V) {
+            int rem = kk;
+            uint32_t go = 0, inrun = 0, smb = 0, ro = 0, f = 0;
             for (int jj = 0; jj < p.a; ++jj) {
                 const int t = p.tOutOrder[jj];
-                const int c = rem % p.tExt[t];
+                const uint32_t x = (uint32_t)(rem % p.tExt[t]);
                 rem /= p.tExt[t];
-                go += (uint32_t)c * (uint32_t)p.tSout[t];
+                go += x * (uint32_t)p.tSout[t];
                 if (t < M) {
-                    inrun += (uint32_t)c * (uint32_t)p.tCin[t];
+                    inrun += x * (uint32_t)p.tCin[t];
                 } else {
-                    smb += (uint32_t)c * (uint32_t)p.tSm[t];
-                    roff += (uint32_t)c * (uint32_t)p.tSin[t];
+                    smb += x * (uint32_t)p.tSm[t];
+                    ro += x * (uint32_t)p.tSin[t];
                 }
-                if (p.nSplit > 0 && t == p.splitTile[0] && c < p.splitTail[0]) f |= 1u;
-                if (p.nSplit > 1 && t == p.splitTile[1] && c < p.splitTail[1]) f |= 2u;
+                if (p.nSplit > 0 && t == p.splitTile[0] && x < (uint32_t)p.splitTail[0]) f |= 1u;
+                if (p.nSplit > 1 && t == p.splitTile[1] && x < (uint32_t)p.splitTail[1]) f |= 2u;
             }
             gout[r] = go;
-            spk[r] = (smb + inrun) * (uint32_t)sizeof(W) | (((roff * (uint32_t)sizeof(W)) & 15u) << 24);
-            fl |= f << (2 * r);
+            spk[r] = (smb + inrun) * E + ((ro * E) & 15u);
+            m0 |= 1u << r;
+            if (f & 1u) m1 |= 1u << r;
+            if (f & 2u) m2 |= 1u << r;
+            if ((f & 3u) == 3u) m3 |= 1u << r;
         }
     }
-    uint32_t smask = 0;  // bit n*NREG + r: slot r valid when the tile's need is n
-#pragma unroll
-    for (int r = 0; r < NREG; ++r) {
-        if (r >= nmine) continue;
-        const uint32_t f = (fl >> (2 * r)) & 3u;
-#pragma unroll
-        for (uint32_t n = 0; n < 4; ++n)
-            if ((f & n) == n && n * NREG + r < 32) smask |= 1u << (n * NREG + r);
-    }
-    // NREG == 16: states 2 and 3 do not fit the 32-bit mask; keep them apart
-    uint32_t smaskHi = 0;
-    if constexpr (NREG == 16) {
-#pragma unroll
-        for (int r = 0; r < NREG; ++r) {
-            if (r >= nmine) continue;
-            const uint32_t f = (fl >> (2 * r)) & 3u;
-            if ((f & 2u) == 2u) smaskHi |= 1u << r;
-            if ((f & 3u) == 3u) smaskHi |= 1u << (16 + r);
-        }
-    }
-    __syncthreads();  // run table visible
+    const uint32_t full = (1u << NREG) - 1u;
 
     const uint32_t nTiles = (uint32_t)p.nTiles;
     const uint32_t G = (uint32_t)gridDim.x;
     const uint32_t t0 = (uint32_t)blockIdx.x;
     if (t0 >= nTiles) return;
-    GridWalker<uint32_t> walk(p, lane);
+    const uint32_t nIt = (nTiles - t0 + G - 1) / G;  // tiles of this CTA: t0 + it*G
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {  // tile bases of iterations 0..63
+        for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32)
+            ring[it] = vg_tile_entry(p, t0 + it * G);
+    }
+    __syncthreads();
 
-    const int Gl = p.vgG;                 // lanes per run group
-    const int grp = tid / Gl, lg = tid % Gl, nGrp = NT / Gl;
-    const char* const inLo = reinterpret_cast<const char*>(in);
-    const char* const inHi = inLo + p.vgInBytes;
+    const char* const inB = reinterpret_cast<const char*>(in);
+    const uint32_t LB = (uint32_t)p.vgL * E, LtB = (uint32_t)p.vgLtail * E;
+    const uint32_t runBit = (uint32_t)p.vgRunBit;
+    const int pol = p.vgPolicy;
+    uint64_t l2pol = 0;
+    if (pol == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
+    if (pol == 3) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(l2pol));
 
-    // load phase of tile t into the stage at byte address sb
-    auto issue = [&](uint32_t t, uint32_t sb) {
-        const TileBase<uint32_t> tb = walk.seek(t);
-        const uint32_t nd = tb.need;
-        const uint32_t Lb = ((p.vgRunBit & nd) ? (uint32_t)p.vgLtail : (uint32_t)p.vgL) * (uint32_t)sizeof(W);
-        const W* const base = in + tb.in;
-        for (int r = grp; r < NR; r += nGrp) {
-            const uint2 e = tab[r];
-            if (!((e.y >> (24 + nd)) & 1u)) continue;
-            const uintptr_t ga = reinterpret_cast<uintptr_t>(base + e.x);
-            const char* const g0 = reinterpret_cast<const char*>(ga & ~(uintptr_t)15);
-            const uint32_t nch = ((uint32_t)(ga & 15u) + Lb + 15u) >> 4;
-            const uint32_t dst = sb + (e.y & 0xffffffu);
-            for (uint32_t c = (uint32_t)lg; c < nch; c += (uint32_t)Gl) {
-                const char* const src = g0 + 16u * c;
-                if (src >= inLo && src + 16 <= inHi) {
-                    cp_async<16>(dst + 16u * c, src);
-                } else {  // a chunk crossing an end of the input tensor
+    auto issue = [&](uint32_t it, uint32_t sb) {
+        const uint4 e = ring[it & 63u];
+        const uint32_t nd = e.z & 3u;
+        const uint32_t Lb = (runBit & nd) ? LtB : LB;
+        const char* const tb = inB + (size_t)e.x * E;
+        const uint32_t vs = 18u + nd;
+        if (e.z & 4u) {
+            auto items = [&](auto polc) {
+                constexpr int POL = decltype(polc)::value;
 #pragma unroll
-                    for (uint32_t k = 0; k < 16u / sizeof(W); ++k) {
-                        const char* const s1 = src + k * sizeof(W);
-                        if (s1 >= inLo && s1 < inHi) cp_async<sizeof(W)>(dst + 16u * c + k * sizeof(W), s1);
-                    }
+                for (int k = 0; k < K; ++k) {
+                    const char* a = tb + roff[k];
+                    const uint32_t s = (uint32_t)reinterpret_cast<uintptr_t>(a) & 15u;
+                    const uint32_t c16 = (pk[k] >> 20) & 0xff0u;
+                    const uint32_t q = ((pk[k] >> 22) & 3u) << 2;
+                    const bool ok = ((pk[k] >> vs) & 1u) && c16 < s + Lb;
+                    const uint32_t dst = sb + (pk[k] & 0x3ffffu) + (s < q ? 16u : 0u);
+                    cp_async16_pred<POL>(dst, a - s + c16, ok, l2pol);
+                }
+            };
+            switch (pol) {
+                case 1: items(std::integral_constant<int, 1>()); break;
+                case 2: case 3: items(std::integral_constant<int, 2>()); break;
+                default: items(std::integral_constant<int, 0>()); break;
+            }
+        } else {  // near an end of the input: element-wise inside the tensor
+            const char* const lo = inB;
+            const char* const hi = inB + p.vgInBytes;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const char* a = tb + roff[k];
+                const uint32_t s = (uint32_t)reinterpret_cast<uintptr_t>(a) & 15u;
+                const uint32_t c16 = (pk[k] >> 20) & 0xff0u;
+                const uint32_t q = ((pk[k] >> 22) & 3u) << 2;
+                if (!(((pk[k] >> vs) & 1u) && c16 < s + Lb)) continue;
+                const uint32_t dst = sb + (pk[k] & 0x3ffffu) + (s < q ? 16u : 0u);
+                const char* src = a - s + c16;
+                if (src >= lo && src + 16 <= hi) {
+                    cp_async<16>(dst, src);
+                } else {
+#pragma unroll
+                    for (uint32_t j = 0; j < 16u / E; ++j)
+                        if (src + j * E >= lo && src + j * E < hi) cp_async<E>(dst + j * E, src + j * E);
                 }
             }
         }
     };
+
 #pragma unroll
     for (int s = 0; s < S - 1; ++s) {
-        const uint32_t t = t0 + (uint32_t)s * G;
-        if (t < nTiles) issue(t, sm0 + (uint32_t)s * sbytes);
+        if ((uint32_t)s < nIt) issue((uint32_t)s, sm0 + (uint32_t)s * sbytes);
         cp_async_commit();
     }
-    const bool allSlots = p.V == NT * NREG;
-    uint32_t k = 0;
-    for (uint32_t t = t0; t < nTiles; t += G) {
+    uint32_t stage = 0;
+    for (uint32_t it = 0; it < nIt; ++it) {
         cp_async_wait<S - 2>();
         __syncthreads();
+        if ((it & 31u) == 0 && it > 0 && warp == 0) {  // next 32 tile bases, other half of the ring
+            const uint32_t j = it + 32u + (uint32_t)lane;
+            if (j < nIt) ring[j & 63u] = vg_tile_entry(p, t0 + j * G);
+        }
         {  // refill the stage read in the previous iteration
-            const uint32_t tn = t + (uint32_t)(S - 1) * G;
-            const uint32_t kn = (k + S - 1) % S;
-            if (tn < nTiles) issue(tn, sm0 + kn * sbytes);
+            const uint32_t itn = it + (uint32_t)(S - 1);
+            const uint32_t sn = (stage == 0) ? (uint32_t)(S - 1) : stage - 1;
+            if (itn < nIt) issue(itn, sm0 + sn * sbytes);
             cp_async_commit();
         }
-        const TileBase<uint32_t> now = walk.seek(t);
-        const uint32_t sb = sm0 + k * sbytes;
-        // byte offset of the tile base inside its 16-byte chunk
-        const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(in + now.in) & 15u);
-        W* __restrict__ dst = opaque(out + now.out);
-        uint32_t m;
-        if constexpr (NREG == 16) {
-            m = now.need == 0 ? (smask & 0xffffu) : now.need == 1 ? (smask >> 16)
-                : now.need == 2 ? (smaskHi & 0xffffu) : (smaskHi >> 16);
-        } else {
-            m = (smask >> (now.need * NREG)) & ((1u << NREG) - 1u);
-        }
-        if (now.need == 0 && allSlots) {
+        const uint4 e = ring[it & 63u];
+        const uint32_t nd = e.z & 3u;
+        const uint32_t sbsh = sm0 + stage * sbytes +
+                              ((uint32_t)reinterpret_cast<uintptr_t>(inB + (size_t)e.x * E) & 15u);
+        W* const dst = out + e.y;
+        const uint32_t m = nd == 0 ? m0 : nd == 1 ? m1 : nd == 2 ? m2 : m3;
+        if (m == full) {
 #pragma unroll
-            for (int r = 0; r < NREG; ++r) {
-                const uint32_t a = sb + (spk[r] & 0xffffffu) + ((sh + (spk[r] >> 24)) & 15u);
-                stg_(elem_addr(dst, gout[r]), lds<W>(a));
-            }
+            for (int r = 0; r < NREG; ++r) stg_(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]));
         } else {
 #pragma unroll
             for (int r = 0; r < NREG; ++r)
-                if (m & (1u << r)) {
-                    const uint32_t a = sb + (spk[r] & 0xffffffu) + ((sh + (spk[r] >> 24)) & 15u);
-                    stg_(elem_addr(dst, gout[r]), lds<W>(a));
-                }
+                stg_pred(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]), (m >> r) & 1u);
         }
-        k = (k + 1 == (uint32_t)S) ? 0u : k + 1;
+        stage = (stage + 1 == (uint32_t)S) ? 0u : stage + 1;
     }
     cp_async_wait<0>();
 }
 
-// vector-gather tile: 4/8-byte words, 4/8/16 slots, 3 or 4 stages, 32-bit indices
-const void* pick_tile_vg(int esize, int nreg, int stages) {
-#define TT_PICKVG(W, S)                                                      \
-    switch (nreg) {                                                          \
-        case 4: return (const void*)&tile_vg_kernel<W, 4, S>;               \
-        case 8: return (const void*)&tile_vg_kernel<W, 8, S>;               \
-        case 16: return (const void*)&tile_vg_kernel<W, 16, S>;             \
-        default: return nullptr;                                             \
+// vector-gather tile: 4/8-byte words, NREG store slots in {4, 8, 16}, K load
+// items in {2, 4}, 3 or 4 stages, 32-bit indices
+const void* pick_tile_vg(int esize, int nreg, int items, int stages) {
+#define TT_VG_K(W, R, S)                                                        \
+    if (items <= 2) return (const void*)&tile_vg_kernel<W, R, 2, S>;          \
+    if (items <= 4) return (const void*)&tile_vg_kernel<W, R, 4, S>;          \
+    return nullptr;
+#define TT_VG_R(W, S)                       \
+    switch (nreg) {                         \
+        case 4: { TT_VG_K(W, 4, S) }        \
+        case 8: { TT_VG_K(W, 8, S) }        \
+        case 16: { TT_VG_K(W, 16, S) }      \
+        default: return nullptr;            \
     }
     if (esize == 4) {
-        if (stages == 3) { TT_PICKVG(uint32_t, 3) }
-        if (stages == 4) { TT_PICKVG(uint32_t, 4) }
+        if (stages == 3) { TT_VG_R(uint32_t, 3) }
+        if (stages == 4) { TT_VG_R(uint32_t, 4) }
     } else if (esize == 8) {
-        if (stages == 3) { TT_PICKVG(uint64_t, 3) }
-        if (stages == 4) { TT_PICKVG(uint64_t, 4) }
+        if (stages == 3) { TT_VG_R(uint64_t, 3) }
+        if (stages == 4) { TT_VG_R(uint64_t, 4) }
     }
     return nullptr;
-#undef TT_PICKVG
+#undef TT_VG_R
+#undef TT_VG_K
 }
 
 }  // namespace tt

@@ -217,11 +217,16 @@ constexpr double kTileLatUs = 1.5;        // per tile iteration of one CTA: load
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Calibration knobs (tools/ experiments only; unset = the defaults below).
-static double knob(const char* name, double dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atof(v) : dflt;
-}
+// Thresholds found by same-box A/B on the suites; the
+// calibration sweeps that set them are in tools/ and profiles/round1_*.
+namespace rule {
+constexpr double kRowMinBytes = 512;      // row copy: rows of un-widened words (profiles/round1_ab_rowmin.txt)
+constexpr double kRowMinBytesWide = 4096; // row copy: rows of widened words
+constexpr double kT2dFill = 0.6;          // 2-D kernel: overall tile fill
+constexpr double kT2dFillB4 = 0.9;        // 2-D kernel: output-side fill, 4-byte words (round1_ab_fillb.txt)
+constexpr double kT2dFillB8 = 0.8;        // ... 8-byte words
+constexpr int kSdRuleVmax = 8192;         // larger slot-dim tiles under the output-run rule (round1_knob_ab_sd_rule.txt)
+}  // namespace rule
 
 // Hacker's Delight unsigned division by invariant integers: l = ceil(log2 d),
 // m = floor(2^32 (2^l - d) / d) + 1; the 33-bit sum umulhi(n, m) + n cannot
@@ -408,9 +413,7 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
     };
     double bestFill = 0;
     TileParams bestTp = tp;
-    const int cfgMask = (int)knob(esize >= 8 ? "TT_KNOB_SD_CFG8" : "TT_KNOB_SD_CFG4", 7);
     for (int cfg = 0; cfg < 3; ++cfg) {
-        if (!(cfgMask & (1 << cfg))) continue;
         const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
         const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
         const Pick L = pick_slot(0, RM), S = pick_slot(1, RM);
@@ -481,19 +484,6 @@ static void tile_need(const Problem& pr, int64_t Tin, int64_t Tout, int64_t* nee
             }
             need[i] = pr.d[i];
             P *= pr.d[i];
-        }
-    }
-    // Balanced chunks: a split dim cut into k chunks of `need` with a short
-    // tail keeps k chunks but leaves slots idle in every ragged tile (5 in
-    // chunks of 3, 4 in chunks of 3); when the chunks fill less than
-    // TT_KNOB_SPLIT_BAL of k * need, use k equal chunks instead.
-    {
-        const double bal = knob("TT_KNOB_SPLIT_BAL", 0.0);
-        for (int i = 0; i < n; ++i) {
-            if (need[i] > 1 && need[i] < pr.d[i]) {
-                const int64_t k = ceil_div(pr.d[i], need[i]);
-                if ((double)pr.d[i] / ((double)k * need[i]) < bal) need[i] = ceil_div(pr.d[i], k);
-            }
         }
     }
 }
@@ -638,8 +628,7 @@ static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSp
                                             slots * slotInstr * (E / 4.0 > 1 ? 1.25 : 1.0));
             const double t_issue = (double)tp.nTiles * perTile / model::kIssuePerClk /
                                    std::max(1, dev.num_sms) / model::kClockMHz;
-            static const double tileLat = knob("TT_KNOB_TILE_LAT", model::kTileLatUs);
-            const double t_lat = std::ceil((double)tp.nTiles / ((double)dev.num_sms * occ)) * tileLat;
+            const double t_lat = std::ceil((double)tp.nTiles / ((double)dev.num_sms * occ)) * model::kTileLatUs;
             const double top = std::max(std::max(t_mem, t_issue), t_lat);
             return top + 0.25 * (t_mem + t_issue + t_lat - top) + model::kLaunchUs;
         };
@@ -788,11 +777,13 @@ static void choose_smem(TileParams& tp, int esize) {
 // Vector-gather layout (kernels_vg.cu tile_vg_kernel) of a chosen generic
 // tile: the run dims (the tile's first dims that are dense in the input),
 // a run slot of 16-byte chunks holding the 16-byte-aligned superset of a run
-// (worst-case shift 16/E - 1 elements), padded slot strides for the other
-// tile dims (multiples of 16 bytes so every slot stays 16-byte aligned),
-// chosen on the transposed read's bank-conflict cost, and the run
-// table behind the S staging buffers.  False when the runs are shorter than
-// `minRunBytes` or the footprint exceeds `maxSmem`.
+// (worst-case shift 16 - E bytes) plus 16 bytes for the folded shift, padded
+// slot strides for the other tile dims (multiples of 16 bytes so every slot
+// stays 16-byte aligned), chosen on the transposed read's bank-conflict cost
+// (P:L225), and the tile-base ring behind the S staging buffers.  Launch
+// shape: NT threads x NREG store slots cover the tile; every thread owns
+// K <= 4 (run, chunk) load items.  False when the runs are shorter than
+// `minRunBytes`, a run needs more than 255 chunks, or it does not fit.
 static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int minRunBytes,
                      int& threads, int& nreg, int& smem) {
     const int E = pr.esize;
@@ -802,6 +793,8 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
     int64_t L = 1;
     while (M < tp.a && tp.tSin[M] == L) L *= tp.tExt[M++];
     if (M == 0 || L * E < minRunBytes || M == tp.a) return false;  // M == a: a plain copy
+    const int64_t nch = (L * E + 16 - E + 15) / 16;  // chunks at the worst shift
+    if (nch > 255) return false;
     tp.vgM = M;
     tp.vgL = (int32_t)L;
     tp.vgLtail = (int32_t)L;
@@ -812,24 +805,26 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
             tp.vgLtail = (int32_t)(L / tp.tExt[M - 1] * tp.splitTail[s]);
         }
     tp.vgNR = (int32_t)(tp.V / L);
-    const int64_t nch = (L + VPC - 1 + VPC - 1) / VPC;  // 16-byte chunks of a run at worst shift
-    int g = 1;
-    while (g < 32 && g < nch) g *= 2;
-    tp.vgG = g;
+    tp.vgNch = (int32_t)nch;
+    tp.vgE = E;
+    int64_t span = 0;
+    for (int t = 0; t < tp.a; ++t) span += (int64_t)(tp.tExt[t] - 1) * tp.tSin[t];
+    tp.vgSpanIn = span + 1;
     // slot strides: tile dims < M dense (the run), the rest padded
     int32_t pad[kMaxDims] = {};
     int32_t sm[kMaxDims];
+    const int64_t pitch = (nch + 1) * VPC;  // elements
     auto strides = [&]() -> int64_t {
         int64_t acc = 1;
         for (int t = 0; t < tp.a; ++t) {
-            if (t == M) acc = nch * VPC;
+            if (t == M) acc = pitch;
             acc += pad[t];
             sm[t] = (int32_t)acc;
             acc *= tp.tExt[t];
         }
         int64_t last = 0;
         for (int t = M; t < tp.a; ++t) last += (int64_t)(tp.tExt[t] - 1) * sm[t];
-        return last + nch * VPC;
+        return last + pitch;
     };
     const SmemSample sample = smem_sample(tp, 2);  // the transposed read only
     strides();
@@ -850,17 +845,21 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
     tp.sbuf = (int32_t)((foot + VPC - 1) / VPC * VPC);
     tp.vgTab = S * tp.sbuf * E;
     tp.vgInBytes = pr.span * E;
-    smem = tp.vgTab + 8 * tp.vgNR;
-    if (smem > maxSmem || (int64_t)(foot + 8) * E >= (int64_t(1) << 24)) return false;
-    // store phase: NT threads x NREG slots cover the tile
+    smem = tp.vgTab + 64 * 16;
+    if (smem > maxSmem || (int64_t)tp.sbuf * E >= (int64_t(1) << 18)) return false;
+    // store phase: NT threads x NREG slots cover the tile; load items <= 4
     threads = 0;
-    for (int R : {8, 4, 16}) {
+    const int64_t items = (int64_t)tp.vgNR * nch;
+    for (int R : {8, 16, 4}) {
         int T = (int)((tp.V + R - 1) / R);
         T = (T + 31) / 32 * 32;
         if (T < 64) T = 64;
-        if (T > (R >= 16 ? 256 : 1024)) continue;  // kernels_vg.cu launch bounds
+        if (T > (R >= 16 ? 512 : 1024)) continue;  // kernels_vg.cu launch bounds
+        const int64_t K = (items + T - 1) / T;
+        if (K > 4) continue;
         threads = T;
         nreg = R;
+        tp.vgK = K <= 2 ? 2 : 4;
         break;
     }
     return threads > 0;
@@ -884,7 +883,7 @@ static bool tiled2d_tile_ok(int esize, int vec, int ta, int tb) {
 }
 
 static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta, int& tb,
-                          double& fill, int wantA, int wantB, int order) {
+                          double& fill, int wantA, int wantB, int order, int vec2) {
     if (pr.n < 2 || pr.p[0] == 0) return false;
     const int B = pr.p[0];
     // the kernels index in[b*sInB + a] and out[a*sOutA + b]: unit strides
@@ -907,8 +906,8 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     } else if (vec_ok(2)) {
         vec = 2;
     }
-    // 2-element vectors vs the scalar kernel (knobs TT_KNOB_T2D_VEC2 /
-    // TT_KNOB_T2D_VEC8: 1 = always vectors, 0 = always scalar).
+    // 2-element vectors vs the scalar kernel (option t2d_vec2: 1 = always
+    // vectors when the extents allow them, -1 = always scalar, 0 = the rule).
     //
     // Defaults from the same-box A/B (tools/vec2_ab.py,
     // profiles/round1_vec2_ab.jsonl): for 4-byte words the scalar kernel beat
@@ -918,10 +917,8 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     // full.
     {
         const double fill64 = (double)dA / (64.0 * ceil_div(dA, 64)) * (double)dB / (64.0 * ceil_div(dB, 64));
-        if (pr.esize == 4 && vec == 2 && knob("TT_KNOB_T2D_VEC2", 0) == 0) vec = 0;
-        if (pr.esize == 8 && vec == 2 &&
-            (knob("TT_KNOB_T2D_VEC8", -1) == 0 || (knob("TT_KNOB_T2D_VEC8", -1) < 0 && fill64 < 0.95)))
-            vec = 0;
+        if (pr.esize == 4 && vec == 2 && vec2 <= 0) vec = 0;
+        if (pr.esize == 8 && vec == 2 && (vec2 < 0 || (vec2 == 0 && fill64 < 0.95))) vec = 0;
     }
     if (vec == 0) vec = 1;  // scalar 2-D kernel (padded staging)
     // default tiles from the B200 calibration sweep (tools/sweep.py t2d,
@@ -1034,7 +1031,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // (several elements per word) the generic tile beat the row copy on 12
     // of 13 cases below 4 KB rows (up to 1.39x, one loss of 0.95x); for
     // un-widened rows it lost on 7 of 8, so those keep 512 B.
-    const double rowMin = pr.widen > 1 ? knob("TT_KNOB_ROW_MIN_W", 4096) : knob("TT_KNOB_ROW_MIN", 512);
+    const double rowMin = pr.widen > 1 ? rule::kRowMinBytesWide : rule::kRowMinBytes;
     if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
     if (!acc && rowClass && (forced == TT_KERNEL_ROWCOPY ||
                      (forced == TT_KERNEL_AUTO && pr.d[0] * E >= rowMin &&
@@ -1105,7 +1102,8 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const bool can2d = !acc && build_tiled2d(pr, plan.t2d, vec2d, ta2d, tb2d, fill2d,
                                      force2d && opts ? opts->run_in : 0,
                                      force2d && opts ? opts->run_out : 0,
-                                     opts && opts->grid_order ? opts->grid_order : 2);
+                                     opts && opts->grid_order ? opts->grid_order : 2,
+                                     opts ? opts->t2d_vec2 : 0);
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
     // fill of the output-fastest (B) side alone: short B extents leave the
     // 2-D kernel short write runs and half-empty tiles
@@ -1113,7 +1111,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // profiles/round1_ab_fillb.txt): below these fills the generic tile won
     // (up to 1.5x); 8-byte words lost above 0.8.
     const double fillB2d = can2d ? (double)pr.d[pr.p[0]] / ((double)tb2d * ceil_div(pr.d[pr.p[0]], tb2d)) : 0.0;
-    const double fillBMin = knob(E == 4 ? "TT_KNOB_T2D_FILLB4" : "TT_KNOB_T2D_FILLB8", E == 4 ? 0.9 : 0.8);
+    const double fillBMin = E == 4 ? rule::kT2dFillB4 : rule::kT2dFillB8;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
     // 512 threads x 8 slots, and staging byte offsets < 2^16 (16-bit packing)
@@ -1126,20 +1124,20 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3 && sdOpt <= 0) &&
                            (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                            !(opts && (opts->threads || opts->slots));
-    // The slot-dim shape inside the tile model (TT_KNOB_SD_VMAX > 0, tiles up
+    // The slot-dim shape inside the tile model (option sd_vmax > 0, tiles up
     // to 8192 elements) and whole-dimension run targets are off by default:
     // on the suites they won and lost by up to 2.4x case by case with equal
     // medians (tools/knob_sweep.sh); the model cannot rank them.  By default
     // the slot-dim map is applied after the classic tile choice, by real
     // occupancy (below), which measured no losses.
-    const int sdVmaxReq = opts && opts->sd_vmax ? opts->sd_vmax : (int)knob("TT_KNOB_SD_VMAX", 0);
+    const int sdVmaxReq = opts && opts->sd_vmax ? opts->sd_vmax : 0;
     const int VmaxSd = sdAllowed ? std::min<int>(E == 4 ? 8192 : 6144, sdVmaxReq) : 0;
     // Larger slot-dim tiles (up to 8192 elements) under the same output-run
-    // rule as the prefix targets (TT_KNOB_SD_RULE: 0 off, else the tile
+    // rule as the prefix targets (rule::kSdRuleVmax, the tile
     // limit).  Same-box A/B on the suites (profiles/round1_knob_ab_sd_rule.txt):
     // 17 cases changed, median 1.016x, up to 1.28x, one loss of 0.88x; Set 2
     // median 0.796 -> 0.803 of memcpy.
-    const int sdRule = (int)knob("TT_KNOB_SD_RULE", 8192);
+    const int sdRule = rule::kSdRuleVmax;
     const int VmaxSdRule = (sdAllowed && VmaxSd == 0 && sdRule > 0) ? std::min(E == 4 ? 8192 : 6144, sdRule) : 0;
     std::vector<int64_t> targets;
     for (int64_t b : {64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384})
@@ -1154,8 +1152,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // it AND its output run is at least as long (and its input run not below
     // half, unless the output run at least doubles).
     std::vector<int64_t> prefix;
-    const int prefixKnob = (int)knob("TT_KNOB_PREFIX_TARGETS", -1);  // -1 default rule, 0 off, 1 free
-    if (prefixKnob != 0) {
+    {
         int64_t P = 1;
         for (int i = 0; i < pr.n && P * pr.d[i] <= std::max(Vmax, VmaxSd); ++i) {
             P *= pr.d[i];
@@ -1196,7 +1193,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         search(all, all, px);
         const bool keepsOut = best.ok && px.ok && px.runOut >= best.runOut &&
                               (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
-        if (px.ok && (!best.ok || (px.cost_us < best.cost_us && (prefixKnob == 1 || keepsOut))))
+        if (px.ok && (!best.ok || (px.cost_us < best.cost_us && keepsOut)))
             best = px;
     }
     if (VmaxSdRule > 0 && !(opts && (opts->run_in || opts->run_out)) && best.ok) {
@@ -1294,11 +1291,10 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // slot-dim map with a cp.async ring of S stages (tile_sd_async_kernel):
     // S-1 tiles in flight per CTA without data registers.  Experimental,
     // options slot_dims > 0 with stages 3 or 4 (measured planning), or
-    // TT_KNOB_SD_STAGES; off by default (suites: mixed, up to 1.18x faster
+    // off by default (suites: mixed, up to 1.18x faster
     // and 1.3x slower case by case, profiles/round1_ab_sd_async.txt).
     if (kc.sdq && !acc && !kc.idx64) {
-        const int S = (opts && opts->slot_dims > 0 && opts->stages >= 3) ? opts->stages
-                                                                          : (int)knob("TT_KNOB_SD_STAGES", 0);
+        const int S = (opts && opts->slot_dims > 0 && opts->stages >= 3) ? opts->stages : 0;
         if ((S == 3 || S == 4) && (int64_t)S * plan.tile.sbuf * E <= dev.max_smem_per_block) {
             kc.stages = S;
             kc.smem = S * plan.tile.sbuf * E;
@@ -1319,6 +1315,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         vt.sdSlot[0] = vt.sdSlot[1] = -1;
         const int S = opts && opts->stages >= 3 ? std::min(4, opts->stages) : 4;
         int thr = 0, nr = 0, sm = 0;
+        vt.vgPolicy = opts ? opts->vg_policy : 0;
         if (build_vg(vt, pr, S, dev.max_smem_per_block, 32, thr, nr, sm)) {
             plan.tile = vt;
             kc.vg = 1;
@@ -1327,7 +1324,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
             kc.threads = thr;
             kc.nreg = nr;
             kc.smem = sm;
-            OccQuery qv{TT_KERNEL_TILE, E, nr, S, thr, sm, false, 0, 0, 0, 0, 0, 1};
+            OccQuery qv{TT_KERNEL_TILE, E, nr, S, thr, sm, false, 0, 0, 0, 0, 0, vt.vgK};
             int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qv, dev) : 0);
             if (per <= 0)
                 per = std::max(1, std::min({dev.max_smem_per_sm / (sm + 1024), dev.max_threads_per_sm / thr,
@@ -1343,7 +1340,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
     // VW elements per instruction on both sides (model: its issue cost is a
     // fraction of the generic kernel's, DRAM sectors are whole).
     const bool want2d = forced == TT_KERNEL_TILED2D ||
-                        (forced == TT_KERNEL_AUTO && can2d && fill2d >= knob("TT_KNOB_T2D_FILL", 0.6) &&
+                        (forced == TT_KERNEL_AUTO && can2d && fill2d >= rule::kT2dFill &&
                          fillB2d >= fillBMin &&
                          !(opts && (opts->run_in || opts->run_out)));
     if (want2d) {
@@ -1383,6 +1380,40 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         kc.predicted_us = bytes / model::kBwBytesPerUs + model::kLaunchUs;
         kc.model_dram_eff = 1.0;
     }
+    // 8-byte words on the generic tile (fp64, or fp32 pairs widened to 8
+    // bytes): the slot-dim map with a 4-stage cp.async ring
+    // (tile_sd_async_kernel) when that plan runs at one CTA per SM.  Same-box
+    // A/B over the suites' 8-byte generic-tile cases
+    // (profiles/round1_ab_sd_async8.txt): 18 of 20 faster, median 1.10x, none
+    // slower; at 2+ CTAs per SM it was a wash; widened fp32 pairs 5 of 5
+    // faster.  Planner-chosen plans only (no options).
+    static const tt_plan_options_t zeroOpts{};
+    const bool noOpts = opts == nullptr || std::memcmp(opts, &zeroOpts, sizeof(zeroOpts)) == 0;
+    if (noOpts && E == 8 && pr.dense && kc.kernel == TT_KERNEL_TILE && !kc.idx64 && !acc && !kc.vg) {
+        Plan alt;
+        alt.device = plan.device;
+        alt.stream = plan.stream;
+        alt.rank = plan.rank;
+        alt.prob = plan.prob;
+        tt_plan_options_t o{};
+        o.slot_dims = 1;
+        o.stages = 4;
+        if (choose_plan(alt, dev, &o, occ) == TT_SUCCESS && alt.kc.kernel == TT_KERNEL_TILE &&
+            alt.kc.sdq && alt.kc.stages == 4) {
+            OccQuery qa{TT_KERNEL_TILE, E, alt.kc.sdq * alt.kc.sdr, 4, alt.kc.threads, alt.kc.smem,
+                        false, 0, 0, 0, alt.kc.sdq, alt.kc.sdr};
+            int per = occ ? occ(qa, dev) : 0;
+            if (per <= 0)
+                per = std::max(1, std::min({dev.max_smem_per_sm / (alt.kc.smem + 1024),
+                                            dev.max_threads_per_sm / alt.kc.threads,
+                                            dev.regs_per_sm / (alt.kc.threads * 64)}));
+            if (per == 1) {
+                plan.tile = alt.tile;
+                plan.kc = alt.kc;
+            }
+        }
+    }
+
     return TT_SUCCESS;
 }
 
@@ -1503,7 +1534,8 @@ std::string describe_json(const Plan& plan) {
         arr(o, t.gSout, t.h);
         if (kc.vg)
             o << ",\"vg\":{\"M\":" << t.vgM << ",\"L\":" << t.vgL << ",\"Ltail\":" << t.vgLtail
-              << ",\"runs\":" << t.vgNR << ",\"group\":" << t.vgG << ",\"stages\":" << kc.stages << "}";
+              << ",\"runs\":" << t.vgNR << ",\"chunks\":" << t.vgNch << ",\"items\":" << t.vgK
+              << ",\"stages\":" << kc.stages << "}";
         if (kc.sdq) {
             o << ",\"sd\":{\"q\":" << kc.sdq << ",\"r\":" << kc.sdr << ",\"slot\":";
             arr(o, t.sdSlot, 2);

@@ -93,8 +93,12 @@ struct TileParams {
     int32_t vgLtail;    // run length when the run's split dim is at its ragged tail
     int32_t vgRunBit;   // need bit (1 or 2) of that split dim; 0 if the run is never ragged
     int32_t vgNR;       // runs per tile
-    int32_t vgG;        // lanes per run group (power of two <= 32)
-    int32_t vgTab;      // byte offset of the run table (uint2 per run) in dynamic shared memory
+    int32_t vgNch;      // 16-byte chunks per run slot at the worst-case shift
+    int32_t vgK;        // load items (run, chunk) per thread
+    int32_t vgE;        // word bytes
+    int32_t vgTab;      // byte offset of the tile-base ring (64 x uint4) in dynamic shared memory
+    int32_t vgPolicy;   // cache flavour of the chunk copies (kernels_vg.cu cp_async16_pred)
+    int64_t vgSpanIn;   // largest input offset inside a tile + 1 (elements)
     int64_t vgInBytes;  // bytes of the input tensor (chunks are clipped to [in, in + vgInBytes))
 };
 
@@ -178,7 +182,6 @@ struct ShardInfo;  // defined in dist.cu
 struct HostPipe;   // defined in api.cu (pipelined tt_execute_host)
 
 struct Plan {
-    uint32_t magic = 0x54545054u;  // "TTPT"
     int device = -1;
     void* stream = nullptr;
     int rank = 0;
@@ -216,6 +219,12 @@ std::string describe_json(const Plan& plan);
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev);
 
 // api.cu --------------------------------------------------------------------
+// Live-handle registry: every handle the ABI hands out (plans, contractions,
+// communicators) is registered; entry points accept a handle only while it is
+// registered, so a destroyed handle reads as invalid instead of as freed memory.
+void* publish_handle(void* h);          // registers h (if non-null), returns it
+bool handle_live(const void* h);
+bool retire_handle(const void* h);      // unregisters; false if h was not live
 Plan* as_plan(tt_plan_t h);
 tt_status_t query_device(DeviceInfo& dev);
 tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(tt.library_path)
     for name in sorted(declared):
         assert hasattr(lib, name), name
-    assert tt.lib.tt_version() == 1
+    assert tt.lib.tt_version() == 2
     assert tt.lib.tt_status_string(0) == b"TT_SUCCESS"
     assert tt.lib.tt_status_string(4) == b"TT_UNSUPPORTED"
 
@@ -56,6 +56,35 @@ def test_validation():
     assert _offline_status([1 << 31, 1 << 31], (1, 0), 8) == 2  # vol*E >= 2^62
     assert tt.lib.tt_destroy(None) == 1
     assert tt.lib.tt_execute(None, None, None) == 1
+
+
+def test_destroyed_handles_are_rejected():
+    """Handles are valid only while registered: a second tt_destroy, and any
+    call on a destroyed plan, return TT_INVALID_PLAN (no read of freed memory)."""
+    n, d, p = 2, (ctypes.c_int64 * 2)(40, 30), (ctypes.c_int * 2)(1, 0)
+    handles = []
+    for _ in range(3):
+        h = ctypes.c_void_p()
+        assert tt.lib.tt_plan_offline(ctypes.byref(h), n, d, p, 4, None, None) == 0
+        handles.append(h)
+    assert tt.lib.tt_destroy(handles[1]) == 0
+    assert tt.lib.tt_destroy(handles[1]) == 1            # double destroy
+    assert tt.lib.tt_execute(handles[1], 16, 1024) == 1  # execute after destroy
+    buf = ctypes.create_string_buffer(64)
+    assert tt.lib.tt_plan_describe(handles[1], buf, 64) == 1
+    assert tt.lib.tt_plan_launches(handles[1]) == -1
+    assert tt.lib.tt_destroy(ctypes.c_void_p(12345)) == 1  # never issued
+    for h in (handles[0], handles[2]):                    # the others are untouched
+        assert tt.lib.tt_plan_launches(h) == 1
+        assert tt.lib.tt_destroy(h) == 0
+
+
+def test_no_environment_knobs_in_the_library():
+    """Planner behaviour is fixed by the ABI (options), never by environment
+    variables: no getenv in the library sources."""
+    import glob
+    for f in glob.glob(os.path.join(ROOT, "paper_1705_01598_b200", "csrc", "*")):
+        assert "getenv" not in open(f).read(), f
 
 
 def test_offline_plan_cannot_execute():
@@ -159,12 +188,9 @@ def test_tiled2d_vector_width_and_rejections(monkeypatch):
     assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 1
     assert tt.plan_offline((11586, 11586), (1, 0), 8)["vec"] == 2
     assert tt.plan_offline((584, 584, 584), (2, 1, 0), 8)["vec"] == 1
-    monkeypatch.setenv("TT_KNOB_T2D_VEC2", "1")
-    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D)["vec"] == 2
-    monkeypatch.setenv("TT_KNOB_T2D_VEC8", "1")
-    assert tt.plan_offline((584, 584, 584), (2, 1, 0), 8)["vec"] == 2
-    monkeypatch.delenv("TT_KNOB_T2D_VEC2")
-    monkeypatch.delenv("TT_KNOB_T2D_VEC8")
+    assert tt.plan_offline((66, 62), (1, 0), 4, kernel=tt.KERNEL_TILED2D, t2d_vec2=1)["vec"] == 2
+    assert tt.plan_offline((584, 584, 584), (2, 1, 0), 8, t2d_vec2=1)["vec"] == 2
+    assert tt.plan_offline((11586, 11586), (1, 0), 8, t2d_vec2=-1)["vec"] == 1
     with pytest.raises(tt.TTError):   # fastest dim unchanged: not the Tiled class
         tt.plan_offline((64, 8, 8), (0, 2, 1), 4, kernel=tt.KERNEL_TILED2D)
     with pytest.raises(tt.TTError):   # tile not instantiated for the scalar kernel

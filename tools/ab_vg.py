@@ -34,7 +34,10 @@ def main():
     ap.add_argument("--variants", default="vg4,vg3")
     ap.add_argument("--only-tile", action="store_true", default=True)
     a = ap.parse_args()
-    variants = {"vg4": dict(vector_gather=1, stages=4), "vg3": dict(vector_gather=1, stages=3)}
+    variants = {}
+    for st in (3, 4):
+        for pol in range(4):
+            variants[f"vg{st}" + (f"p{pol}" if pol else "")] = dict(vector_gather=1, stages=st, vg_policy=pol)
     f = open(a.out, "w") if a.out else None
     ratios = {v: [] for v in a.variants.split(",")}
     for c in cases_for(a.suite.split(","), a.per_cell):
