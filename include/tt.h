@@ -365,6 +365,26 @@ tt_status_t tt_plan_sharded_p2p_offline(tt_plan_t* plan, int nranks, int proc, i
 tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local);
 
 /*
+ * The same registration without the communicator, for callers that exchange
+ * the records themselves (and for several processes sharing one GPU, where
+ * NCCL cannot form a communicator):
+ *   tt_sharded_export_record -- allocate this rank's signal words and write
+ *     its record (IPC handles of the allocations holding out_local and the
+ *     signal words; TT_SHARD_RECORD_BYTES bytes) to the HOST buffer `record`.
+ *     On failure the record is still written, flagged invalid, so peers that
+ *     receive it fail too instead of waiting.
+ *   tt_sharded_import_records -- `records` = the nranks records in rank
+ *     order (host memory); opens every peer's handles.  Afterwards
+ *     tt_execute_sharded(plan, in_local, out_local) runs the barriers and the
+ *     fused stores as with a communicator.  TT_INVALID_PARAMETER if a record
+ *     is flagged invalid or out of order.
+ * Works on tt_plan_sharded_p2p(_ex) plans with or without a communicator.
+ */
+#define TT_SHARD_RECORD_BYTES 256
+tt_status_t tt_sharded_export_record(tt_plan_t plan, void* out_local, void* record);
+tt_status_t tt_sharded_import_records(tt_plan_t plan, const void* records);
+
+/*
  * tt_execute_sharded_p2p -- single-process form: in_local = this process's
  * input slab (device pointer), out_slabs = host array [nranks] of every
  * rank's output slab, each writable from the plan's device.  Enqueues the
@@ -376,8 +396,9 @@ tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local);
  * peer reached this execute on its stream, so its slab is free), the
  * sub-box launches, exit barrier (every peer's stores into this slab have
  * landed).  The barriers are system-scope release/acquire signal words in
- * device memory; a peer missing for 30 s sets an error word instead of
- * hanging, reported by tt_sharded_timings as TT_CUDA_ERROR.
+ * device memory; a peer missing for 30 s sets an error word and traps the
+ * barrier kernel (the stream stops: later calls and synchronisations report
+ * TT_CUDA_ERROR) instead of hanging or storing into slabs still in use.
  * tt_sharded_timings then returns (entry barrier, fused permute, exit
  * barrier) milliseconds.
  */

@@ -99,6 +99,8 @@ def _load():
         "tt_plan_sharded_p2p_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         i64p, ip, ctypes.c_size_t],
         "tt_sharded_register_output": [vp, vp],
+        "tt_sharded_export_record": [vp, vp, vp],
+        "tt_sharded_import_records": [vp, vp],
         "tt_execute_sharded_p2p": [vp, vp, ctypes.POINTER(vp)],
     }
     for name, args in sig.items():

@@ -12,6 +12,8 @@ import ctypes
 
 from . import lib, _check, _arrays, _stream_handle, _describe, _ptr, _options, NCCL_UNIQUE_ID_BYTES
 
+SHARD_RECORD_BYTES = 256
+
 
 def unique_id() -> bytes:
     buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
@@ -143,6 +145,21 @@ class P2PShardedPlan(ShardedPlan):
         _check(lib.tt_sharded_register_output(self._h, _ptr(out_local)),
                "tt_sharded_register_output")
         self._registered = out_local   # keep the buffer alive with the plan
+
+    def export_record(self, out_local) -> bytes:
+        """This rank's registration record (tt_sharded_export_record)."""
+        buf = ctypes.create_string_buffer(SHARD_RECORD_BYTES)
+        _check(lib.tt_sharded_export_record(self._h, _ptr(out_local), buf), "tt_sharded_export_record")
+        self._registered = out_local
+        return buf.raw
+
+    def import_records(self, records) -> None:
+        """Every rank's record, rank order (tt_sharded_import_records)."""
+        blob = b"".join(records)
+        if len(blob) != SHARD_RECORD_BYTES * self.nranks:
+            raise ValueError("need one record per rank")
+        _check(lib.tt_sharded_import_records(self._h, ctypes.create_string_buffer(blob, len(blob))),
+               "tt_sharded_import_records")
 
     def execute_slabs(self, in_local, out_slabs) -> None:
         if len(out_slabs) != self.nranks:

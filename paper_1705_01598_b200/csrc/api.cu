@@ -318,6 +318,20 @@ static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, cons
     return st;
 }
 
+static tt_status_t check_exec(Plan* p, const void* in, void* out) {
+    if (p == nullptr) return TT_INVALID_PLAN;
+    if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
+    const uintptr_t mis = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
+                          (uintptr_t)(p->prob.esize / p->widen - 1);
+    if (mis) return TT_INVALID_PARAMETER;
+    if (p->device < 0) return TT_INVALID_DEVICE;
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    if (d != p->device) return TT_INVALID_DEVICE;
+    return TT_SUCCESS;
+}
+
+
 extern "C" {
 
 int tt_version(void) { return TT_VERSION; }
@@ -372,6 +386,9 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
     Plan* heur = nullptr;
     st = create_plan(&heur, rank, dims, perm, elem_size, stream, dev, nullptr, &cuda_occupancy);
     if (st != TT_SUCCESS) return st;
+    // the execute-time checks (alignment, device) before any candidate runs
+    st = check_exec(heur, in, out);
+    if (st != TT_SUCCESS) { destroy_plan(heur); return st; }
 
     // candidate options (elements of the widened problem when it widens)
     std::vector<tt_plan_options_t> vars;
@@ -553,19 +570,6 @@ tt_status_t tt_plan_strided_offline(tt_plan_t* plan, int rank, const int64_t* di
                                    in_strides, out_strides);
     *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
-}
-
-static tt_status_t check_exec(Plan* p, const void* in, void* out) {
-    if (p == nullptr) return TT_INVALID_PLAN;
-    if (in == nullptr || out == nullptr || in == out) return TT_INVALID_PARAMETER;
-    const uintptr_t mis = (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
-                          (uintptr_t)(p->prob.esize / p->widen - 1);
-    if (mis) return TT_INVALID_PARAMETER;
-    if (p->device < 0) return TT_INVALID_DEVICE;
-    int d = -1;
-    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TT_INVALID_DEVICE; }
-    if (d != p->device) return TT_INVALID_DEVICE;
-    return TT_SUCCESS;
 }
 
 tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out) {

@@ -79,6 +79,7 @@ struct ShardInfo {
     int64_t in_step = 0;            // elements between destination sub-boxes in the input slab
     int64_t out_off = 0;            // this rank's block inside every output slab (elements)
     void* reg_out = nullptr;        // registered output slab (tt_sharded_register_output)
+    void* exported = nullptr;       // output slab of tt_sharded_export_record, until imported
     std::vector<void*> peer_out;    // [P] output slabs as mapped in this process
     std::vector<void*> ipc_bases;   // peer allocations opened with cudaIpcOpenMemHandle
     int* sig = nullptr;             // [P] signal words of this rank (device), + [P] error word
@@ -303,21 +304,27 @@ __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
         asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(a.mine + q) : "memory");
         if (v - a.epoch >= 0) break;
         if (global_ns() - t0 > kP2PTimeoutNs) {
+            // a peer is missing: record it and stop the stream for good (the
+            // context's sticky launch error makes every later tt_* call and
+            // synchronisation fail) -- never let the fused stores run into
+            // slabs a peer may still be reading, or hand out a slab whose
+            // peers' stores have not landed
             atomicExch(a.mine + a.P, 1);
-            break;
+            __threadfence_system();
+            __trap();
         }
         __nanosleep(200);
     }
 }
 
-static int launch_barrier(ShardInfo* s, cudaStream_t st) {
+static int launch_barrier(ShardInfo* s, cudaStream_t st, int epoch) {
     BarrierArgs a;
     std::memset(&a, 0, sizeof(a));
     for (int q = 0; q < s->nranks; ++q) a.peer_sig[q] = s->peer_sig[q];
     a.mine = s->sig;
     a.P = s->nranks;
     a.rank = s->proc;
-    a.epoch = ++s->epoch;
+    a.epoch = epoch;
     p2p_barrier_kernel<<<1, 64, 0, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -384,9 +391,77 @@ struct RegRecord {
     cudaIpcMemHandle_t sig;
     int64_t out_off;
     int32_t device, proc;
-    char pad[256 - 2 * sizeof(cudaIpcMemHandle_t) - 16];
+    int32_t ok;        // 1: this rank's handles are valid (a failed rank still joins the exchange)
+    char pad[256 - 2 * sizeof(cudaIpcMemHandle_t) - 20];
 };
-static_assert(sizeof(RegRecord) == 256, "registration record");
+static_assert(sizeof(RegRecord) == TT_SHARD_RECORD_BYTES, "registration record");
+
+// This rank's record: its signal words (allocated once, zeroed, reused on a
+// retry) and the IPC handles of the allocations holding them and out_local.
+static tt_status_t make_record(ShardInfo* s, int device, void* out_local, RegRecord& mine) {
+    std::memset(&mine, 0, sizeof(mine));
+    mine.device = device;
+    mine.proc = s->proc;
+    const int P = s->nranks;
+    if (s->sig == nullptr && cudaMalloc(&s->sig, (P + 1) * sizeof(int)) != cudaSuccess) {
+        s->sig = nullptr;
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    if (cudaMemset(s->sig, 0, (P + 1) * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    void* base = nullptr;
+    size_t off = 0;
+    if (!alloc_base(out_local, &base, &off) || cudaIpcGetMemHandle(&mine.out, base) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.sig, s->sig) != cudaSuccess) {
+        cudaGetLastError();
+        return TT_CUDA_ERROR;
+    }
+    mine.out_off = (int64_t)off;
+    mine.ok = 1;
+    return TT_SUCCESS;
+}
+
+// Open every peer's record (all[q] is rank q's); on any failure nothing stays open.
+static tt_status_t open_records(ShardInfo* s, void* out_local, const RegRecord* all) {
+    const int P = s->nranks;
+    for (int q = 0; q < P; ++q)
+        if (!all[q].ok || all[q].proc != q) return TT_INVALID_PARAMETER;
+    std::vector<void*> opened;
+    std::vector<void*> pout(P, nullptr);
+    std::vector<int*> psig(P, nullptr);
+    for (int q = 0; q < P; ++q) {
+        if (q == s->proc) {
+            pout[q] = out_local;
+            psig[q] = s->sig;
+            continue;
+        }
+        void* ob = nullptr;
+        void* sb = nullptr;
+        if (cudaIpcOpenMemHandle(&ob, all[q].out, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+            opened.push_back(ob);
+        else
+            ob = nullptr;
+        if (ob && cudaIpcOpenMemHandle(&sb, all[q].sig, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess)
+            opened.push_back(sb);
+        else
+            sb = nullptr;
+        if (!ob || !sb) {
+            cudaGetLastError();
+            for (void* b : opened) cudaIpcCloseMemHandle(b);
+            return TT_CUDA_ERROR;
+        }
+        pout[q] = static_cast<char*>(ob) + all[q].out_off;
+        psig[q] = static_cast<int*>(sb);
+    }
+    s->ipc_bases = opened;
+    s->peer_out = pout;
+    s->peer_sig = psig;
+    s->reg_out = out_local;
+    return TT_SUCCESS;
+}
 
 }  // namespace tt
 
@@ -503,7 +578,8 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
     if (((reinterpret_cast<uintptr_t>(in_local) | reinterpret_cast<uintptr_t>(out_local)) &
          (uintptr_t)(s->esize - 1)) != 0)
         return TT_INVALID_PARAMETER;
-    if (s->comm == nullptr || p->device < 0) return TT_INVALID_DEVICE;
+    // a communicator, or a p2p plan registered through exported / imported records
+    if ((s->comm == nullptr && !(s->p2p && s->reg_out != nullptr)) || p->device < 0) return TT_INVALID_DEVICE;
     int d = -1;
     if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
@@ -512,13 +588,17 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
     if (s->p2p) {
         // fused: entry barrier, P sub-box permutations into the peers' slabs, exit barrier
         if (s->reg_out == nullptr || out_local != s->reg_out) return TT_INVALID_PARAMETER;
+        // epochs advance by two per execute whatever happens below, so a
+        // failed execute cannot leave this rank one barrier behind its peers
+        const int base = s->epoch;
+        s->epoch += 2;
         cudaEventRecord(s->ev[0], st);
-        if (launch_barrier(s, st) != 0) return TT_CUDA_ERROR;
+        if (launch_barrier(s, st, base + 1) != 0) return TT_CUDA_ERROR;
         cudaEventRecord(s->ev[1], st);
         tt_status_t rc = launch_fused(s, in_local, s->peer_out.data(), p->stream);
         if (rc != TT_SUCCESS) return rc;
         cudaEventRecord(s->ev[2], st);
-        if (launch_barrier(s, st) != 0) return TT_CUDA_ERROR;
+        if (launch_barrier(s, st, base + 2) != 0) return TT_CUDA_ERROR;
         cudaEventRecord(s->ev[3], st);
         s->timed = true;
         return TT_SUCCESS;
@@ -636,26 +716,10 @@ tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local) {
     if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
     const int P = s->nranks;
     cudaStream_t st = static_cast<cudaStream_t>(p->stream);
-    // own signal words (+ error word), zeroed before any peer can see them
-    if (cudaMalloc(&s->sig, (P + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMemset(s->sig, 0, (P + 1) * sizeof(int)) != cudaSuccess) {
-        cudaGetLastError();
-        return TT_CUDA_ERROR;
-    }
     RegRecord mine;
-    std::memset(&mine, 0, sizeof(mine));
-    void* base = nullptr;
-    size_t off = 0;
-    if (!alloc_base(out_local, &base, &off) ||
-        cudaIpcGetMemHandle(&mine.out, base) != cudaSuccess ||
-        cudaIpcGetMemHandle(&mine.sig, s->sig) != cudaSuccess) {
-        cudaGetLastError();
-        return TT_CUDA_ERROR;
-    }
-    mine.out_off = (int64_t)off;
-    mine.device = d;
-    mine.proc = s->proc;
-    // all-gather the records with the communicator (no host-side rendezvous)
+    const tt_status_t local = make_record(s, d, out_local, mine);
+    // all-gather the records with the communicator (no host-side rendezvous);
+    // a rank that failed above still joins with ok = 0 so no peer blocks
     void* dbuf = nullptr;
     std::vector<RegRecord> all(P);
     if (cudaMalloc(&dbuf, (size_t)(P + 1) * sizeof(RegRecord)) != cudaSuccess) {
@@ -673,32 +737,40 @@ tt_status_t tt_sharded_register_output(tt_plan_t plan, void* out_local) {
         rc = TT_CUDA_ERROR;
     cudaFree(dbuf);
     if (rc != TT_SUCCESS) { cudaGetLastError(); return rc; }
-    s->peer_out.assign(P, nullptr);
-    s->peer_sig.assign(P, nullptr);
-    for (int q = 0; q < P; ++q) {
-        if (all[q].proc != q) return TT_INTERNAL_ERROR;
-        if (q == s->proc) {
-            s->peer_out[q] = out_local;
-            s->peer_sig[q] = s->sig;
-            continue;
-        }
-        void* ob = nullptr;
-        void* sb = nullptr;
-        if (cudaIpcOpenMemHandle(&ob, all[q].out, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            return TT_CUDA_ERROR;
-        }
-        s->ipc_bases.push_back(ob);
-        if (cudaIpcOpenMemHandle(&sb, all[q].sig, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            return TT_CUDA_ERROR;
-        }
-        s->ipc_bases.push_back(sb);
-        s->peer_out[q] = static_cast<char*>(ob) + all[q].out_off;
-        s->peer_sig[q] = static_cast<int*>(sb);
-    }
-    s->reg_out = out_local;
-    return TT_SUCCESS;
+    if (local != TT_SUCCESS) return local;
+    return open_records(s, out_local, all.data());
+}
+
+tt_status_t tt_sharded_export_record(tt_plan_t plan, void* out_local, void* record) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr || p->shard == nullptr) return TT_INVALID_PLAN;
+    ShardInfo* s = p->shard;
+    if (!s->p2p) return TT_INVALID_PLAN;
+    if (record == nullptr || out_local == nullptr ||
+        (reinterpret_cast<uintptr_t>(out_local) & (uintptr_t)(s->esize - 1)))
+        return TT_INVALID_PARAMETER;
+    if (s->reg_out != nullptr) return TT_INVALID_PARAMETER;
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    RegRecord mine;
+    const tt_status_t st = make_record(s, d, out_local, mine);
+    std::memcpy(record, &mine, sizeof(mine));   // ok = 0 on failure: peers see it
+    if (st == TT_SUCCESS) s->exported = out_local;
+    return st;
+}
+
+tt_status_t tt_sharded_import_records(tt_plan_t plan, const void* records) {
+    Plan* p = as_plan(plan);
+    if (p == nullptr || p->shard == nullptr) return TT_INVALID_PLAN;
+    ShardInfo* s = p->shard;
+    if (!s->p2p) return TT_INVALID_PLAN;
+    if (records == nullptr || s->exported == nullptr) return TT_INVALID_PARAMETER;
+    if (s->reg_out != nullptr) return TT_INVALID_PARAMETER;
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d != p->device) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    std::vector<RegRecord> all(s->nranks);
+    std::memcpy(all.data(), records, all.size() * sizeof(RegRecord));
+    return open_records(s, s->exported, all.data());
 }
 
 tt_status_t tt_execute_sharded_p2p(tt_plan_t plan, const void* in_local, void* const* out_slabs) {

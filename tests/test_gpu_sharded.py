@@ -179,3 +179,75 @@ def test_p2p_single_rank_comm_barriers(monkeypatch):
         assert fused_ms > 0 and bar_in >= 0 and bar_out >= 0
         sp.destroy()
     comm.destroy()
+
+
+def _ipc_worker(rank, port, gdims, perm, result_q):
+    """One of two processes sharing cuda:0: the fused redistribution with its
+    peer registered through exported / imported IPC records (gloo carries the
+    records), entry/exit barriers across the processes, remote stores into the
+    other process's output slab."""
+    import torch.distributed as dist
+    import paper_1705_01598_b200 as tt_
+    import tt_workloads as wl_
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+    try:
+        vol = int(np.prod(gdims))
+        words = wl_.random_words(vol, 8, 31)
+        slab = vol // 2
+        x = torch.from_numpy(words[rank * slab:(rank + 1) * slab].view(np.int64).copy()).cuda()
+        y = torch.zeros(slab, dtype=torch.int64, device="cuda")
+        plan = tt_.P2PShardedPlan(None, gdims, perm, 8, nranks=2, proc=rank)
+        rec = plan.export_record(y)
+        recs = [None, None]
+        dist.all_gather_object(recs, rec)
+        plan.import_records(recs)
+        outs = []
+        for it in range(3):                       # epochs advance across executes
+            y.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            plan.execute(x, y)
+            torch.cuda.synchronize()
+            dist.barrier()                        # both exit barriers passed
+            outs.append(y.cpu().numpy().view(np.uint64).copy())
+        t = plan.timings()
+        result_q.put((rank, outs, t, plan.describe()["mode"]))
+        dist.barrier()
+        plan.destroy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_two_processes_one_gpu_ipc():
+    """Two processes on one GPU run the multi-process fused path end to end:
+    IPC open of the peer's output slab and signal words, cross-process
+    release/acquire barriers, remote stores; the gathered output equals the
+    oracle's, on every one of three executes."""
+    _dev()
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    gdims, perm = (16, 24, 8, 40), (3, 2, 1, 0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, gdims, perm, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, outs, t, mode = q.get(timeout=300)
+        res[r] = (outs, t, mode)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    words = wl.random_words(int(np.prod(gdims)), 8, 31)
+    want = orc.permute(gdims, perm, words)
+    for it in range(3):
+        got = np.concatenate([res[0][0][it], res[1][0][it]])
+        np.testing.assert_array_equal(got, want, err_msg=f"execute {it}")
+    for r in range(2):
+        assert res[r][2] == "p2p"
+        assert all(v >= 0 for v in res[r][1])
