@@ -109,8 +109,8 @@ typedef struct {
                             1 = always, -1 = never (scalar kernel), 0 = planner's measured rule */
     int force_redistribute; /* sharded plans (tt_plan_sharded_ex / _p2p_ex): take the
                             redistribution path even with one rank (single-GPU tests) */
-    int vg_policy;       /* vector-gather loads, calibration: 0 = cp.async.cg, 1 = .ca,
-                            2 = .cg with an L2 evict_last hint, 3 = evict_normal hint */
+    int vg_policy;       /* vector-gather loads, calibration: 0 = cp.async.ca (default),
+                            1 = cp.async.cg (L2 only) */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */

@@ -33,8 +33,14 @@
 // LDS + IMAD.WIDE + STG + one add; ragged tiles predicate the STG
 // per slot instead of branching.
 //
-// Shared memory: S stages of p.sbuf elements, then the tile-base ring (64 x
-// uint4: input offset, output offset, ragged state | interior << 2).
+// Pipeline: S stages, S-1 tiles in flight; per stage a "full" mbarrier (the
+// copies have landed: cp.async.mbarrier.arrive) and an "empty" one (every
+// warp has read it), so warps wait only for data and for the slowest reader
+// of the stage being refilled -- no CTA-wide barrier per tile.
+//
+// Shared memory: S stages of p.sbuf elements, then the tile-base ring (128 x
+// uint4: input offset, output offset, ragged state | interior << 2), then
+// the 2 S mbarriers.
 #include "kern_common.cuh"
 #include "kern_pick.h"
 
@@ -50,20 +56,42 @@ __device__ __forceinline__ void stg_pred(uint64_t* p, uint64_t v, bool ok) {
                  "r"((uint32_t)ok)
                  : "memory");
 }
-// cache flavour of the 16-byte chunk copies (p.vgPolicy, calibration):
-// 0 = .cg (L2 only), 1 = .ca (L1 and L2), 2 = .cg with an L2 evict_last hint,
-// 3 = .cg with an L2 evict_normal hint
+// Cache flavour of the 16-byte chunk copies (p.vgPolicy): 0 = .ca (through
+// L1), 1 = .cg (L2 only).  Measured (profiles/round2_vg_policy.txt): with .cg
+// the L1 does not merge the 16-byte requests of one 32-byte sector, so L2
+// sees ~1.5x the sector requests and DRAM re-reads the sectors shared by
+// neighbouring runs (+24 % read traffic on 5^12 fp32); .ca is the default.
 template <int POL>
-__device__ __forceinline__ void cp_async16_pred(uint32_t saddr, const void* g, bool ok, uint64_t pol) {
+__device__ __forceinline__ void cp_async16_pred(uint32_t saddr, const void* g, bool ok) {
     if constexpr (POL == 0)
-        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(saddr),
-                     "l"(g), "r"((uint32_t)ok));
-    else if constexpr (POL == 1)
         asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.ca.shared.global [%0], [%1], 16; }" ::"r"(saddr),
                      "l"(g), "r"((uint32_t)ok));
     else
-        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3; }"
-                     ::"r"(saddr), "l"(g), "r"((uint32_t)ok), "l"(pol));
+        asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(saddr),
+                     "l"(g), "r"((uint32_t)ok));
+}
+
+// mbarrier pipeline (per stage: "full" = the stage's copies have landed,
+// count NT, one asynchronous arrive per thread after its copies; "empty" =
+// every warp has read the stage, count = warps)
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t a) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.b32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
 }
 
 // Tile-base entry of one tile (Algorithm 1 over the grid dims, one lane):
@@ -172,6 +200,14 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
     if (t0 >= nTiles) return;
     const uint32_t nIt = (nTiles - t0 + G - 1) / G;  // tiles of this CTA: t0 + it*G
     const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t fullB = sm0 + (uint32_t)p.vgTab + 128u * 16u;  // full[s] at fullB + 8 s
+    const uint32_t emptyB = fullB + 8u * S;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(fullB + 8u * s, (uint32_t)NT);
+            mbar_init(emptyB + 8u * s, (uint32_t)(NT >> 5));
+        }
+    }
     if (warp == 0) {  // tile bases of iterations 0..63
         for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32)
             ring[it] = vg_tile_entry(p, t0 + it * G);
@@ -182,12 +218,9 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
     const uint32_t LB = (uint32_t)p.vgL * E, LtB = (uint32_t)p.vgLtail * E;
     const uint32_t runBit = (uint32_t)p.vgRunBit;
     const int pol = p.vgPolicy;
-    uint64_t l2pol = 0;
-    if (pol == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
-    if (pol == 3) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(l2pol));
 
     auto issue = [&](uint32_t it, uint32_t sb) {
-        const uint4 e = ring[it & 63u];
+        const uint4 e = ring[it & 127u];
         const uint32_t nd = e.z & 3u;
         const uint32_t Lb = (runBit & nd) ? LtB : LB;
         const char* const tb = inB + (size_t)e.x * E;
@@ -203,14 +236,11 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
                     const uint32_t q = ((pk[k] >> 22) & 3u) << 2;
                     const bool ok = ((pk[k] >> vs) & 1u) && c16 < s + Lb;
                     const uint32_t dst = sb + (pk[k] & 0x3ffffu) + (s < q ? 16u : 0u);
-                    cp_async16_pred<POL>(dst, a - s + c16, ok, l2pol);
+                    cp_async16_pred<POL>(dst, a - s + c16, ok);
                 }
             };
-            switch (pol) {
-                case 1: items(std::integral_constant<int, 1>()); break;
-                case 2: case 3: items(std::integral_constant<int, 2>()); break;
-                default: items(std::integral_constant<int, 0>()); break;
-            }
+            if (pol == 1) items(std::integral_constant<int, 1>());
+            else items(std::integral_constant<int, 0>());
         } else {  // near an end of the input: element-wise inside the tensor
             const char* const lo = inB;
             const char* const hi = inB + p.vgInBytes;
@@ -236,40 +266,48 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
 
 #pragma unroll
     for (int s = 0; s < S - 1; ++s) {
-        if ((uint32_t)s < nIt) issue((uint32_t)s, sm0 + (uint32_t)s * sbytes);
-        cp_async_commit();
+        if ((uint32_t)s < nIt) {
+            issue((uint32_t)s, sm0 + (uint32_t)s * sbytes);
+            cp_async_mbar_arrive(fullB + 8u * s);
+        }
     }
     uint32_t stage = 0;
     for (uint32_t it = 0; it < nIt; ++it) {
-        cp_async_wait<S - 2>();
-        __syncthreads();
-        if ((it & 31u) == 0 && it > 0 && warp == 0) {  // next 32 tile bases, other half of the ring
+        mbar_wait(fullB + 8u * stage, (it / S) & 1u);   // tile it has landed in its stage
+        if ((it & 31u) == 0 && it >= 32u && warp == 0) {  // tile bases of iterations it+32 .. it+63
             const uint32_t j = it + 32u + (uint32_t)lane;
-            if (j < nIt) ring[j & 63u] = vg_tile_entry(p, t0 + j * G);
+            if (j < nIt) ring[j & 127u] = vg_tile_entry(p, t0 + j * G);
         }
-        {  // refill the stage read in the previous iteration
-            const uint32_t itn = it + (uint32_t)(S - 1);
+        // transposed read of the staged tile (Eq. 6), coalesced writes (Eq. 5)
+        {
+            const uint4 e = ring[it & 127u];
+            const uint32_t nd = e.z & 3u;
+            const uint32_t sbsh = sm0 + stage * sbytes +
+                                  ((uint32_t)reinterpret_cast<uintptr_t>(inB + (size_t)e.x * E) & 15u);
+            W* const dst = out + e.y;
+            const uint32_t m = nd == 0 ? m0 : nd == 1 ? m1 : nd == 2 ? m2 : m3;
+            if (m == full) {
+#pragma unroll
+                for (int r = 0; r < NREG; ++r) stg_(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]));
+            } else {
+#pragma unroll
+                for (int r = 0; r < NREG; ++r)
+                    stg_pred(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]), (m >> r) & 1u);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(emptyB + 8u * stage);
+        // refill the stage read in the previous iteration with tile it+S-1,
+        // once every warp has read it
+        const uint32_t itn = it + (uint32_t)(S - 1);
+        if (itn < nIt) {
             const uint32_t sn = (stage == 0) ? (uint32_t)(S - 1) : stage - 1;
-            if (itn < nIt) issue(itn, sm0 + sn * sbytes);
-            cp_async_commit();
-        }
-        const uint4 e = ring[it & 63u];
-        const uint32_t nd = e.z & 3u;
-        const uint32_t sbsh = sm0 + stage * sbytes +
-                              ((uint32_t)reinterpret_cast<uintptr_t>(inB + (size_t)e.x * E) & 15u);
-        W* const dst = out + e.y;
-        const uint32_t m = nd == 0 ? m0 : nd == 1 ? m1 : nd == 2 ? m2 : m3;
-        if (m == full) {
-#pragma unroll
-            for (int r = 0; r < NREG; ++r) stg_(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]));
-        } else {
-#pragma unroll
-            for (int r = 0; r < NREG; ++r)
-                stg_pred(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]), (m >> r) & 1u);
+            if (itn >= (uint32_t)S) mbar_wait(emptyB + 8u * sn, ((itn - S) / S) & 1u);
+            issue(itn, sm0 + sn * sbytes);
+            cp_async_mbar_arrive(fullB + 8u * sn);
         }
         stage = (stage + 1 == (uint32_t)S) ? 0u : stage + 1;
     }
-    cp_async_wait<0>();
 }
 
 // vector-gather tile: 4/8-byte words, NREG store slots in {4, 8, 16}, K load

@@ -317,40 +317,46 @@ struct SmemSample {
     int a = 0, nacc = 0;
     std::vector<int> nl;     // lanes per distinct access pattern
     std::vector<int> wt;     // sampled accesses with that pattern
-    std::vector<int> coord;  // [pattern][lane][tile dim], relative to lane 0
+    std::vector<int> coord;  // [pattern][lane][tile dim + 1], relative to lane 0; the last
+                             // entry is a layout-independent extra offset (elements)
 };
 
 // Adding the same offset to every lane's position permutes the banks, so an
 // access's wavefront count depends only on the lanes' coordinates relative to
 // lane 0: sampled accesses with equal relative patterns are merged (weighted).
-static SmemSample smem_sample(const TileParams& tp, int sides = 3) {
+static int no_extra(const int*) { return 0; }
+
+template <typename Extra = int (*)(const int*)>
+static SmemSample smem_sample(const TileParams& tp, int sides = 3, Extra extra = no_extra) {
     SmemSample s;
     s.a = tp.a;
     const int V = tp.V;
     const int nw = (V + 31) / 32;
     const int step = std::max(1, nw / 8);
-    std::vector<int> cur(32 * tp.a);
+    const int A = tp.a + 1;
+    std::vector<int> cur(32 * A);
     for (int w = 0; w < nw; w += step) {
         const int nl = std::min(32, V - w * 32);
         for (int side = 0; side < 2; ++side) {  // 0: staging store (input order), 1: transposed read
             if (!(sides & (1 << side))) continue;
-            int c0[kMaxDims] = {};
+            int c0[kMaxDims + 1] = {};
             for (int l = 0; l < 32; ++l) {
                 int kk = w * 32 + l;
-                int c[kMaxDims] = {};
+                int c[kMaxDims + 1] = {};
                 for (int jj = 0; jj < tp.a && l < nl; ++jj) {
                     const int t = side == 0 ? jj : tp.tOutOrder[jj];
                     c[t] = kk % tp.tExt[t];
                     kk /= tp.tExt[t];
                 }
+                c[tp.a] = l < nl ? extra(c) : 0;
                 if (l == 0)
-                    for (int i = 0; i < tp.a; ++i) c0[i] = c[i];
-                for (int i = 0; i < tp.a; ++i) cur[l * tp.a + i] = l < nl ? c[i] - c0[i] : 0;
+                    for (int i = 0; i < A; ++i) c0[i] = c[i];
+                for (int i = 0; i < A; ++i) cur[l * A + i] = l < nl ? c[i] - c0[i] : 0;
             }
             bool merged = false;
             for (int q = 0; q < s.nacc && !merged; ++q) {
                 if (s.nl[q] != nl) continue;
-                if (std::equal(cur.begin(), cur.end(), s.coord.begin() + (size_t)q * 32 * tp.a)) {
+                if (std::equal(cur.begin(), cur.end(), s.coord.begin() + (size_t)q * 32 * A)) {
                     ++s.wt[q];
                     merged = true;
                 }
@@ -372,8 +378,8 @@ static long smem_cost(const SmemSample& s, int esize, const int32_t* sm, long bo
     const int* c = s.coord.data();
     for (int q = 0; q < s.nacc; ++q) {
         if (bound >= 0 && cost >= bound) return cost;  // already no better than the incumbent
-        for (int l = 0; l < 32; ++l, c += s.a) {
-            int sp = 0;
+        for (int l = 0; l < 32; ++l, c += s.a + 1) {
+            int sp = c[s.a];
             for (int i = 0; i < s.a; ++i) sp += c[i] * sm[i];
             pos[l] = sp + 4096;  // relative positions may be negative: keep the low bits' meaning
         }
@@ -491,7 +497,7 @@ static void tile_need(const Problem& pr, int64_t Tin, int64_t Tout, int64_t* nee
 // Build the tile with extents need[] (from tile_need).
 static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSplit, int outSplit,
                                 int Vmax, const DeviceInfo& dev, int forceThreads, int maxR,
-                                int forceR, int VmaxSd) {
+                                int forceR, int VmaxSd, bool full = true) {
     TileCand c;
     const int n = pr.n;
     long double V = 1;
@@ -559,7 +565,7 @@ static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSp
         }
     }
     tp.nTiles = acc;
-    fill_magic(tp);
+    if (full) fill_magic(tp);  // the searches only compare costs; the winner is rebuilt in full
     for (int s = 0; s < tp.nSplit; ++s)
         if (tp.splitChunk[s] > 256) return c;  // kernel packs split coordinates in 8 bits
 
@@ -704,27 +710,86 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
 }
 
 // Many run-target pairs give the same tile (a dim is taken whole from one
-// target up): the searches of choose_plan evaluate each distinct tile once.
+// target up): the searches of choose_plan evaluate each distinct tile once,
+// keep only what the searches compare (model cost, runs), and the winner is
+// rebuilt in full at the end.  A memo may be shared by the plans of one
+// problem (the fp64 ring rule re-plans it with other options).
+struct TileSumm {
+    bool ok = false;
+    double cost = 1e30;
+    int64_t runIn = 0, runOut = 0;
+    int64_t Tin = 0, Tout = 0;   // run targets that built it
+    int VmaxSd = 0;
+};
+
 struct TileMemo {
-    struct Entry {
-        int64_t key[kMaxDims + 3];
-        TileCand c;
-    };
-    std::vector<Entry> e;
-    const TileCand& get(const Problem& pr, int64_t Tin, int64_t Tout, int Vmax, const DeviceInfo& dev,
-                        int forceThreads, int maxR, int forceR, int VmaxSd) {
-        Entry x;
+    Problem prob;
+    bool bound = false;
+    bool same_problem(const Problem& p) const {
+        if (!bound || p.n != prob.n || p.esize != prob.esize || p.dense != prob.dense || p.span != prob.span)
+            return false;
+        for (int i = 0; i < p.n; ++i)
+            if (p.d[i] != prob.d[i] || p.p[i] != prob.p[i] || p.sin[i] != prob.sin[i] || p.sout[i] != prob.sout[i])
+                return false;
+        return true;
+    }
+    std::vector<int64_t> keys;   // kMaxDims + 4 per entry
+    std::vector<TileSumm> val;
+    std::vector<int> table;      // open addressing over entry indices, -1 = empty
+    int width = 0;
+
+    static uint64_t hash(const int64_t* k, int n) {
+        uint64_t h = 1469598103934665603ull;
+        for (int i = 0; i < n; ++i) h = (h ^ (uint64_t)k[i]) * 1099511628211ull;
+        return h ^ (h >> 29);
+    }
+    TileSumm get(const Problem& p, int64_t Tin, int64_t Tout, int Vmax, const DeviceInfo& dev,
+                 int forceThreads, int maxR, int forceR, int VmaxSd) {
+        if (!same_problem(p)) {  // (re)bind to this problem
+            prob = p;
+            bound = true;
+            width = p.n + 4;
+            keys.clear();
+            val.clear();
+            table.assign(1024, -1);
+        }
+        int64_t k[kMaxDims + 4];
         int inSplit, outSplit;
-        tile_need(pr, Tin, Tout, x.key, inSplit, outSplit);
-        x.key[pr.n] = Vmax;
-        x.key[pr.n + 1] = VmaxSd;
-        x.key[pr.n + 2] = (int64_t)(inSplit + 1) * 64 + (outSplit + 1);
-        const size_t kb = sizeof(int64_t) * (pr.n + 3);
-        for (const Entry& y : e)
-            if (std::memcmp(x.key, y.key, kb) == 0) return y.c;
-        x.c = build_tile_need(pr, x.key, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd);
-        e.push_back(x);
-        return e.back().c;
+        tile_need(p, Tin, Tout, k, inSplit, outSplit);
+        k[p.n] = Vmax;
+        k[p.n + 1] = VmaxSd;
+        k[p.n + 2] = (int64_t)(inSplit + 1) * 64 + (outSplit + 1);
+        k[p.n + 3] = (int64_t)forceThreads * 4096 + maxR * 64 + forceR;
+        const size_t mask = table.size() - 1;
+        size_t h = hash(k, width) & mask;
+        for (; table[h] >= 0; h = (h + 1) & mask) {
+            const int64_t* y = &keys[(size_t)table[h] * width];
+            if (std::memcmp(k, y, sizeof(int64_t) * width) == 0) return val[table[h]];
+        }
+        const TileCand c = build_tile_need(p, k, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR,
+                                           VmaxSd, false);
+        TileSumm sm;
+        sm.ok = c.ok;
+        sm.cost = c.cost_us;
+        sm.runIn = c.runIn;
+        sm.runOut = c.runOut;
+        sm.Tin = Tin;
+        sm.Tout = Tout;
+        sm.VmaxSd = VmaxSd;
+        table[h] = (int)val.size();
+        keys.insert(keys.end(), k, k + width);
+        val.push_back(sm);
+        if (val.size() * 2 > table.size()) {  // grow and rehash
+            std::vector<int> t2(table.size() * 2, -1);
+            const size_t m2 = t2.size() - 1;
+            for (size_t i = 0; i < val.size(); ++i) {
+                size_t g = hash(&keys[i * width], width) & m2;
+                while (t2[g] >= 0) g = (g + 1) & m2;
+                t2[g] = (int)i;
+            }
+            table.swap(t2);
+        }
+        return sm;
     }
 };
 
@@ -826,7 +891,14 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
         for (int t = M; t < tp.a; ++t) last += (int64_t)(tp.tExt[t] - 1) * sm[t];
         return last + pitch;
     };
-    const SmemSample sample = smem_sample(tp, 2);  // the transposed read only
+    // the transposed read only; an element of run r sits q_r = (run offset
+    // mod 16 bytes) further (the folded shift, kernels_vg.cu)
+    auto qshift = [&](const int* c) {
+        int64_t off = 0;
+        for (int t = M; t < tp.a; ++t) off += (int64_t)c[t] * tp.tSin[t];
+        return (int)(off % VPC);
+    };
+    const SmemSample sample = smem_sample(tp, 2, qshift);
     strides();
     long best = smem_cost(sample, E, sm);
     for (int pass = 0; pass < 2; ++pass)
@@ -845,7 +917,7 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
     tp.sbuf = (int32_t)((foot + VPC - 1) / VPC * VPC);
     tp.vgTab = S * tp.sbuf * E;
     tp.vgInBytes = pr.span * E;
-    smem = tp.vgTab + 64 * 16;
+    smem = tp.vgTab + 128 * 16 + 16 * S;   // tile-base ring, full/empty mbarriers
     if (smem > maxSmem || (int64_t)tp.sbuf * E >= (int64_t(1) << 18)) return false;
     // store phase: NT threads x NREG slots cover the tile; load items <= 4
     threads = 0;
@@ -996,8 +1068,16 @@ int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
 // --------------------------------------------------------------------------
 // a-3 classify + a-4 choose + a-5 materialise
 // --------------------------------------------------------------------------
+static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
+                                 OccupancyFn occ, TileMemo* sharedMemo);
+
 tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
                         OccupancyFn occ) {
+    return choose_plan_m(plan, dev, opts, occ, nullptr);
+}
+
+static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_plan_options_t* opts,
+                                 OccupancyFn occ, TileMemo* sharedMemo) {
     const Problem& pr = plan.prob;
     KernelChoice& kc = plan.kc;
     const int forced = opts ? opts->kernel : TT_KERNEL_AUTO;
@@ -1166,20 +1246,20 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         std::sort(prefix.begin(), prefix.end());
         prefix.erase(std::unique(prefix.begin(), prefix.end()), prefix.end());
     }
-    TileCand best;
+    TileSumm best;
     const int forceThreads = opts ? opts->threads : 0;
     const int forceR = opts ? opts->slots : 0;
-    TileMemo memo;
-    memo.e.reserve(256);
-    auto search = [&](const std::vector<int64_t>& tin, const std::vector<int64_t>& tout, TileCand& b) {
+    TileMemo localMemo;
+    TileMemo& memo = sharedMemo ? *sharedMemo : localMemo;
+    auto search = [&](const std::vector<int64_t>& tin, const std::vector<int64_t>& tout, TileSumm& b) {
         for (int64_t ti : tin) {
             for (int64_t to : tout) {
                 int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
                 int64_t Tout = opts && opts->run_out ? opts->run_out : to;
-                const TileCand& c = memo.get(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                             VmaxSd);
+                const TileSumm c = memo.get(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                            VmaxSd);
                 if (!c.ok) continue;
-                if (!b.ok || c.cost_us < b.cost_us) b = c;
+                if (!b.ok || c.cost < b.cost) b = c;
             }
         }
     };
@@ -1189,11 +1269,11 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         all.insert(all.end(), prefix.begin(), prefix.end());
         std::sort(all.begin(), all.end());
         all.erase(std::unique(all.begin(), all.end()), all.end());
-        TileCand px;
+        TileSumm px;
         search(all, all, px);
         const bool keepsOut = best.ok && px.ok && px.runOut >= best.runOut &&
                               (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
-        if (px.ok && (!best.ok || (px.cost_us < best.cost_us && keepsOut)))
+        if (px.ok && (!best.ok || (px.cost < best.cost && keepsOut)))
             best = px;
     }
     if (VmaxSdRule > 0 && !(opts && (opts->run_in || opts->run_out)) && best.ok) {
@@ -1209,58 +1289,63 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         }
         std::sort(all.begin(), all.end());
         all.erase(std::unique(all.begin(), all.end()), all.end());
-        TileCand sx;
+        TileSumm sx;
         for (int64_t ti : all)
             for (int64_t to : all) {
-                const TileCand& c = memo.get(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                             VmaxSdRule);
-                if (c.ok && (!sx.ok || c.cost_us < sx.cost_us)) sx = c;
+                const TileSumm c = memo.get(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                                            VmaxSdRule);
+                if (c.ok && (!sx.ok || c.cost < sx.cost)) sx = c;
             }
         const bool keepsOut = sx.ok && sx.runOut >= best.runOut &&
                               (2 * sx.runIn >= best.runIn || sx.runOut >= 2 * best.runOut);
-        if (sx.ok && sx.cost_us < best.cost_us && keepsOut) best = sx;
+        if (sx.ok && sx.cost < best.cost && keepsOut) best = sx;
     }
-    if (!best.ok) {
+    TileCand bestTile;
+    if (best.ok)  // the winner in full
+        bestTile = build_tile(pr, best.Tin, best.Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
+                              best.VmaxSd);
+    if (!bestTile.ok) {
         // fall back to the smallest legal tile
-        for (int64_t t = 64; t >= 2 && !best.ok; t /= 2) {
+        for (int64_t t = 64; t >= 2 && !bestTile.ok; t /= 2) {
             TileCand c = build_tile(pr, t, t, 12288, dev, forceThreads, acc ? 8 : 16);
-            if (c.ok) best = c;
+            if (c.ok) bestTile = c;
         }
     }
-    if (!best.ok) return TT_INTERNAL_ERROR;
+    if (!bestTile.ok) return TT_INTERNAL_ERROR;
+    const TileCand& bt = bestTile;
 
-    plan.tile = best.tp;
-    if (!best.sd) plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
+    plan.tile = bt.tp;
+    if (!bt.sd) plan.tile.sdSlot[0] = plan.tile.sdSlot[1] = -1;
     choose_smem(plan.tile, E);
     kc.kernel = TT_KERNEL_TILE;
-    kc.threads = best.threads;
-    kc.nreg = best.nreg;
+    kc.threads = bt.threads;
+    kc.nreg = bt.nreg;
     // staging pipeline: register double buffer (default) or a cp.async ring
     // of 3 stages (32-bit indices only)
-    kc.stages = (opts && opts->stages >= 3 && opts->slot_dims <= 0 && !kc.idx64 && !acc && !best.sd) ? 3 : 0;
+    kc.stages = (opts && opts->stages >= 3 && opts->slot_dims <= 0 && !kc.idx64 && !acc && !bt.sd) ? 3 : 0;
     // interleaved tiles (neighbouring tiles on concurrently running CTAs)
     // measured better than contiguous ranges on 72 of 84 suite cases
     plan.tile.interleave = (opts && opts->grid_order == 2) ? 0 : 1;
     kc.smem = (kc.stages ? kc.stages : 2) * plan.tile.sbuf * E;
     if (kc.smem > dev.max_smem_per_block) { kc.stages = 0; kc.smem = 2 * plan.tile.sbuf * E; }
     kc.vec = 1;
-    kc.predicted_us = best.cost_us;
-    kc.model_dram_eff = best.dram_eff;
-    kc.m_runIn = best.runIn;
-    kc.m_runOut = best.runOut;
-    kc.m_secIn = best.secIn;
-    kc.m_secOut = best.secOut;
-    kc.m_inflight = best.inflight;
+    kc.predicted_us = bt.cost_us;
+    kc.model_dram_eff = bt.dram_eff;
+    kc.m_runIn = bt.runIn;
+    kc.m_runOut = bt.runOut;
+    kc.m_secIn = bt.secIn;
+    kc.m_secOut = bt.secOut;
+    kc.m_inflight = bt.inflight;
     auto occOf = [&](int T, int q, int r) {
         OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem, false, 0, 0, 0, q, r};
         int v = occ ? occ(qs, dev) : 0;
         return v > 0 ? v : estimate_occupancy(qs, dev);
     };
-    if (best.sd) {
+    if (bt.sd) {
         // the model picked the slot-dim launch shape (possibly a tile larger
         // than the classic map can hold)
-        kc.sdq = best.sdq;
-        kc.sdr = best.sdr;
+        kc.sdq = bt.sdq;
+        kc.sdr = bt.sdr;
         const int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm
                                                   : occOf(kc.threads, kc.sdq, kc.sdr);
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
@@ -1269,16 +1354,16 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
                kc.idx64, 0, 0, kc.acc};
     int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
-    if (!best.sd)
+    if (!bt.sd)
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
     // The model kept the classic map: switch to the slot-dim map anyway when
     // it keeps more tiles in flight per SM with the device's real occupancy
     // (measured on the suites: the win/loss boundary), or when forced.
-    if (!best.sd) {
+    if (!bt.sd) {
         int thr = 0, sq = 0, sr = 0, perSd = 0;
         TileParams sdTile = plan.tile;
         if ((sdAllowed || (sdOpt > 0 && !acc && !kc.idx64 && (E == 4 || E == 8))) &&
-            kc.stages == 0 && build_sd(sdTile, E, best.runIn, best.runOut, occOf, thr, sq, sr, perSd) &&
+            kc.stages == 0 && build_sd(sdTile, E, bt.runIn, bt.runOut, occOf, thr, sq, sr, perSd) &&
             (sdOpt > 0 || perSd > perSm)) {
             plan.tile = sdTile;
             kc.sdq = sq;
@@ -1398,7 +1483,7 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
         tt_plan_options_t o{};
         o.slot_dims = 1;
         o.stages = 4;
-        if (choose_plan(alt, dev, &o, occ) == TT_SUCCESS && alt.kc.kernel == TT_KERNEL_TILE &&
+        if (choose_plan_m(alt, dev, &o, occ, &memo) == TT_SUCCESS && alt.kc.kernel == TT_KERNEL_TILE &&
             alt.kc.sdq && alt.kc.stages == 4) {
             OccQuery qa{TT_KERNEL_TILE, E, alt.kc.sdq * alt.kc.sdr, 4, alt.kc.threads, alt.kc.smem,
                         false, 0, 0, 0, alt.kc.sdq, alt.kc.sdr};

@@ -96,7 +96,7 @@ struct TileParams {
     int32_t vgNch;      // 16-byte chunks per run slot at the worst-case shift
     int32_t vgK;        // load items (run, chunk) per thread
     int32_t vgE;        // word bytes
-    int32_t vgTab;      // byte offset of the tile-base ring (64 x uint4) in dynamic shared memory
+    int32_t vgTab;      // byte offset of the tile-base ring (128 x uint4) + mbarriers in dynamic smem
     int32_t vgPolicy;   // cache flavour of the chunk copies (kernels_vg.cu cp_async16_pred)
     int64_t vgSpanIn;   // largest input offset inside a tile + 1 (elements)
     int64_t vgInBytes;  // bytes of the input tensor (chunks are clipped to [in, in + vgInBytes))
