@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <list>
+#include <unordered_map>
 #include <mutex>
 #include <unordered_set>
 
@@ -46,9 +48,17 @@ Plan* as_plan(tt_plan_t h) {
     return handle_live(h) ? reinterpret_cast<Plan*>(h) : nullptr;
 }
 
+static std::mutex g_dev_mu;
+static std::unordered_map<int, DeviceInfo> g_dev;
+
 tt_status_t query_device(DeviceInfo& dev) {
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TT_INVALID_DEVICE; }
+    {
+        std::lock_guard<std::mutex> g(g_dev_mu);
+        auto it = g_dev.find(d);
+        if (it != g_dev.end()) { dev = it->second; return TT_SUCCESS; }
+    }
     dev.device = d;
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
@@ -65,7 +75,89 @@ tt_status_t query_device(DeviceInfo& dev) {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxRegistersPerMultiprocessor, d) == cudaSuccess)
         dev.regs_per_sm = v;
     cudaGetLastError();
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    g_dev[d] = dev;
     return TT_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Plan cache: planning is pure host work whose result depends only on the
+// problem, the options and the device, so tt_plan of a problem seen before
+// (LRU of 64) copies the earlier decision instead of searching again -- the
+// one-shot transposes of P:L167 pay the search once per process.
+// ---------------------------------------------------------------------------
+static Plan* clone_plan(const Plan& src) {
+    Plan* p = new (std::nothrow) Plan();
+    if (p == nullptr) return nullptr;
+    p->device = src.device;
+    p->stream = src.stream;
+    p->rank = src.rank;
+    p->dims = src.dims;
+    p->perm = src.perm;
+    p->prob = src.prob;
+    p->kc = src.kc;
+    p->tile = src.tile;
+    p->row = src.row;
+    p->t2d = src.t2d;
+    p->widen = src.widen;
+    if (src.narrow) {
+        p->narrow = clone_plan(*src.narrow);
+        if (p->narrow == nullptr) { delete p; return nullptr; }
+    }
+    return p;
+}
+
+struct PlanCache {
+    std::mutex mu;
+    std::list<std::pair<std::string, Plan*>> lru;  // front = most recent
+    std::unordered_map<std::string, std::list<std::pair<std::string, Plan*>>::iterator> map;
+    static constexpr size_t kCap = 64;
+    ~PlanCache() {
+        for (auto& e : lru) destroy_plan(e.second);
+    }
+};
+static PlanCache g_cache;
+
+static std::string cache_key(int rank, const int64_t* dims, const int* perm, size_t elem_size,
+                             const DeviceInfo& dev, const tt_plan_options_t* opts) {
+    std::string k;
+    k.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+    k.append(reinterpret_cast<const char*>(&rank), sizeof(rank));
+    k.append(reinterpret_cast<const char*>(&elem_size), sizeof(elem_size));
+    k.append(reinterpret_cast<const char*>(dims), sizeof(int64_t) * rank);
+    k.append(reinterpret_cast<const char*>(perm), sizeof(int) * rank);
+    tt_plan_options_t o{};
+    if (opts) o = *opts;
+    k.append(reinterpret_cast<const char*>(&o), sizeof(o));
+    return k;
+}
+
+static Plan* cache_get(const std::string& key, void* stream) {
+    std::lock_guard<std::mutex> g(g_cache.mu);
+    auto it = g_cache.map.find(key);
+    if (it == g_cache.map.end()) return nullptr;
+    g_cache.lru.splice(g_cache.lru.begin(), g_cache.lru, it->second);
+    Plan* p = clone_plan(*it->second->second);
+    if (p) {
+        p->stream = stream;
+        if (p->narrow) p->narrow->stream = stream;
+    }
+    return p;
+}
+
+static void cache_put(const std::string& key, const Plan& plan) {
+    Plan* c = clone_plan(plan);
+    if (c == nullptr) return;
+    std::lock_guard<std::mutex> g(g_cache.mu);
+    if (g_cache.map.count(key)) { destroy_plan(c); return; }
+    g_cache.lru.emplace_front(key, c);
+    g_cache.map[key] = g_cache.lru.begin();
+    if (g_cache.lru.size() > PlanCache::kCap) {
+        auto& last = g_cache.lru.back();
+        g_cache.map.erase(last.first);
+        destroy_plan(last.second);
+        g_cache.lru.pop_back();
+    }
 }
 
 tt_status_t create_plan(Plan** out, int rank, const int64_t* dims, const int* perm,
@@ -313,7 +405,18 @@ static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, cons
                              size_t elem_size, tt_stream_t stream, const DeviceInfo& dev,
                              const tt_plan_options_t* opts, OccupancyFn occ) {
     Plan* p = nullptr;
+    const bool cacheable = dev.device >= 0;  // device plans (validated below before insertion)
+    std::string key;
+    if (cacheable) {
+        key = cache_key(rank, dims, perm, elem_size, dev, opts);
+        p = cache_get(key, stream);
+        if (p != nullptr) {
+            if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));
+            return TT_SUCCESS;
+        }
+    }
     tt_status_t st = create_plan(&p, rank, dims, perm, elem_size, stream, dev, opts, occ);
+    if (st == TT_SUCCESS && cacheable) cache_put(key, *p);
     if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }

@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <unordered_map>
 #include <unordered_set>
 
 #include "tt_internal.h"
@@ -47,6 +48,22 @@ static cudaError_t ensure_max_smem(const void* fn) {
     return e;
 }
 
+struct OccKey {
+    const void* fn;
+    int threads, smem, device;
+    bool operator==(const OccKey& o) const {
+        return fn == o.fn && threads == o.threads && smem == o.smem && device == o.device;
+    }
+};
+struct OccKeyHash {
+    size_t operator()(const OccKey& k) const {
+        return std::hash<const void*>()(k.fn) ^ ((size_t)k.threads << 1) ^ ((size_t)k.smem << 12) ^
+               ((size_t)k.device << 40);
+    }
+};
+static std::mutex g_occ_mu;
+static std::unordered_map<OccKey, int, OccKeyHash> g_occ;
+
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
     const void* fn = q.kernel == TT_KERNEL_TILE
@@ -62,6 +79,16 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
                      : q.kernel == TT_KERNEL_ROWCOPY ? pick_rowcopy(q.esize, q.idx64)
                                                      : nullptr;
     if (!fn) return 0;
+    // one CUDA query per (kernel, launch shape, device) and process: planning
+    // asks the same questions many times (candidates, re-plans)
+    int devn = 0;
+    if (cudaGetDevice(&devn) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const OccKey key{fn, q.threads, q.smem, devn};
+    {
+        std::lock_guard<std::mutex> g(g_occ_mu);
+        auto it = g_occ.find(key);
+        if (it != g_occ.end()) return it->second;
+    }
     if (ensure_max_smem(fn) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -71,6 +98,8 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
         cudaGetLastError();
         return 0;
     }
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    g_occ[key] = blocks;
     return blocks;
 }
 

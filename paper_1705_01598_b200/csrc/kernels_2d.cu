@@ -57,7 +57,10 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
     const I r0 = warp * per;
     if (r0 >= nRows) return;
     const I r1 = min(r0 + per, nRows);
-    const I L = (I)p.row;
+    // segmented rows: lane 0's digit is the segment index (planner.cpp)
+    const bool segd = p.nseg > 1;
+    const I nseg = (I)p.nseg, seg = (I)p.seg, segTail = (I)p.segTail, rowFull = (I)p.rowFull;
+    I obase = segd ? (r0 / nseg) * rowFull + (r0 % nseg) * seg : r0 * rowFull;
 
     I x = 0, d = 1, s = 0;
     if (lane < p.h) {
@@ -73,7 +76,9 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
     I base = warp_sum<I>(x * s);
     for (I r = r0; r < r1; ++r) {
         const W* __restrict__ src = opaque(in + base);
-        W* __restrict__ dst = opaque(out + r * L);
+        W* __restrict__ dst = opaque(out + obase);
+        const I segIdx = segd ? __shfl_sync(0xffffffffu, x, 0) : (I)0;
+        const I L = (segd && segIdx == nseg - 1) ? segTail : seg;
         for (I c = lane; c < L; c += 32 * U) {
             W t[U];
 #pragma unroll
@@ -90,6 +95,9 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
         if (lane < f) { delta = (I)0 - (d - 1) * s; x = 0; }
         else if (lane == f) { delta = s; x += 1; }
         base += warp_sum<I>(delta);
+        // output rows are dense in output order: the next segment, or the
+        // next row's first segment (after this row's last, segTail long)
+        obase += L;
     }
 }
 

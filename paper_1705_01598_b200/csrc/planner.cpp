@@ -1136,20 +1136,23 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
         const int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : 4;
         // Few long rows (e.g. the sharded unpack's (inner, middle, P) rows of
         // megabytes): a warp per row leaves most warps idle, so cut each row
-        // into nseg segments of `seg` elements (seg | row, seg*E >= 2 KB).
-        // Segment k of row q is a virtual row v = q*nseg + k whose output
-        // starts at v*seg -- a new fastest row dim of extent nseg and input
-        // stride seg; the kernel is unchanged.
+        // into nseg segments of `seg` elements (>= 2 KB, a multiple of 32
+        // words; the last one may be shorter), about four per warp in all.
+        // Segment k of row q is a virtual row v = q*nseg + k -- a new fastest
+        // row dim of extent nseg and input stride seg.
         const int64_t warpsTotal = (int64_t)dev.num_sms * perSm * (kc.threads / 32);
+        r.rowFull = r.row;
+        r.seg = r.segTail = r.row;
+        r.nseg = 1;
         if (r.nRows < 4 * warpsTotal && r.h < kMaxDims - 1) {
-            int64_t best = 0;
-            for (int64_t seg = r.row / 2; seg >= 1 && seg * E >= 2048; --seg) {
-                if (r.row % seg) continue;
-                best = seg;  // smallest admissible so far (most segments)
-                if (r.nRows * (r.row / seg) >= 4 * warpsTotal) break;  // largest reaching the target
-            }
-            if (best > 0) {
-                const int64_t nseg = r.row / best;
+            const int64_t want = ceil_div(4 * warpsTotal, r.nRows);
+            int64_t best = ceil_div(ceil_div(r.row, want), 32) * 32;
+            best = std::max<int64_t>(best, ceil_div(2048, E));
+            if (best < r.row) {
+                const int64_t nseg = ceil_div(r.row, best);
+                r.seg = best;
+                r.segTail = r.row - (nseg - 1) * best;
+                r.nseg = nseg;
                 for (int j = r.h; j > 0; --j) {
                     r.rC[j] = r.rC[j - 1] * nseg;
                     r.rD[j] = r.rD[j - 1];
@@ -1201,7 +1204,9 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     // opt-in); larger tiles than the classic map (16 elements x 512 / 384
     // threads, 16-bit staging offsets)
     const int sdOpt = opts ? opts->slot_dims : 0;
-    const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(opts && opts->stages >= 3 && sdOpt <= 0) &&
+    // the stages option belongs to the vector-gather kernel when that is requested
+    const int stOpt = opts && opts->vector_gather <= 0 ? opts->stages : 0;
+    const bool sdAllowed = sdOpt >= 0 && !acc && !kc.idx64 && !(stOpt >= 3 && sdOpt <= 0) &&
                            (E == 4 || (E == 8 && (sdOpt > 0 || pr.widen > 1))) &&
                            !(opts && (opts->threads || opts->slots));
     // The slot-dim shape inside the tile model (option sd_vmax > 0, tiles up
@@ -1322,7 +1327,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     kc.nreg = bt.nreg;
     // staging pipeline: register double buffer (default) or a cp.async ring
     // of 3 stages (32-bit indices only)
-    kc.stages = (opts && opts->stages >= 3 && opts->slot_dims <= 0 && !kc.idx64 && !acc && !bt.sd) ? 3 : 0;
+    kc.stages = (stOpt >= 3 && opts->slot_dims <= 0 && !kc.idx64 && !acc && !bt.sd) ? 3 : 0;
     // interleaved tiles (neighbouring tiles on concurrently running CTAs)
     // measured better than contiguous ranges on 72 of 84 suite cases
     plan.tile.interleave = (opts && opts->grid_order == 2) ? 0 : 1;
@@ -1379,7 +1384,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     // off by default (suites: mixed, up to 1.18x faster
     // and 1.3x slower case by case, profiles/round1_ab_sd_async.txt).
     if (kc.sdq && !acc && !kc.idx64) {
-        const int S = (opts && opts->slot_dims > 0 && opts->stages >= 3) ? opts->stages : 0;
+        const int S = (opts && opts->slot_dims > 0 && stOpt >= 3) ? stOpt : 0;
         if ((S == 3 || S == 4) && (int64_t)S * plan.tile.sbuf * E <= dev.max_smem_per_block) {
             kc.stages = S;
             kc.smem = S * plan.tile.sbuf * E;
@@ -1394,8 +1399,19 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     }
     // vector-gather load phase (tile_vg_kernel): 16-byte cp.async chunks of
     // the aligned superset of every input run, S-stage ring
-    const int vgOpt = opts ? opts->vector_gather : 0;
-    if (vgOpt > 0 && !acc && !kc.idx64) {
+    // Default: fastest dimension unchanged after fusion (perm[0] == 0, rows
+    // too short for the row copy) on 4-byte words or 8-byte words widened
+    // from 4-byte pairs.  Same-box A/B (profiles/round2_ab_vg*.jsonl): on
+    // those suite cases median 1.04x, up to 1.51x on the worst suite case
+    // (5^12 fp32), losses down to 0.83x where the heuristic's output runs are
+    // very long; on fp64 elements and on perm[0] != 0 gathers it lost.
+    static const tt_plan_options_t zeroO{};
+    const bool noOptsVg = opts == nullptr || std::memcmp(opts, &zeroO, sizeof(zeroO)) == 0;
+    const int vgOpt = opts ? opts->vector_gather
+                           : 0;
+    const bool vgDefault = noOptsVg && pr.dense && pr.n >= 2 && pr.p[0] == 0 &&
+                           (E == 4 || (E == 8 && pr.widen > 1));
+    if ((vgOpt > 0 || vgDefault) && !acc && !kc.idx64) {
         TileParams vt = plan.tile;
         vt.sdSlot[0] = vt.sdSlot[1] = -1;
         const int S = opts && opts->stages >= 3 ? std::min(4, opts->stages) : 4;
@@ -1552,6 +1568,8 @@ std::string describe_json(const Plan& plan) {
     if (kc.kernel == TT_KERNEL_ROWCOPY) {
         const RowParams& r = plan.row;
         o << ",\"rowcopy\":{\"row\":" << (long long)r.row << ",\"nRows\":" << (long long)r.nRows
+          << ",\"row_full\":" << (long long)r.rowFull << ",\"seg\":" << (long long)r.seg
+          << ",\"seg_tail\":" << (long long)r.segTail << ",\"nseg\":" << (long long)r.nseg
           << ",\"row_c\":";
         arr(o, r.rC, r.h);
         o << ",\"row_d\":";

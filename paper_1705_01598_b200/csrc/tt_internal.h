@@ -106,8 +106,15 @@ struct TileParams {
 // row of `row` contiguous elements is contiguous on both sides.  Rows are
 // enumerated in OUTPUT order over the remaining dims.
 struct RowParams {
-    int64_t row;        // elements per row (fused dim 0); output row r starts at r*row
-    int64_t nRows;
+    int64_t row;        // elements per (virtual) row; = seg when rows are segmented
+    int64_t nRows;      // virtual rows (segments x rows)
+    // Segmented rows (few long rows): digit 0 of the row odometer is the
+    // segment index (extent nseg, input stride seg); segment k of a row is
+    // [k*seg, min((k+1)*seg, rowFull)), the last one segTail long.  Output
+    // row r starts at (r / nseg) * rowFull + (r % nseg) * seg.
+    int64_t rowFull;    // elements of a whole row (fused dim 0)
+    int64_t seg, segTail;
+    int64_t nseg;       // 1: not segmented
     int32_t h;          // remaining dims (output dims 1..n-1, output order)
     int64_t rC[kMaxDims];     // cumulative row count in output order
     int64_t rD[kMaxDims];     // extent

@@ -175,11 +175,14 @@ def interpret_rowcopy_plan(j, words):
     """Replay the row-copy kernel: output row r = contiguous input row at
     sum_j digit_j(r) * row_sin[j]."""
     t = j["rowcopy"]
-    L, n = t["row"], t["nRows"]
-    out = np.zeros(L * n, dtype=words.dtype)
+    n, full, seg, tail, nseg = t["nRows"], t["row_full"], t["seg"], t["seg_tail"], t["nseg"]
+    out = np.zeros(full * (n // nseg), dtype=words.dtype)
     for r in range(n):
         base = sum(((r // c) % d) * s for c, d, s in zip(t["row_c"], t["row_d"], t["row_sin"]))
-        out[r * L:(r + 1) * L] = words[base:base + L]
+        k = r % nseg                      # segment of the row (digit 0 when segmented)
+        L = tail if (nseg > 1 and k == nseg - 1) else seg
+        o = (r // nseg) * full + k * seg
+        out[o:o + L] = words[base:base + L]
     return out
 
 

@@ -352,19 +352,32 @@ def test_strided_plan_validation():
     ((6144, 5, 3), (0, 2, 1), 4),        # 15 rows of 24 KB -> segmented
     ((2048, 3, 7), (0, 2, 1), 8),        # 21 rows of 16 KB
     ((1536, 4, 3, 2), (0, 3, 1, 2), 4),
-    ((4099, 3, 2), (0, 2, 1), 4),        # prime row: no admissible segment
+    ((4099, 3, 2), (0, 2, 1), 4),        # prime row: ragged last segment
+    ((100003, 3, 2), (0, 2, 1), 4),      # prime row of 400 KB: many segments + a tail
 ])
 def test_rowcopy_segmented_rows_match_oracle(dims, perm, esize):
-    """Few long rows are cut into segments (a new fastest row dim); the
-    replayed plan must still equal the oracle."""
+    """Few long rows are cut into segments (a new fastest row dim, the last
+    segment of a row possibly shorter); the replayed plan must still equal
+    the oracle."""
     j = tt.plan_offline(dims, perm, esize)
     assert j["kernel"] == "rowcopy"
     r = j["rowcopy"]
     vol = int(np.prod(dims))
-    if dims[0] != 4099:
-        assert r["nRows"] > vol // dims[0] and r["row"] * j["word_size"] >= 2048
+    assert r["nseg"] > 1 and r["nRows"] > vol // dims[0] and r["seg"] * j["word_size"] >= 2048
+    assert (r["nseg"] - 1) * r["seg"] + r["seg_tail"] == r["row_full"] and 0 < r["seg_tail"] <= r["seg"]
     words = wl.random_words(vol, esize, 78)
     np.testing.assert_array_equal(interpret_plan(j, words), orc.permute(dims, perm, words))
+
+
+def test_rowcopy_planning_is_constant_time_for_huge_prime_rows():
+    """the segment search was a linear divisor scan (4 s for a
+    row of 2^31 - 19 elements); segments are now computed directly."""
+    import time
+    t0 = time.perf_counter()
+    j = tt.plan_offline((2147483629, 2, 2), (0, 2, 1), 4)
+    assert time.perf_counter() - t0 < 0.5
+    r = j["narrow"]["rowcopy"] if "narrow" in j else j["rowcopy"]
+    assert r["nseg"] > 1 and r["grid" if False else "nRows"] >= 4 * 148
 
 
 # Shapes where the measured classification thresholds decide (DESIGN.md,
