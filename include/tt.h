@@ -248,6 +248,14 @@ const char* tt_status_string(tt_status_t s);
 /* TT_VERSION of the loaded library. */
 int tt_version(void);
 
+/* Planner log: level >= 1 prints one line per plan created (fused problem,
+ * kernel family and variant, launch shape, model prediction, planning time,
+ * plan-cache hits) to stderr; 0 (default) is silent.  Returns the previous
+ * level.  (The Python binding sets it from the TT_LOG environment variable.)
+ * The library also marks tt_plan / tt_execute / the sharded phases as NVTX
+ * ranges for timeline tools. */
+int tt_set_log_level(int level);
+
 /* ------------------------------------------------------------------------
  * Multi-GPU (one box, one process per GPU).  The paper has no multi-GPU
  * transpose ("we will only consider local tensor transposes"); this is

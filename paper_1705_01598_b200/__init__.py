@@ -113,6 +113,10 @@ def _load():
     L.tt_status_string.restype = ctypes.c_char_p
     L.tt_version.argtypes = []
     L.tt_version.restype = ctypes.c_int
+    L.tt_set_log_level.argtypes = [ctypes.c_int]
+    L.tt_set_log_level.restype = ctypes.c_int
+    if os.environ.get("TT_LOG"):
+        L.tt_set_log_level(int(os.environ["TT_LOG"]))
     return L
 
 

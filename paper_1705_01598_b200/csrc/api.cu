@@ -15,11 +15,41 @@
 #include <mutex>
 #include <unordered_set>
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <atomic>
+#include <chrono>
+
 #include "tt_internal.h"
 
 using namespace tt;
 
 namespace tt {
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+
+static std::atomic<int> g_log_level{0};
+int log_level() { return g_log_level.load(std::memory_order_relaxed); }
+
+void log_plan(const Plan& p, double us, bool cached) {
+    const Problem& pr = p.prob;
+    const KernelChoice& kc = p.kc;
+    std::string f = "[";
+    for (int i = 0; i < pr.n; ++i) f += (i ? "," : "") + std::to_string(pr.d[i]);
+    f += "] perm [";
+    for (int i = 0; i < pr.n; ++i) f += (i ? "," : "") + std::to_string(pr.p[i]);
+    f += "]";
+    const char* k = kc.kernel == TT_KERNEL_COPY ? "copy" : kc.kernel == TT_KERNEL_ROWCOPY ? "rowcopy"
+                    : kc.kernel == TT_KERNEL_TILED2D ? "tiled2d" : "tile";
+    const char* var = kc.kernel != TT_KERNEL_TILE ? "" : kc.vg ? "/vector-gather" : kc.sdq ? "/slot-dim" : "/classic";
+    std::fprintf(stderr,
+                 "[tt] plan rank %d E %d -> fused %s word %dB: %s%s threads %d grid %d smem %d slots %d "
+                 "stages %d tile V %d predicted %.1f us, planned in %.1f us%s\n",
+                 p.rank, pr.esize / p.widen, f.c_str(), pr.esize, k, var, kc.threads, kc.grid, kc.smem,
+                 kc.nreg, kc.stages, kc.kernel == TT_KERNEL_TILE ? p.tile.V : 0, kc.predicted_us, us,
+                 cached ? " (plan cache)" : "");
+}
 
 static std::mutex g_handles_mu;
 static std::unordered_set<const void*> g_handles;
@@ -404,6 +434,11 @@ void destroy_plan(Plan* p) {
 static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, const int* perm,
                              size_t elem_size, tt_stream_t stream, const DeviceInfo& dev,
                              const tt_plan_options_t* opts, OccupancyFn occ) {
+    NvtxRange nv("tt_plan");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto us = [&]() {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    };
     Plan* p = nullptr;
     const bool cacheable = dev.device >= 0;  // device plans (validated below before insertion)
     std::string key;
@@ -411,11 +446,13 @@ static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, cons
         key = cache_key(rank, dims, perm, elem_size, dev, opts);
         p = cache_get(key, stream);
         if (p != nullptr) {
+            if (log_level() > 0) log_plan(*p, us(), true);
             if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));
             return TT_SUCCESS;
         }
     }
     tt_status_t st = create_plan(&p, rank, dims, perm, elem_size, stream, dev, opts, occ);
+    if (st == TT_SUCCESS && log_level() > 0) log_plan(*p, us(), false);
     if (st == TT_SUCCESS && cacheable) cache_put(key, *p);
     if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
@@ -438,6 +475,10 @@ static tt_status_t check_exec(Plan* p, const void* in, void* out) {
 extern "C" {
 
 int tt_version(void) { return TT_VERSION; }
+
+int tt_set_log_level(int level) {
+    return g_log_level.exchange(level < 0 ? 0 : level);
+}
 
 const char* tt_status_string(tt_status_t s) {
     switch (s) {
@@ -676,6 +717,7 @@ tt_status_t tt_plan_strided_offline(tt_plan_t* plan, int rank, const int64_t* di
 }
 
 tt_status_t tt_execute(tt_plan_t plan, const void* in, void* out) {
+    NvtxRange nv("tt_execute");
     Plan* p = as_plan(plan);
     tt_status_t st = check_exec(p, in, out);
     if (st != TT_SUCCESS) return st;

@@ -592,6 +592,7 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
         // failed execute cannot leave this rank one barrier behind its peers
         const int base = s->epoch;
         s->epoch += 2;
+        NvtxRange nv("tt_execute_sharded p2p (barrier, fused stores, barrier)");
         cudaEventRecord(s->ev[0], st);
         if (launch_barrier(s, st, base + 1) != 0) return TT_CUDA_ERROR;
         cudaEventRecord(s->ev[1], st);
@@ -604,13 +605,22 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
         return TT_SUCCESS;
     }
     cudaEventRecord(s->ev[0], st);
-    if (launch_plan(*s->pack, in_local, s->send, p->stream) != 0) return TT_CUDA_ERROR;
+    {
+        NvtxRange nv("tt_execute_sharded pack");
+        if (launch_plan(*s->pack, in_local, s->send, p->stream) != 0) return TT_CUDA_ERROR;
+    }
     cudaEventRecord(s->ev[1], st);
     const ncclDataType_t dt = s->esize == 4 ? ncclUint32 : ncclUint64;
-    if (ncclAlltoAll(s->send, s->recv, s->a2a_count, dt, s->comm->nccl, st) != ncclSuccess)
-        return TT_NCCL_ERROR;
+    {
+        NvtxRange nv("tt_execute_sharded all-to-all");
+        if (ncclAlltoAll(s->send, s->recv, s->a2a_count, dt, s->comm->nccl, st) != ncclSuccess)
+            return TT_NCCL_ERROR;
+    }
     cudaEventRecord(s->ev[2], st);
-    if (launch_plan(*s->unpack, s->recv, out_local, p->stream) != 0) return TT_CUDA_ERROR;
+    {
+        NvtxRange nv("tt_execute_sharded unpack");
+        if (launch_plan(*s->unpack, s->recv, out_local, p->stream) != 0) return TT_CUDA_ERROR;
+    }
     cudaEventRecord(s->ev[3], st);
     s->timed = true;
     return TT_SUCCESS;

@@ -225,6 +225,16 @@ tt_status_t choose_plan(Plan& plan, const DeviceInfo& dev, const tt_plan_options
 std::string describe_json(const Plan& plan);
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev);
 
+// Observability (api.cu): NVTX ranges around plan / execute / the sharded
+// phases (visible in Nsight timelines), and one log line per planner
+// decision on stderr when tt_set_log_level(1) was called.
+struct NvtxRange {
+    explicit NvtxRange(const char* name);
+    ~NvtxRange();
+};
+int log_level();
+void log_plan(const Plan& p, double us, bool cached);
+
 // api.cu --------------------------------------------------------------------
 // Live-handle registry: every handle the ABI hands out (plans, contractions,
 // communicators) is registered; entry points accept a handle only while it is

@@ -397,3 +397,22 @@ def test_classification_thresholds(dims, perm, esize, kernel):
     assert j["kernel"] == kernel
     words = wl.random_words(int(np.prod(dims)), esize, 91)
     np.testing.assert_array_equal(interpret_plan(j, words), orc.permute(dims, perm, words))
+
+
+def test_planner_log_lines():
+    """tt_set_log_level(1) (TT_LOG=1 in the binding) prints one line per plan
+    decision to stderr; level 0 is silent."""
+    import subprocess
+    import sys
+    code = ("import paper_1705_01598_b200 as tt\n"
+            "tt.plan_offline((5,)*12, (0,8,4,10,1,3,9,5,7,2,6,11), 4)\n"
+            "tt.plan_offline((64, 63), (1, 0), 8)\n")
+    env = dict(os.environ, TT_LOG="1", PYTHONPATH=ROOT)
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    lines = [l for l in p.stderr.splitlines() if l.startswith("[tt] plan")]
+    assert p.returncode == 0 and len(lines) == 2, p.stderr
+    assert "vector-gather" in lines[0] and "tiled2d" in lines[1]
+    env["TT_LOG"] = "0"
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert "[tt] plan" not in p.stderr
+    assert tt.lib.tt_set_log_level(0) in (0, 1)
