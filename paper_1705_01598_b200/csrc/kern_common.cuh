@@ -141,8 +141,8 @@ struct GridWalker {
     int h, lane;
 
     template <typename P>
-    __device__ __forceinline__ GridWalker(const P& p, int lane_) : lane(lane_) {
-        h = p.h;
+    __device__ __forceinline__ GridWalker(const P& p, int lane_, bool enabled = true) : lane(lane_) {
+        h = enabled ? p.h : 0;
         d = 1; sIn = 0; sOut = 0; x = 0; cC = 1;
         mC = 1; lC = 0; mD = 1; lD = 0;
         splitBit = 0;
@@ -211,6 +211,34 @@ struct GridWalker {
         return b;
     }
 };
+
+// Tile-base entry of one tile (Algorithm 1 over the grid dims, P:L84-103,
+// computed by one lane with multiply-shift division): x = input offset, y =
+// output offset, z = ragged state (2 bits) | interior << 2 (vector-gather
+// plans: the tile's 16-byte chunks stay >= 32 bytes inside the input).
+// Kernels with an interleaved tile schedule (tile t0 + it*G) keep these in a
+// shared ring filled 32 tiles at a time by one warp, so a tile costs every
+// warp one 16-byte shared load instead of a warp-wide Algorithm-1 decode.
+__device__ __forceinline__ uint4 tile_entry(const TileParams& p, uint32_t t) {
+    uint32_t vin = 0, vout = 0, need = 0;
+    for (int g = 0; g < p.h; ++g) {
+        const uint32_t q1 = fast_div(t, p.gMC[g], p.gLC[g]);
+        const uint32_t x = q1 - fast_div(q1, p.gMD[g], p.gLD[g]) * (uint32_t)p.gD[g];
+        vin += x * (uint32_t)p.gSin[g];
+        vout += x * (uint32_t)p.gSout[g];
+        if (x == (uint32_t)p.gD[g] - 1) {
+            if (p.nSplit > 0 && g == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) need |= 1u;
+            if (p.nSplit > 1 && g == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]) need |= 2u;
+        }
+    }
+    uint32_t interior = 0;
+    if (p.vgE > 0) {
+        const int64_t lo = (int64_t)vin * p.vgE;
+        const int64_t hi = ((int64_t)vin + p.vgSpanIn) * p.vgE;
+        interior = (lo >= 32 && hi + 32 <= p.vgInBytes) ? 4u : 0u;
+    }
+    return make_uint4(vin, vout, need | interior, 0u);
+}
 
 // Stateless Algorithm-1 decode for the 2-D kernels' interleaved tile order:
 // each lane reads its grid dim's values from the parameter block per tile.

@@ -32,7 +32,19 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
     const uint32_t G = (uint32_t)gridDim.x;
     const uint32_t t0 = (uint32_t)blockIdx.x;
     if (t0 >= nTiles) return;
-    GridWalker<uint32_t> walk(p, lane);
+    const uint32_t nIt = (nTiles - t0 + G - 1) / G;  // tiles t0 + it*G
+    uint4* const ring = reinterpret_cast<uint4*>(smem_raw + p.ringOff);
+    if ((tid >> 5) == 0)
+        for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32) ring[it] = tile_entry(p, t0 + it * G);
+    __syncthreads();
+    auto base = [&](uint32_t it) {
+        const uint4 e = ring[it & 63u];
+        TileBase<uint32_t> b;
+        b.in = e.x;
+        b.out = e.y;
+        b.need = e.z & 3u;
+        return b;
+    };
 
     W v[QM][RM];
     auto load = [&](const TileBase<uint32_t>& tb) {
@@ -52,11 +64,11 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             }
         }
     };
-    TileBase<uint32_t> cur = walk.seek(t0);
+    TileBase<uint32_t> cur = base(0);
     load(cur);
 
     uint32_t sb = sm0;
-    for (uint32_t t = t0; t < nTiles; t += G) {
+    for (uint32_t it = 0; it < nIt; ++it) {
         // stage the tile (input-side map)
         {
             const uint32_t sh = 8u * cur.need;
@@ -71,9 +83,13 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             }
         }
         __syncthreads();
+        if ((it & 31u) == 0 && it >= 32u && (tid >> 5) == 0) {  // bases of tiles it+32 .. it+63
+            const uint32_t j = it + 32u + (uint32_t)lane;
+            if (j < nIt) ring[j & 63u] = tile_entry(p, t0 + j * G);
+        }
         const TileBase<uint32_t> now = cur;
-        if (t + G < nTiles) {
-            cur = walk.seek(t + G);
+        if (it + 1 < nIt) {
+            cur = base(it + 1);
             load(cur);
         }
         // transposed read of the staged tile, coalesced writes (output-side map)
@@ -135,11 +151,23 @@ tile_sd_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__
     const uint32_t G = (uint32_t)gridDim.x;
     const uint32_t t0 = (uint32_t)blockIdx.x;
     if (t0 >= nTiles) return;
-    GridWalker<uint32_t> walk(p, lane);
+    const uint32_t nIt = (nTiles - t0 + G - 1) / G;  // tiles t0 + it*G
+    uint4* const ring = reinterpret_cast<uint4*>(smem_raw + p.ringOff);
+    if ((tid >> 5) == 0)
+        for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32) ring[it] = tile_entry(p, t0 + it * G);
+    __syncthreads();
+    auto base = [&](uint32_t it) {
+        const uint4 e = ring[it & 63u];
+        TileBase<uint32_t> b;
+        b.in = e.x;
+        b.out = e.y;
+        b.need = e.z & 3u;
+        return b;
+    };
 
-    // load phase of tile t into the staging buffer at byte address sb
-    auto issue = [&](uint32_t t, uint32_t sb) {
-        const TileBase<uint32_t> tb = walk.seek(t);
+    // load phase of iteration it into the staging buffer at byte address sb
+    auto issue = [&](uint32_t it, uint32_t sb) {
+        const TileBase<uint32_t> tb = base(it);
         const uint32_t sh = 8u * tb.need;
 #pragma unroll
         for (int q = 0; q < QM; ++q) {
@@ -154,23 +182,26 @@ tile_sd_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__
     };
 #pragma unroll
     for (int s = 0; s < S - 1; ++s) {
-        const uint32_t t = t0 + (uint32_t)s * G;
-        if (t < nTiles) issue(t, sm0 + (uint32_t)s * sbytes);
+        if ((uint32_t)s < nIt) issue((uint32_t)s, sm0 + (uint32_t)s * sbytes);
         cp_async_commit();
     }
     uint32_t k = 0;
-    for (uint32_t t = t0; t < nTiles; t += G) {
+    for (uint32_t it = 0; it < nIt; ++it) {
         cp_async_wait<S - 2>();
         __syncthreads();
+        if ((it & 31u) == 0 && it >= 32u && (tid >> 5) == 0) {  // bases of tiles it+32 .. it+63
+            const uint32_t j = it + 32u + (uint32_t)lane;
+            if (j < nIt) ring[j & 63u] = tile_entry(p, t0 + j * G);
+        }
         // refill the stage read in the previous iteration (all threads are
         // past its reads: they passed this iteration's barrier)
         {
-            const uint32_t tn = t + (uint32_t)(S - 1) * G;
+            const uint32_t itn = it + (uint32_t)(S - 1);
             const uint32_t kn = (k + S - 1) % S;
-            if (tn < nTiles) issue(tn, sm0 + kn * sbytes);
+            if (itn < nIt) issue(itn, sm0 + kn * sbytes);
             cp_async_commit();
         }
-        const TileBase<uint32_t> now = walk.seek(t);
+        const TileBase<uint32_t> now = base(it);
         const uint32_t sb = sm0 + k * sbytes;
         const uint32_t sh = 8u * now.need;
 #pragma unroll

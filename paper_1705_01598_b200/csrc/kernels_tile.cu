@@ -13,7 +13,8 @@ namespace tt {
 // ragged A-chunk, ... B-chunk); a slot is valid in a ragged tile iff its bits
 // cover the tile's `need`.
 template <typename W, int NREG, typename I, int ACC = 0>
-__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512, (NREG >= 16 ? 2 : (sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
+__global__ void __launch_bounds__(NREG >= 16 ? 256 : 512,
+                                  (NREG >= 16 ? 2 : (ACC || sizeof(I) == 8 || (NREG >= 8 && sizeof(W) >= 8) ? 1 : 2)))
 tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -45,7 +46,27 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
     const I t1 = il ? nTiles : (I)(((uint64_t)nTiles * (blockIdx.x + 1)) / G);
     const I step = il ? G : (I)1;
     if (t0 >= t1) return;
-    GridWalker<I> walk(p, lane);
+    // tile bases: 32-bit plans read them from a shared ring (tile_entry,
+    // 32 tiles decoded at a time by one warp); 64-bit plans keep the
+    // warp-parallel walker
+    constexpr bool kRingBases = sizeof(I) == 4;
+    const uint32_t nIt = (uint32_t)((t1 - t0 + step - 1) / step);
+    uint4* const ring = reinterpret_cast<uint4*>(smem_raw + p.ringOff);
+    if constexpr (kRingBases) {
+        if ((tid >> 5) == 0)
+            for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32)
+                ring[it] = tile_entry(p, (uint32_t)t0 + it * (uint32_t)step);
+        __syncthreads();
+    }
+    auto ring_base = [&](uint32_t it) {
+        const uint4 e = ring[it & 63u];
+        TileBase<I> b;
+        b.in = (I)e.x;
+        b.out = (I)e.y;
+        b.need = e.z & 3u;
+        return b;
+    };
+    GridWalker<I> walk(p, lane, !kRingBases);
 
     W v[NREG];
     auto load = [&](const TileBase<I>& tb) {
@@ -74,12 +95,15 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (m & (1u << r)) ov[r] = ldgo_(elem_addr(o, gout[r]));
         }
     };
-    TileBase<I> cur = walk.seek(t0);
+    TileBase<I> cur;
+    if constexpr (kRingBases) cur = ring_base(0);
+    else cur = walk.seek(t0);
     load(cur);
     load_out(cur);
 
     uint32_t sb = sm0;
-    for (I t = t0; t < t1; t += step) {
+    uint32_t it = 0;
+    for (I t = t0; t < t1; t += step, ++it) {
         // stage the tile in input order
         if (allSlots) {
 #pragma unroll
@@ -90,10 +114,17 @@ tile_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* _
                 if (r < nmine) sts(sb + (spk[r] & 0xffffu), v[r]);
         }
         __syncthreads();
+        if constexpr (kRingBases) {
+            if ((it & 31u) == 0 && it >= 32u && (tid >> 5) == 0) {  // bases of tiles it+32 .. it+63
+                const uint32_t j = it + 32u + (uint32_t)lane;
+                if (j < nIt) ring[j & 63u] = tile_entry(p, (uint32_t)t0 + j * (uint32_t)step);
+            }
+        }
         // issue the next tile's global loads before writing this one
         const TileBase<I> now = cur;
         if (t + step < t1) {
-            cur = il ? walk.seek(t + step) : walk.next(cur);
+            if constexpr (kRingBases) cur = ring_base(it + 1);
+            else cur = il ? walk.seek(t + step) : walk.next(cur);
             load(cur);
         }
         // transposed read of shared memory (Eq. 6), coalesced writes (Eq. 5)
@@ -217,7 +248,6 @@ const void* pick_tile_acc(int esize, int nreg) {
         case 2: return (const void*)&tile_kernel<W, 2, uint32_t, 1>;               \
         case 4: return (const void*)&tile_kernel<W, 4, uint32_t, 1>;               \
         case 8: return (const void*)&tile_kernel<W, 8, uint32_t, 1>;               \
-        case 16: return (const void*)&tile_kernel<W, 16, uint32_t, 1>;             \
         default: return nullptr;                                                    \
     }
     if (esize == 4) { TT_PICKACC(uint32_t) }
@@ -236,10 +266,21 @@ const void* pick_tile(int esize, int nreg, bool idx64) {
         case 16: return tile_fn<W, 16, I>();        \
         default: return nullptr;                    \
     }
+#define TT_PICK8(W, I)                              \
+    switch (nreg) {                                 \
+        case 1: return tile_fn<W, 1, I>();          \
+        case 2: return tile_fn<W, 2, I>();          \
+        case 4: return tile_fn<W, 4, I>();          \
+        case 8: return tile_fn<W, 8, I>();          \
+        default: return nullptr;                    \
+    }
+    // 16 slots only with 32-bit indices (the planner never pairs them with
+    // 64-bit indices: 256-thread CTAs could not hold the tables)
+    if (idx64 && nreg > 8) return nullptr;
     if (esize == 4) {
-        if (idx64) { TT_PICK(uint32_t, int64_t) } else { TT_PICK(uint32_t, uint32_t) }
+        if (idx64) { TT_PICK8(uint32_t, int64_t) } else { TT_PICK(uint32_t, uint32_t) }
     } else if (esize == 8) {
-        if (idx64) { TT_PICK(uint64_t, int64_t) } else { TT_PICK(uint64_t, uint32_t) }
+        if (idx64) { TT_PICK8(uint64_t, int64_t) } else { TT_PICK(uint64_t, uint32_t) }
     } else if (esize == 16) {  // widened words: at most 4 slots (register budget)
         switch (nreg) {
             case 1: return idx64 ? tile_fn<uint4, 1, int64_t>() : tile_fn<uint4, 1, uint32_t>();
@@ -249,6 +290,7 @@ const void* pick_tile(int esize, int nreg, bool idx64) {
         }
     }
     return nullptr;
+#undef TT_PICK8
 #undef TT_PICK
 }
 

@@ -94,27 +94,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     } while (!done);
 }
 
-// Tile-base entry of one tile (Algorithm 1 over the grid dims, one lane):
-// x = input offset, y = output offset, z = ragged state (2 bits) | interior
-// (the tile's 16-byte chunks stay >= 32 bytes inside the input) << 2.
-__device__ __forceinline__ uint4 vg_tile_entry(const TileParams& p, uint32_t t) {
-    uint32_t vin = 0, vout = 0, need = 0;
-    for (int g = 0; g < p.h; ++g) {
-        const uint32_t q1 = fast_div(t, p.gMC[g], p.gLC[g]);
-        const uint32_t x = q1 - fast_div(q1, p.gMD[g], p.gLD[g]) * (uint32_t)p.gD[g];
-        vin += x * (uint32_t)p.gSin[g];
-        vout += x * (uint32_t)p.gSout[g];
-        if (x == (uint32_t)p.gD[g] - 1) {
-            if (p.nSplit > 0 && g == p.splitLane[0] && p.splitTail[0] != p.splitChunk[0]) need |= 1u;
-            if (p.nSplit > 1 && g == p.splitLane[1] && p.splitTail[1] != p.splitChunk[1]) need |= 2u;
-        }
-    }
-    const int64_t lo = (int64_t)vin * p.vgE;
-    const int64_t hi = ((int64_t)vin + p.vgSpanIn) * p.vgE;
-    const uint32_t interior = (lo >= 32 && hi + 32 <= p.vgInBytes) ? 4u : 0u;
-    return make_uint4(vin, vout, need | interior, 0u);
-}
-
 template <typename W, int NREG, int K, int S>
 __global__ void __launch_bounds__(NREG >= 16 ? 512 : 1024, 1)
 tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
@@ -210,7 +189,7 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
     }
     if (warp == 0) {  // tile bases of iterations 0..63
         for (uint32_t it = (uint32_t)lane; it < 64u && it < nIt; it += 32)
-            ring[it] = vg_tile_entry(p, t0 + it * G);
+            ring[it] = tile_entry(p, t0 + it * G);
     }
     __syncthreads();
 
@@ -276,7 +255,7 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
         mbar_wait(fullB + 8u * stage, (it / S) & 1u);   // tile it has landed in its stage
         if ((it & 31u) == 0 && it >= 32u && warp == 0) {  // tile bases of iterations it+32 .. it+63
             const uint32_t j = it + 32u + (uint32_t)lane;
-            if (j < nIt) ring[j & 127u] = vg_tile_entry(p, t0 + j * G);
+            if (j < nIt) ring[j & 127u] = tile_entry(p, t0 + j * G);
         }
         // transposed read of the staged tile (Eq. 6), coalesced writes (Eq. 5)
         {

@@ -1341,8 +1341,9 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     kc.m_secIn = bt.secIn;
     kc.m_secOut = bt.secOut;
     kc.m_inflight = bt.inflight;
+    constexpr int kRing = 64 * 16;  // slot-dim kernels: tile-base ring behind the staging buffers
     auto occOf = [&](int T, int q, int r) {
-        OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem, false, 0, 0, 0, q, r};
+        OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem + kRing, false, 0, 0, 0, q, r};
         int v = occ ? occ(qs, dev) : 0;
         return v > 0 ? v : estimate_occupancy(qs, dev);
     };
@@ -1385,9 +1386,9 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     // and 1.3x slower case by case, profiles/round1_ab_sd_async.txt).
     if (kc.sdq && !acc && !kc.idx64) {
         const int S = (opts && opts->slot_dims > 0 && stOpt >= 3) ? stOpt : 0;
-        if ((S == 3 || S == 4) && (int64_t)S * plan.tile.sbuf * E <= dev.max_smem_per_block) {
+        if ((S == 3 || S == 4) && (int64_t)S * plan.tile.sbuf * E + kRing <= dev.max_smem_per_block) {
             kc.stages = S;
-            kc.smem = S * plan.tile.sbuf * E;
+            kc.smem = S * plan.tile.sbuf * E + kRing;
             OccQuery qa{TT_KERNEL_TILE, E, kc.sdq * kc.sdr, S, kc.threads, kc.smem, false, 0, 0, 0, kc.sdq, kc.sdr};
             int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qa, dev) : 0);
             if (per <= 0)
@@ -1432,6 +1433,13 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
                                             dev.regs_per_sm / (thr * 64)}));
             kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * per));
         }
+    }
+    // tile-base ring (kernels read the bases of their tiles from it): the
+    // slot-dim kernels, and the classic register-pipeline kernel on 32-bit
+    // indices (the classic cp.async variant and 64-bit plans decode in place)
+    if (kc.kernel == TT_KERNEL_TILE && !kc.vg && (kc.sdq || (!kc.idx64 && kc.stages == 0))) {
+        plan.tile.ringOff = (kc.stages >= 3 ? kc.stages : 2) * plan.tile.sbuf * E;
+        kc.smem = plan.tile.ringOff + kRing;
     }
     kc.fb_threads = kc.threads;
     kc.fb_grid = kc.grid;

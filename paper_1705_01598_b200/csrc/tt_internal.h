@@ -83,6 +83,7 @@ struct TileParams {
     int32_t sdC[2];     // chunks of the slot dim, ceil(ext / sdR)
     int32_t sdU[2];     // thread-space size: V / ext * chunks
     int32_t sdQ[2];     // passes, ceil(sdU / threads)
+    int32_t ringOff;    // slot-dim kernels: byte offset of the 64-entry tile-base ring in dynamic smem
     // vector-gather variant (tile_vg_kernel, kernels_vg.cu): the load phase
     // copies the 16-byte-aligned superset of every input run (the tile's
     // first vgM dims, contiguous in the input) in 16-byte cp.async chunks.

@@ -1,0 +1,5 @@
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r2check3; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.txt 2>&1; tail -3 $O/pytest_gpu.txt
+( time timeout 2400 python bench.py --suites-out $O/suites_cases.jsonl > $O/bench.json 2> $O/bench.err ) 2> $O/bench_time.txt
+tail -c 1200 $O/bench.json; tail -3 $O/bench.err
