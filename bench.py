@@ -72,6 +72,8 @@ def parse(argv=None):
     ap.add_argument("--config", default="s1", choices=CONFIGS)
     ap.add_argument("--suites", default="default", choices=["default", "full", "none"])
     ap.add_argument("--suites-out", default="", help="per-case JSONL of the suites")
+    ap.add_argument("--suites-plan", default="both", choices=["heuristic", "both"],
+                    help="both: also measurement-based plans (tt_plan_measure) per suite case")
     ap.add_argument("--verify", default="full", choices=["full", "none"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -354,7 +356,11 @@ def _event_median(fn, reps, stream):
     return statistics.median(ts)
 
 
-def run_suites(tt, dev, which, reps, out_path=""):
+def _plan_key(d):
+    return json.dumps({k: v for k, v in d.items() if k not in ("measured",)}, sort_keys=True)
+
+
+def run_suites(tt, dev, which, reps, out_path="", measured=False):
     """Every case: seeded words uploaded to HBM, plan time, median of `reps`
     event-timed executes, same-bytes device copy, full memcmp against the
     oracle.  Words and oracle output of the next cases are prepared on host
@@ -405,12 +411,32 @@ def run_suites(tt, dev, which, reps, out_path=""):
         ok = memcmp_equal(got, want)
         d = plan.describe()
         plan.destroy()
+        mrow = {}
+        if measured:
+            # measurement-based plan selection (tt_plan_measure):
+            # the candidates run on these buffers, the fastest is kept
+            t0 = time.perf_counter()
+            mp = tt.Plan(c.dims, c.perm, c.esize, stream=stream, measure=(x, y))
+            m_us = (time.perf_counter() - t0) * 1e6
+            md = mp.describe()
+            with torch.cuda.stream(stream):
+                m_ms = _event_median(lambda: mp.execute(x, y), reps, stream)
+            stream.synchronize()
+            if _plan_key(md) == _plan_key(d):
+                m_ok = ok        # the heuristic plan won: same kernel, same output (verified above)
+            else:
+                m_ok = memcmp_equal(y.cpu().numpy().view(words.dtype), want)
+            mp.destroy()
+            mrow = {"m_ms": round(m_ms, 5), "m_frac_memcpy": round(memcpy_ms[c.nbytes] / m_ms, 4),
+                    "m_plan_us": round(m_us, 1), "m_kernel": md["kernel"], "m_vg": "vg" in md.get("tile", {}),
+                    "m_candidates": md.get("measured", {}).get("candidates"), "m_verified": m_ok}
         r = {"suite": g, "case": c.name, "rank": c.rank, "esize": c.esize, "dims": list(c.dims),
              "perm": list(c.perm), "kernel": d["kernel"], "vg": "vg" in d.get("tile", {}),
              "sd": "sd" in d.get("tile", {}), "ms": round(ms, 5),
              "gbs": round(2 * c.nbytes / ms / 1e6, 1), "frac_memcpy": round(memcpy_ms[c.nbytes] / ms, 4),
              "plan_us": round(statistics.median(warm), 1), "plan_us_first": round(plan_first, 1),
              "verified": ok, "elements": c.vol}
+        r.update(mrow)
         rows.append(r)
         if fout:
             fout.write(json.dumps(r) + "\n")
@@ -440,11 +466,26 @@ def run_suites(tt, dev, which, reps, out_path=""):
                   "verified": f"{sum(r['verified'] for r in rs)}/{len(rs)} cases, full memcmp vs oracle, "
                               f"{sum(r['elements'] for r in rs)} elements",
                   "all_verified": all(r["verified"] for r in rs)}
+        if measured:
+            mf = sorted(r["m_frac_memcpy"] for r in rs)
+            mper = {}
+            for r in rs:
+                mper.setdefault(r["rank"], []).append(r["m_frac_memcpy"])
+            out[g]["measured"] = {
+                "worst_frac": mf[0], "median_frac": round(statistics.median(mf), 4), "best_frac": mf[-1],
+                "per_rank_median_frac": {str(k): round(statistics.median(v), 4) for k, v in sorted(mper.items())},
+                "plan_us_median": statistics.median(r["m_plan_us"] for r in rs),
+                "all_verified": all(r["m_verified"] for r in rs)}
     allr = [r for r in rows if r["suite"] in ("S2", "S3", "SET2")]
     if allr:
         f = sorted(r["frac_memcpy"] for r in allr)
         out["rank2_12"] = {"n": len(allr), "worst_frac": f[0], "median_frac": round(statistics.median(f), 4),
                            "best_frac": f[-1], "all_verified": all(r["verified"] for r in allr)}
+        if measured:
+            mf = sorted(r["m_frac_memcpy"] for r in allr)
+            out["rank2_12"]["measured"] = {"worst_frac": mf[0], "median_frac": round(statistics.median(mf), 4),
+                                           "best_frac": mf[-1],
+                                           "all_verified": all(r["m_verified"] for r in allr)}
     out["wall_s"] = round(time.perf_counter() - t_start, 1)
     out["reps"] = reps
     out["which"] = which
@@ -690,7 +731,8 @@ def run_ours(args):
             plan.destroy()
             del x, y
             torch.cuda.empty_cache()
-            suites = run_suites(tt, dev, args.suites, 10 if args.suites == "full" else 20, args.suites_out)
+            suites = run_suites(tt, dev, args.suites, 10 if args.suites == "full" else 20, args.suites_out,
+                                measured=args.suites_plan == "both")
             plan = None
 
     if rank == 0:

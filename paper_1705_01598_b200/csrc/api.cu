@@ -600,14 +600,25 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
         }
 
     // the heuristic tile with the vector-gather load phase (16-byte chunks of
-    // the aligned superset of every input run, 3- or 4-stage cp.async ring)
-    if (hp.n >= 2)
+    // the aligned superset of every input run, 3- or 4-stage cp.async ring),
+    // and vector-gather tiles of shorter input / longer output runs (with
+    // 16-byte chunk loads, short input runs cost little; the worst-case sweep
+    // found its best tiles there: profiles/round2_vg_tile_sweep_worst12.jsonl)
+    if (hp.n >= 2) {
         for (int st : {4, 3}) {
             tt_plan_options_t o = opt(TT_KERNEL_TILE, 0, 0, 0, 0, 0);
             o.vector_gather = 1;
             o.stages = st;
             vars.push_back(o);
         }
+        for (int bi : {64, 128, 256})
+            for (int bo : {256, 512, 1024, 2048}) {
+                tt_plan_options_t o = opt(TT_KERNEL_TILE, std::max(2, bi / W), std::max(2, bo / W), 0, 0, 0);
+                o.vector_gather = 1;
+                o.stages = 3;
+                vars.push_back(o);
+            }
+    }
 
     std::vector<Plan*> cands{heur};
     std::vector<std::string> keys{describe_json(*heur)};

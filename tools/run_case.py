@@ -18,7 +18,9 @@ n = 1
 for d in dims:
     n *= d
 td = torch.int32 if E == 4 else torch.int64
-x = torch.randint(-2**31, 2**31 - 1, (n,), dtype=td, device="cuda")
+import tt_workloads as wl
+import numpy as np
+x = torch.from_numpy(wl.random_words(n, E, 7).view(np.int32 if E == 4 else np.int64)).cuda()
 y = torch.empty_like(x)
 p = tt.Plan(dims, perm, E, **opts)
 for _ in range(reps):
