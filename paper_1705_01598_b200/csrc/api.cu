@@ -129,6 +129,8 @@ static Plan* clone_plan(const Plan& src) {
     p->tile = src.tile;
     p->row = src.row;
     p->t2d = src.t2d;
+    p->tma = src.tma;
+    if (src.tmaCache) p->tmaCache = new (std::nothrow) Plan::TmaCache();
     p->widen = src.widen;
     if (src.narrow) {
         p->narrow = clone_plan(*src.narrow);
@@ -236,6 +238,7 @@ tt_status_t create_plan_s(Plan** out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
+    if (p->kc.tma) p->tmaCache = new (std::nothrow) Plan::TmaCache();
     *out = p;
     return TT_SUCCESS;
 }
@@ -286,6 +289,7 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
+    if (p->kc.tma) p->tmaCache = new (std::nothrow) Plan::TmaCache();
     *out = p;
     return TT_SUCCESS;
 }
@@ -418,6 +422,7 @@ tt_status_t execute_host_pipelined(Plan& p, const void* host_in, void* host_out,
 }
 
 Plan::~Plan() {
+    delete tmaCache;
     delete narrow;
     delete pipe;
 }

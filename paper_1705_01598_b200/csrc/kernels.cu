@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cuda.h>
 #include <mutex>
 #include <unordered_map>
 #include <unordered_set>
@@ -66,7 +67,8 @@ static std::unordered_map<OccKey, int, OccKeyHash> g_occ;
 
 int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
-    const void* fn = q.kernel == TT_KERNEL_TILE
+    const void* fn = q.tma ? pick_tiled2d_tma(q.esize, q.tma)
+                     : q.kernel == TT_KERNEL_TILE
                          ? (q.vg ? pick_tile_vg(q.esize, q.nreg, q.vg, q.vec)
                             : q.sdq ? pick_tile_sd(q.esize, q.sdq, q.sdr, q.vec >= 3 ? q.vec : 0)
                             : q.acc ? pick_tile_acc(q.esize, q.nreg)
@@ -103,6 +105,78 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     return blocks;
 }
 
+// TMA tensor maps hold the global address: encoded for each (in, out) pair
+// (cuTensorMapEncodeTiled through the driver entry point), the last pair
+// cached in the plan.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+static bool encode_maps(const Tma2DParams& t, int E, const void* in, void* out, CUtensorMap* mi, CUtensorMap* mo) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const CUtensorMapDataType dt = E == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_INT64;
+    const cuuint32_t boxIn[5] = {(cuuint32_t)t.TA, (cuuint32_t)t.TB, 1, 1, 1};
+    const cuuint32_t boxOut[5] = {(cuuint32_t)t.TB, (cuuint32_t)t.TA, 1, 1, 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (fn(mi, dt, (cuuint32_t)t.rank, const_cast<void*>(in), t.gDimIn, t.gStrideIn, boxIn, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return fn(mo, dt, (cuuint32_t)t.rank, out, t.gDimOut, t.gStrideOut, boxOut, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int launch_tma(const Plan& plan, const void* in, void* out, cudaStream_t stream) {
+    const KernelChoice& kc = plan.kc;
+    const int E = plan.prob.esize;
+    // TMA needs 16-byte-aligned global addresses
+    if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) != 0)
+        return (int)cudaErrorMisalignedAddress;
+    Tma2DParams p = plan.tma;
+    Plan::TmaCache* c = plan.tmaCache;
+    bool ok = false;
+    if (c) {
+        std::lock_guard<std::mutex> g(c->mu);
+        if (c->in == in && c->out == out) {
+            p.inMap = c->inMap;
+            p.outMap = c->outMap;
+            ok = true;
+        } else if (encode_maps(plan.tma, E, in, out, &p.inMap, &p.outMap)) {
+            c->in = in;
+            c->out = out;
+            c->inMap = p.inMap;
+            c->outMap = p.outMap;
+            ok = true;
+        }
+    } else {
+        ok = encode_maps(plan.tma, E, in, out, &p.inMap, &p.outMap);
+    }
+    if (!ok) return (int)cudaErrorInvalidValue;
+    const void* fn = pick_tiled2d_tma(E, p.rank);
+    if (!fn) return (int)cudaErrorInvalidConfiguration;
+    cudaError_t e = ensure_max_smem(fn);
+    if (e != cudaSuccess) return (int)e;
+    void* args[] = {(void*)&p};
+    return (int)cudaLaunchKernel(fn, dim3(kc.grid), dim3(kc.threads), args, kc.smem, stream);
+}
+
 int launch_plan(const Plan& plan0, const void* in, void* out, void* stream_) {
     return launch_plan_scaled(plan0, in, out, stream_, 1.0, 0.0);
 }
@@ -130,6 +204,7 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
         void* args[] = {(void*)&plan.row, (void*)&in, (void*)&out};
         return (int)cudaLaunchKernel(fn, dim3(kc.grid), dim3(kc.threads), args, 0, stream);
     }
+    if (kc.tma) return launch_tma(plan, in, out, stream);
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
         bool t2 = kc.kernel == TT_KERNEL_TILED2D;
         int threads = kc.threads, grid = kc.grid, smem = kc.smem;

@@ -1047,6 +1047,48 @@ static bool build_tiled2d(const Problem& pr, Tiled2DParams& t, int& vec, int& ta
     return true;
 }
 
+// TMA-staged 2-D transpose (kernels_tma.cu): the Tiled class with every
+// stride a multiple of 16 bytes (cuTensorMapEncodeTiled) and at most 3 batch
+// dims (tensor rank <= 5).  Boxes: 64 x 64 (4-byte) / 32 x 64 (8-byte words).
+static bool build_tma2d(const Problem& pr, Tma2DParams& t) {
+    const int E = pr.esize;
+    if ((E != 4 && E != 8) || pr.n < 2 || pr.n > 5 || pr.p[0] == 0) return false;
+    const int B = pr.p[0];
+    if (pr.sin[0] != 1 || pr.sout[B] != 1) return false;
+    std::memset(&t, 0, sizeof(t));
+    t.TA = E == 4 ? 64 : 32;
+    t.TB = 64;
+    t.nb = pr.n - 2;
+    t.rank = pr.n;
+    t.gDimIn[0] = pr.d[0];
+    t.gDimIn[1] = pr.d[B];
+    t.gDimOut[0] = pr.d[B];
+    t.gDimOut[1] = pr.d[0];
+    t.gStrideIn[0] = (uint64_t)pr.sin[B] * E;
+    t.gStrideOut[0] = (uint64_t)pr.sout[0] * E;
+    int k = 0;
+    for (int i = 1; i < pr.n; ++i) {
+        if (i == B) continue;
+        t.bExt[k] = (int32_t)pr.d[i];
+        t.gDimIn[2 + k] = pr.d[i];
+        t.gDimOut[2 + k] = pr.d[i];
+        t.gStrideIn[1 + k] = (uint64_t)pr.sin[i] * E;
+        t.gStrideOut[1 + k] = (uint64_t)pr.sout[i] * E;
+        ++k;
+    }
+    for (int r = 0; r < t.rank; ++r)
+        if (t.gDimIn[r] >= (uint64_t(1) << 32) || t.gDimIn[r] == 0) return false;
+    for (int r = 0; r + 1 < t.rank; ++r)
+        if (t.gStrideIn[r] % 16 || t.gStrideOut[r] % 16 || t.gStrideIn[r] >= (uint64_t(1) << 40) ||
+            t.gStrideOut[r] >= (uint64_t(1) << 40))
+            return false;
+    t.nA = (int32_t)ceil_div(pr.d[0], t.TA);
+    t.nB = (int32_t)ceil_div(pr.d[B], t.TB);
+    t.nTiles = (int64_t)t.nA * t.nB;
+    for (int q = 0; q < t.nb; ++q) t.nTiles *= t.bExt[q];
+    return t.nTiles < (int64_t(1) << 31);
+}
+
 int estimate_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     // register counts of the tile kernels as compiled (ptxas -v, build/obj)
     int regs;
@@ -1445,6 +1487,28 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     kc.fb_grid = kc.grid;
     kc.fb_smem = kc.smem;
 
+    // TMA-staged 2-D kernel (option tma): whole boxes through the Tensor
+    // Memory Accelerator, ragged tiles clipped by the hardware
+    if (opts && opts->tma > 0) {
+        if (acc || !build_tma2d(pr, plan.tma)) return TT_UNSUPPORTED;
+        kc.kernel = TT_KERNEL_TILED2D;
+        kc.tma = 1;
+        kc.vec = 1;
+        kc.tile0 = plan.tma.TA;
+        kc.tile1 = plan.tma.TB;
+        kc.threads = 256;
+        kc.stages = 3;
+        kc.smem = 5 * plan.tma.TA * plan.tma.TB * E + 3 * 8 + 128;
+        OccQuery qt{TT_KERNEL_TILED2D, E, 0, 1, 256, kc.smem, false, 0, 0, 0, 0, 0, 0};
+        qt.tma = plan.tma.rank;
+        int per = opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qt, dev) : 0);
+        if (per <= 0) per = std::max(1, dev.max_smem_per_sm / (kc.smem + 1024));
+        kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tma.nTiles, (int64_t)dev.num_sms * per));
+        kc.predicted_us = 2.0 * pr.vol * E / model::kBwBytesPerUs + model::kLaunchUs;
+        kc.model_dram_eff = 1.0;
+        return TT_SUCCESS;
+    }
+
     // Vectorised 2-D tiled kernel when the tiles are mostly full: it moves
     // VW elements per instruction on both sides (model: its issue cost is a
     // fraction of the generic kernel's, DRAM sectors are whole).
@@ -1606,7 +1670,11 @@ std::string describe_json(const Plan& plan) {
         arr(o, t.gSin, t.h);
         o << ",\"grid_sout\":";
         arr(o, t.gSout, t.h);
-        o << "},\"fallback\":{\"kernel\":\"tile\",\"threads\":" << kc.fb_threads
+        o << "},\"tma\":" << kc.tma;
+        if (kc.tma)
+            o << ",\"tma_box\":{\"rank\":" << plan.tma.rank << ",\"TA\":" << plan.tma.TA << ",\"TB\":"
+              << plan.tma.TB << ",\"nTiles\":" << (long long)plan.tma.nTiles << "}";
+        o << ",\"fallback\":{\"kernel\":\"tile\",\"threads\":" << kc.fb_threads
           << ",\"grid\":" << kc.fb_grid << ",\"smem\":" << kc.fb_smem << ",\"nreg\":" << kc.nreg << "}";
     }
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {

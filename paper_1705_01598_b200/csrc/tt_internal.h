@@ -3,7 +3,10 @@
 // kernels.cu).  Citations: P:Lnn = PAPER.md line nn (arXiv 1705.01598).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (the TMA 2-D kernel's parameter block)
+
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -144,6 +147,21 @@ struct Tiled2DParams {
     uint32_t gMC[kMaxDims], gLC[kMaxDims], gMD[kMaxDims], gLD[kMaxDims];
 };
 
+// TMA-staged 2-D tiled transpose (kernels_tma.cu): tensor maps of the input
+// (dims A, B, batch...) and the output (B, A, batch...), encoded per device
+// pointer pair at launch (they hold the global address), tile grid.
+struct alignas(64) Tma2DParams {
+    CUtensorMap inMap, outMap;
+    int64_t nTiles;
+    int32_t nA, nB;        // chunks along A and B
+    int32_t nb;            // batch dims (0..3)
+    int32_t TA, TB;        // box extents along A and B
+    int32_t rank;          // tensor rank 2 + nb
+    int32_t bExt[3];
+    // host-side geometry for encoding (elements; strides in bytes)
+    uint64_t gDimIn[5], gDimOut[5], gStrideIn[4], gStrideOut[4];
+};
+
 struct KernelChoice {
     int kernel = TT_KERNEL_AUTO;   // tt_kernel_t
     int threads = 0;
@@ -158,6 +176,7 @@ struct KernelChoice {
     int acc = 0;                   // accumulate plan (f-3): generic tile with alpha/beta
     int sdq = 0, sdr = 0;          // generic tile, slot-dim variant: passes x slots (0 = classic)
     int vg = 0;                    // generic tile, vector-gather variant (tile_vg_kernel)
+    int tma = 0;                   // TILED2D staged by TMA (tiled2d_tma_kernel)
     double predicted_us = 0.0;
     double model_dram_eff = 0.0;   // algorithmic / modelled DRAM bytes
     // model features of the generic tile (describe "model"; calibration)
@@ -183,6 +202,7 @@ struct OccQuery {
     int acc;     // TILE accumulate variant
     int sdq, sdr;  // TILE slot-dim variant (passes, slots); 0 = classic; TILED2D: sdq = cp.async stages
     int vg;        // TILE vector-gather variant (nreg = slots, vec = stages)
+    int tma;       // TILED2D TMA variant: tensor rank (0 = not TMA)
 };
 typedef int (*OccupancyFn)(const OccQuery&, const DeviceInfo&);
 
@@ -200,6 +220,14 @@ struct Plan {
     TileParams tile{};
     RowParams row{};
     Tiled2DParams t2d{};
+    Tma2DParams tma{};             // kc.tma plans
+    struct TmaCache {              // tensor maps of the last (in, out) pair, per plan
+        std::mutex mu;
+        const void* in = nullptr;
+        void* out = nullptr;
+        CUtensorMap inMap, outMap;
+    };
+    TmaCache* tmaCache = nullptr;
     ShardInfo* shard = nullptr;    // sharded plans only
     bool measured = false;         // chosen by tt_plan_measure
     float measured_ms = 0.f, heuristic_ms = 0.f;

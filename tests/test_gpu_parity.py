@@ -298,6 +298,25 @@ def test_vector_gather(esize, stages):
             check(dims, perm, esize, run_in=run[0], run_out=run[1], vector_gather=1, stages=stages)
 
 
+@pytest.mark.parametrize("esize", [4, 8])
+def test_tma_2d(esize):
+    """The TMA-staged 2-D kernel (tiled2d_tma_kernel, option tma=1): full and
+    ragged boxes (the hardware zero-fills loads and clips stores at the
+    tensor ends), batch dims up to tensor rank 5, permutations where B is not
+    dim 1.  Shapes whose strides are not 16-byte multiples are refused."""
+    q = 16 // esize
+    shapes = [((64, 64), (1, 0)), ((132, 68), (1, 0)), ((4 * q, 1000 * q), (1, 0)),
+              ((96, 5, 40), (2, 1, 0)), ((36, 7, 44, 3), (2, 0, 3, 1)), ((8, 5, 12, 3), (2, 3, 0, 1)),
+              ((40, 3, 2, 3, 24), (4, 1, 2, 3, 0)), ((2 * q, 3, 6 * q), (2, 0, 1)),
+              ((8, 3, 5, 7, 4), (4, 2, 0, 3, 1))]   # tensor rank 5
+    for dims, perm in shapes:
+        d = tt.Plan(dims, perm, esize, tma=1).describe()
+        assert d["kernel"] == "tiled2d" and d["tma"] == 1
+        check(dims, perm, esize, tma=1)
+    with pytest.raises(tt.TTError):
+        tt.Plan((67, 45), (1, 0), esize, tma=1)
+
+
 @pytest.mark.parametrize("threads", [64, 96, 256, 512])
 def test_forced_threads(threads):
     check((97, 89, 3), (1, 2, 0), 4, threads=threads)
