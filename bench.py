@@ -379,6 +379,14 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
     th = threading.Thread(target=producer, daemon=True)
     t_start = time.perf_counter()
     th.start()
+    # one pinned host buffer for the outputs copied back for verification
+    # (pageable copies of 1-2 GB cost ~0.5 s each under the oracle's threads)
+    pin = torch.empty(max(c.nbytes for _, c in cases), dtype=torch.uint8).pin_memory()
+
+    def fetch(y, dtype):
+        h = pin[:y.numel() * y.element_size()]
+        h.copy_(y.view(torch.uint8))
+        return h.numpy().view(dtype)
     stream = torch.cuda.Stream(device=dev)
     memcpy_ms = {}
     rows = []
@@ -407,8 +415,7 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
                 memcpy_ms[c.nbytes] = _event_median(lambda: z.copy_(x), reps, stream)
                 del z
         stream.synchronize()
-        got = y.cpu().numpy().view(words.dtype)
-        ok = memcmp_equal(got, want)
+        ok = memcmp_equal(fetch(y, words.dtype), want)
         d = plan.describe()
         plan.destroy()
         mrow = {}
@@ -425,13 +432,18 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
             if _plan_key(md) == _plan_key(d):
                 m_ok = ok        # the heuristic plan won: same kernel, same output (verified above)
             else:
-                m_ok = memcmp_equal(y.cpu().numpy().view(words.dtype), want)
+                m_ok = memcmp_equal(fetch(y, words.dtype), want)
             mp.destroy()
+            mt = md.get("tile", {})
             mrow = {"m_ms": round(m_ms, 5), "m_frac_memcpy": round(memcpy_ms[c.nbytes] / m_ms, 4),
-                    "m_plan_us": round(m_us, 1), "m_kernel": md["kernel"], "m_vg": "vg" in md.get("tile", {}),
+                    "m_plan_us": round(m_us, 1), "m_kernel": md["kernel"], "m_vg": "vg" in mt,
+                    "m_sd": "sd" in mt, "m_stages": md.get("stages"), "m_tile": mt.get("ext"),
+                    "m_run": [md.get("model", {}).get("run_in"), md.get("model", {}).get("run_out")],
                     "m_candidates": md.get("measured", {}).get("candidates"), "m_verified": m_ok}
         r = {"suite": g, "case": c.name, "rank": c.rank, "esize": c.esize, "dims": list(c.dims),
              "perm": list(c.perm), "kernel": d["kernel"], "vg": "vg" in d.get("tile", {}),
+             "tile": d.get("tile", {}).get("ext"),
+             "run": [d.get("model", {}).get("run_in"), d.get("model", {}).get("run_out")],
              "sd": "sd" in d.get("tile", {}), "ms": round(ms, 5),
              "gbs": round(2 * c.nbytes / ms / 1e6, 1), "frac_memcpy": round(memcpy_ms[c.nbytes] / ms, 4),
              "plan_us": round(statistics.median(warm), 1), "plan_us_first": round(plan_first, 1),
@@ -441,7 +453,7 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
         if fout:
             fout.write(json.dumps(r) + "\n")
             fout.flush()
-        del x, y, got, want, words
+        del x, y, want, words
         torch.cuda.empty_cache()
     th.join()
     if fout:

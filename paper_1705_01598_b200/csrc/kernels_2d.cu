@@ -74,6 +74,46 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
         }
     }
     I base = warp_sum<I>(x * s);
+    // odometer step to the next row: returns the input base delta
+    auto step = [&]() {
+        const uint32_t wraps = __ballot_sync(0xffffffffu, lane < p.h && x == d - 1);
+        const int f = __ffs(~wraps) - 1;
+        I delta = 0;
+        if (lane < f) { delta = (I)0 - (d - 1) * s; x = 0; }
+        else if (lane == f) { delta = s; x += 1; }
+        return warp_sum<I>(delta);
+    };
+    if (!segd && (I)p.seg <= (I)(32 * U)) {
+        // short rows (one load per lane and word slot per row): the next
+        // row's loads are issued before this row's stores, so two rows per
+        // warp are in flight instead of one (rows of 0.7-1 KB were
+        // latency-bound at ~0.77-0.88 of memcpy)
+        const I L = (I)p.seg;
+        W t[U], t2[U];
+        {
+            const W* __restrict__ src = opaque(in + base);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lane + 32 * u < L) t[u] = ldg_(src + lane + 32 * u);
+        }
+        for (I r = r0; r < r1; ++r) {
+            base += step();
+            if (r + 1 < r1) {
+                const W* __restrict__ src = opaque(in + base);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (lane + 32 * u < L) t2[u] = ldg_(src + lane + 32 * u);
+            }
+            W* __restrict__ dst = opaque(out + obase);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lane + 32 * u < L) stg_(dst + lane + 32 * u, t[u]);
+            obase += L;
+#pragma unroll
+            for (int u = 0; u < U; ++u) t[u] = t2[u];
+        }
+        return;
+    }
     for (I r = r0; r < r1; ++r) {
         const W* __restrict__ src = opaque(in + base);
         W* __restrict__ dst = opaque(out + obase);
@@ -88,13 +128,7 @@ rowcopy_kernel(const __grid_constant__ RowParams p, const W* __restrict__ in, W*
             for (int u = 0; u < U; ++u)
                 if (c + 32 * u < L) stg_(dst + c + 32 * u, t[u]);
         }
-        // odometer step to row r+1
-        const uint32_t wraps = __ballot_sync(0xffffffffu, lane < p.h && x == d - 1);
-        const int f = __ffs(~wraps) - 1;
-        I delta = 0;
-        if (lane < f) { delta = (I)0 - (d - 1) * s; x = 0; }
-        else if (lane == f) { delta = s; x += 1; }
-        base += warp_sum<I>(delta);
+        base += step();  // odometer step to row r+1
         // output rows are dense in output order: the next segment, or the
         // next row's first segment (after this row's last, segTail long)
         obase += L;
