@@ -625,6 +625,16 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
             }
     }
 
+    // the TMA-staged 2-D kernel where its strides allow (on plain 2-D
+    // transposes it measured 0.90-0.95x of the vector 2-D kernel, but won on
+    // some batched shapes: profiles/round2_ab_tma.jsonl)
+    if (hp.n >= 2 && hp.p[0] != 0)
+        for (int cps : {0, 2}) {
+            tt_plan_options_t o = opt(0, 0, 0, 0, cps, 0);
+            o.tma = 1;
+            vars.push_back(o);
+        }
+
     std::vector<Plan*> cands{heur};
     std::vector<std::string> keys{describe_json(*heur)};
     for (const auto& o : vars) {
