@@ -550,7 +550,13 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
     };
     const Problem& hp = heur->prob;
     const int W = hp.esize;
-    if (hp.n >= 2 && hp.p[0] != 0) {
+    // 2-D candidates only when the two fastest dims fill 64 x 64 tiles
+    // reasonably: forced on, say, a 2 x 2 pair the 2-D kernel is correct but
+    // ~2000x slower (every tile nearly empty), which made measuring a rank-12
+    // problem take 80 s
+    auto fill64 = [&](int64_t d) { return (double)d / (64.0 * (double)((d + 63) / 64)); };
+    const bool t2dSane = hp.n >= 2 && hp.p[0] != 0 && fill64(hp.d[0]) * fill64(hp.d[hp.p[0]]) >= 0.25;
+    if (t2dSane) {
         const int tiles4[4][2] = {{64, 128}, {128, 64}, {128, 128}, {64, 64}};
         const int tiles8[4][2] = {{64, 64}, {64, 32}, {32, 64}, {32, 32}};
         for (int t = 0; t < 4; ++t)
@@ -660,7 +666,17 @@ tt_status_t tt_plan_measure(tt_plan_t* plan, int rank, const int64_t* dims, cons
     int best = 0;
     float bestMs = 1e30f, heurMs = 0.f;
     for (size_t i = 0; i < cands.size(); ++i) {
+        // one timed launch first: a candidate over 4x the heuristic's time
+        // is dropped without further repetitions
+        cudaEventRecord(e0, s);
         if (launch_plan(*cands[i], in, out, stream) != 0) { cudaGetLastError(); continue; }
+        cudaEventRecord(e1, s);
+        if (cudaEventSynchronize(e1) != cudaSuccess) { cudaGetLastError(); continue; }
+        if (i > 0) {
+            float first = 0.f;
+            cudaEventElapsedTime(&first, e0, e1);
+            if (first > 4.f * heurMs) continue;
+        }
         cudaEventRecord(e0, s);
         const int reps = 3;
         for (int r = 0; r < reps; ++r) launch_plan(*cands[i], in, out, stream);
