@@ -72,9 +72,9 @@ def parse(argv=None):
     ap.add_argument("--config", default="s1", choices=CONFIGS)
     ap.add_argument("--suites", default="default", choices=["default", "full", "none"])
     ap.add_argument("--suites-out", default="", help="per-case JSONL of the suites")
-    ap.add_argument("--suites-plan", default="both", choices=["heuristic", "both", "both-all"],
-                    help="both: also measurement-based plans (tt_plan_measure) on Set 2 and S3 ranks "
-                         "10-12; both-all: on every suite case")
+    ap.add_argument("--suites-plan", default="both-all", choices=["heuristic", "both", "both-all"],
+                    help="both-all: also the measurement-based plan (tt_plan_measure) of every suite case; "
+                         "both: only on Set 2 and S3 ranks 10-12")
     ap.add_argument("--verify", default="full", choices=["full", "none"])
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps (capped at 20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
