@@ -111,7 +111,6 @@ typedef struct {
                             redistribution path even with one rank (single-GPU tests) */
     int vg_policy;       /* vector-gather loads, calibration: 0 = cp.async.ca (default),
                             1 = cp.async.cg (L2 only) */
-    int t2d_streaming;   /* TILED2D vector kernel, calibration: 1 = evict-first (.cs) loads/stores */
     int tma;             /* TILED2D: 1 = stage the tiles with the Tensor Memory Accelerator
                             (tiled2d_tma_kernel) when every stride is a multiple of 16 bytes
                             and there are at most 3 batch dims; else TT_UNSUPPORTED */

@@ -49,7 +49,7 @@ class PlanOptions(ctypes.Structure):
                 ("slot_dims", ctypes.c_int), ("sd_vmax", ctypes.c_int),
                 ("vector_gather", ctypes.c_int), ("t2d_vec2", ctypes.c_int),
                 ("force_redistribute", ctypes.c_int), ("vg_policy", ctypes.c_int),
-                ("t2d_streaming", ctypes.c_int), ("tma", ctypes.c_int)]
+                ("tma", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -140,12 +140,12 @@ def _arrays(dims, perm):
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
              grid_order=0, no_widen=False, stages=0, accumulate=False, slots=0, slot_dims=0,
              sd_vmax=0, vector_gather=0, t2d_vec2=0, force_redistribute=False,
-             vg_policy=0, t2d_streaming=0, tma=0):
+             vg_policy=0, tma=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
                        1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
                        1 if accumulate else 0, int(slots), int(slot_dims), int(sd_vmax),
                        int(vector_gather), int(t2d_vec2), 1 if force_redistribute else 0, int(vg_policy),
-                       int(t2d_streaming), int(tma))
+                       int(tma))
 
 
 def _ptr(x) -> int:

@@ -185,8 +185,7 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
                 for (int ma = 0; ma < MA; ++ma) {
                     const int a0 = (ta + 16 * ma) * VW;
                     if (a0 < limA && b0 < limB) {
-                        const V* const ga = reinterpret_cast<const V*>(in + (tb.in + (I)(b0 + k) * sInB + a0));
-                        const V x = p.streaming ? __ldcs(ga) : __ldg(ga);
+                        const V x = __ldg(reinterpret_cast<const V*>(in + (tb.in + (I)(b0 + k) * sInB + a0)));
                         *reinterpret_cast<V*>(&v[mb][ma][k][0]) = x;
                     }
                 }
@@ -231,9 +230,7 @@ tiled2d_kernel(const __grid_constant__ Tiled2DParams p, const W* __restrict__ in
             const int c = q % CPR;
             if (a < limA && c * VW < limB) {
                 const V x = sb[a * CPR + (c ^ ((a / VW) & (CPR - 1)))];
-                V* const ga = reinterpret_cast<V*>(out + (now.out + (I)a * sOutA + c * VW));
-                if (p.streaming) __stcs(ga, x);
-                else *ga = x;
+                *reinterpret_cast<V*>(out + (now.out + (I)a * sOutA + c * VW)) = x;
             }
         }
         buf ^= 1;

@@ -1230,7 +1230,6 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
                                      opts && opts->grid_order ? opts->grid_order : 2,
                                      opts ? opts->t2d_vec2 : 0);
     if (forced == TT_KERNEL_TILED2D && !can2d) return TT_UNSUPPORTED;
-    if (can2d) plan.t2d.streaming = opts && opts->t2d_streaming > 0 ? 1 : 0;
     // fill of the output-fastest (B) side alone: short B extents leave the
     // 2-D kernel short write runs and half-empty tiles
     // Same-box A/B over the S2/S3/Set-2 suites (tools/ab_fillb.sh,

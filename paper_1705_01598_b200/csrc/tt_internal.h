@@ -141,7 +141,6 @@ struct Tiled2DParams {
     int32_t splitLane[2];    // 0, 1
     int32_t splitChunk[2];   // TA, TB
     int32_t splitTail[2];    // valid extent of the last chunk along A / B
-    int32_t streaming;       // vector kernel: evict-first loads/stores (option t2d_streaming, calibration)
     int64_t sInB;            // input stride of dim B (elements)
     int64_t sOutA;           // output stride of dim A (elements)
     int64_t gC[kMaxDims], gD[kMaxDims], gSin[kMaxDims], gSout[kMaxDims];
