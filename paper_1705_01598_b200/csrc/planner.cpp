@@ -315,6 +315,7 @@ static int warp_wavefronts(const int* pos, int nlanes, int esize) {
 // candidate layout costs one dot product per lane.
 struct SmemSample {
     int a = 0, nacc = 0;
+    int maxVary = -1;        // highest tile dim whose coordinate varies inside a sampled access
     std::vector<int> nl;     // lanes per distinct access pattern
     std::vector<int> wt;     // sampled accesses with that pattern
     std::vector<int> coord;  // [pattern][lane][tile dim + 1], relative to lane 0; the last
@@ -361,6 +362,9 @@ static SmemSample smem_sample(const TileParams& tp, int sides = 3, Extra extra =
                     merged = true;
                 }
             }
+            for (int l = 0; l < 32; ++l)
+                for (int i = 0; i < tp.a; ++i)
+                    if (cur[l * A + i] != 0) s.maxVary = std::max(s.maxVary, i);
             if (!merged) {
                 s.nl.push_back(nl);
                 s.wt.push_back(1);
@@ -797,7 +801,40 @@ struct TileMemo {
 // + pad[i] (the L x (L+1) padding of P:L123 generalised to every level of
 // the tile), chosen by coordinate descent on the conflict model, then by
 // footprint.  Footprint is capped so the 16-bit staging offsets fit.
+static void choose_smem_search(TileParams& tp, int esize);
+
+// The layout search is a pure function of the tile's extents, output order
+// and word size: recent answers are kept per thread (the plans of one
+// problem -- narrow, widened, the fp64 ring alternative -- often share a tile).
 static void choose_smem(TileParams& tp, int esize) {
+    struct Entry {
+        std::vector<int32_t> key;
+        int32_t sm[kMaxDims];
+        int32_t sbuf;
+    };
+    thread_local std::vector<Entry> cache;
+    std::vector<int32_t> key;
+    key.reserve(2 * tp.a + 2);
+    key.push_back(tp.a);
+    key.push_back(esize);
+    for (int i = 0; i < tp.a; ++i) key.push_back(tp.tExt[i]);
+    for (int i = 0; i < tp.a; ++i) key.push_back(tp.tOutOrder[i]);
+    for (const Entry& e : cache)
+        if (e.key == key) {
+            for (int i = 0; i < tp.a; ++i) tp.tSm[i] = e.sm[i];
+            tp.sbuf = e.sbuf;
+            return;
+        }
+    choose_smem_search(tp, esize);
+    Entry e;
+    e.key = key;
+    for (int i = 0; i < tp.a; ++i) e.sm[i] = tp.tSm[i];
+    e.sbuf = tp.sbuf;
+    if (cache.size() >= 32) cache.erase(cache.begin());
+    cache.push_back(e);
+}
+
+static void choose_smem_search(TileParams& tp, int esize) {
     const int a = tp.a;
     int32_t pad[kMaxDims] = {};
     int32_t sm[kMaxDims];
@@ -820,8 +857,11 @@ static void choose_smem(TileParams& tp, int esize) {
     const int ideal_per_warp = esize == 4 ? 2 : esize == 8 ? 4 : 8;  // store + read
     const int nw = (tp.V + 31) / 32;
     const long ideal = (long)((nw + std::max(1, nw / 8) - 1) / std::max(1, nw / 8)) * ideal_per_warp;
+    // pad[i] moves the strides of dims >= i only: dims above the highest one
+    // that varies inside a sampled access cannot change any cost
+    const int hi = std::min(a - 1, sample.maxVary);
     for (int pass = 0; pass < 2 && best > ideal; ++pass) {
-        for (int i = 1; i < a && best > ideal; ++i) {
+        for (int i = 1; i <= hi && best > ideal; ++i) {
             int32_t keep = pad[i];
             int32_t bestPad = keep;
             for (int c = 0; c < 32; ++c) {
