@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--variants", default="vg4,vg3")
     ap.add_argument("--only-tile", action="store_true", default=True)
+    ap.add_argument("--esize", type=int, default=0)
+    ap.add_argument("--perm0", default="", choices=["", "zero", "nonzero"])
+    ap.add_argument("--kind", default="", choices=["", "classic", "sd", "vg"])
     a = ap.parse_args()
     variants = {}
     for st in (3, 4):
@@ -43,6 +46,13 @@ def main():
     for c in cases_for(a.suite.split(","), a.per_cell):
         base = tt.plan_offline(c.dims, c.perm, c.esize)
         if a.only_tile and base["kernel"] != "tile":
+            continue
+        if a.esize and c.esize != a.esize:
+            continue
+        if a.perm0 and (base["fused"]["perm"][0] == 0) != (a.perm0 == "zero"):
+            continue
+        kind = "vg" if "vg" in base.get("tile", {}) else "sd" if "sd" in base.get("tile", {}) else "classic"
+        if a.kind and kind != a.kind:
             continue
         words = c.words()
         nd = np.int32 if c.esize == 4 else np.int64
