@@ -41,6 +41,9 @@ def main():
     for st in (3, 4):
         for pol in range(4):
             variants[f"vg{st}" + (f"p{pol}" if pol else "")] = dict(vector_gather=1, stages=st, vg_policy=pol)
+    # slot-dim map on the heuristic tile, synchronous and cp.async ring
+    variants["sd"] = dict(slot_dims=1)
+    variants["sd3"] = dict(slot_dims=1, stages=3)
     f = open(a.out, "w") if a.out else None
     ratios = {v: [] for v in a.variants.split(",")}
     for c in cases_for(a.suite.split(","), a.per_cell):
@@ -71,7 +74,8 @@ def main():
             except tt.TTError:
                 continue
             d = p.describe()
-            if "vg" not in d.get("tile", {}):
+            want_key = "sd" if v.startswith("sd") else "vg"
+            if want_key not in d.get("tile", {}):
                 p.destroy(); continue
             y.zero_()
             t = timeit(p, x, y)
