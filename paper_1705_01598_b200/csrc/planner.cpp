@@ -250,18 +250,17 @@ static void fill_magic(T& t) {
 static double run_sectors(double bytes, int64_t align) {
     if (align >= 32) return std::ceil(bytes / model::kSector);
     // start offset uniform over the multiples of align inside a sector
-    double s = 0;
+    // (bytes is a whole number: the sums below are exact in integers)
+    const int64_t b = (int64_t)bytes;
+    int64_t s = 0;
     int cnt = 0;
-    for (int64_t off = 0; off < 32; off += align, ++cnt)
-        s += std::ceil((off + bytes) / model::kSector);
-    return s / cnt;
+    for (int64_t off = 0; off < 32; off += align, ++cnt) s += (off + b + 31) >> 5;
+    return (double)s / cnt;
 }
 
 static int64_t pow2_align(int64_t x) {  // largest power of two dividing x (x>0), capped
     if (x == 0) return 1 << 20;
-    int64_t a = 1;
-    while ((x % (a * 2)) == 0 && a < (1 << 20)) a *= 2;
-    return a;
+    return std::min<int64_t>(x & -x, 1 << 20);
 }
 
 struct TileCand {
@@ -289,18 +288,19 @@ struct TileCand {
 static int warp_wavefronts(const int* pos, int nlanes, int esize) {
     if (nlanes <= 0) return 0;
     if (esize == 4) {
-        int cnt[32] = {};
-        int worst = 0;
-        for (int l = 0; l < nlanes; ++l) worst = std::max(worst, ++cnt[pos[l] & 31]);
+        uint8_t cnt[32] = {};
+        for (int l = 0; l < nlanes; ++l) ++cnt[pos[l] & 31];
+        uint8_t worst = 0;
+        for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
         return worst;
     }
     const int per = 16, banks = 16;        // half-warp phases, bank pairs
     int total = 0;
     for (int ph = 0; ph * per < nlanes; ++ph) {
-        int cnt[32] = {};
-        int worst = 0;
-        for (int l = ph * per; l < std::min(nlanes, ph * per + per); ++l)
-            worst = std::max(worst, ++cnt[pos[l] & (banks - 1)]);
+        uint8_t cnt[16] = {};
+        for (int l = ph * per; l < std::min(nlanes, ph * per + per); ++l) ++cnt[pos[l] & (banks - 1)];
+        uint8_t worst = 0;
+        for (int b = 0; b < 16; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
         total += worst;
     }
     return total;
@@ -316,6 +316,7 @@ static int warp_wavefronts(const int* pos, int nlanes, int esize) {
 struct SmemSample {
     int a = 0, nacc = 0;
     int maxVary = -1;        // highest tile dim whose coordinate varies inside a sampled access
+    int av = 0;              // maxVary + 1: relative coordinates of higher dims are all zero
     std::vector<int> nl;     // lanes per distinct access pattern
     std::vector<int> wt;     // sampled accesses with that pattern
     std::vector<int> coord;  // [pattern][lane][tile dim + 1], relative to lane 0; the last
@@ -341,14 +342,27 @@ static SmemSample smem_sample(const TileParams& tp, int sides = 3, Extra extra =
         for (int side = 0; side < 2; ++side) {  // 0: staging store (input order), 1: transposed read
             if (!(sides & (1 << side))) continue;
             int c0[kMaxDims + 1] = {};
-            for (int l = 0; l < 32; ++l) {
-                int kk = w * 32 + l;
-                int c[kMaxDims + 1] = {};
-                for (int jj = 0; jj < tp.a && l < nl; ++jj) {
+            // lane 0's coordinates by division, the next lanes by an odometer
+            // step in this side's order (same values as decoding each lane)
+            int c[kMaxDims + 1] = {};
+            {
+                int kk = w * 32;
+                for (int jj = 0; jj < tp.a; ++jj) {
                     const int t = side == 0 ? jj : tp.tOutOrder[jj];
                     c[t] = kk % tp.tExt[t];
                     kk /= tp.tExt[t];
                 }
+            }
+            for (int l = 0; l < 32; ++l) {
+                if (l > 0 && l < nl) {
+                    for (int jj = 0; jj < tp.a; ++jj) {
+                        const int t = side == 0 ? jj : tp.tOutOrder[jj];
+                        if (++c[t] < tp.tExt[t]) break;
+                        c[t] = 0;
+                    }
+                }
+                if (l >= nl)
+                    for (int i = 0; i < tp.a; ++i) c[i] = 0;
                 c[tp.a] = l < nl ? extra(c) : 0;
                 if (l == 0)
                     for (int i = 0; i < A; ++i) c0[i] = c[i];
@@ -373,6 +387,23 @@ static SmemSample smem_sample(const TileParams& tp, int sides = 3, Extra extra =
             }
         }
     }
+    s.av = s.maxVary + 1;
+    // heaviest accesses first: the candidate costs are sums of integers, so
+    // the order changes no cost, but a losing candidate exceeds its bound
+    // (smem_cost_at) sooner
+    if (s.nacc > 1) {
+        std::vector<int> ord(s.nacc);
+        for (int q = 0; q < s.nacc; ++q) ord[q] = q;
+        std::stable_sort(ord.begin(), ord.end(), [&](int u, int v) { return s.wt[u] > s.wt[v]; });
+        SmemSample t = s;
+        for (int q = 0; q < s.nacc; ++q) {
+            t.nl[q] = s.nl[ord[q]];
+            t.wt[q] = s.wt[ord[q]];
+            std::copy(s.coord.begin() + (size_t)ord[q] * 32 * A, s.coord.begin() + (size_t)(ord[q] + 1) * 32 * A,
+                      t.coord.begin() + (size_t)q * 32 * A);
+        }
+        return t;
+    }
     return s;
 }
 
@@ -384,9 +415,52 @@ static long smem_cost(const SmemSample& s, int esize, const int32_t* sm, long bo
         if (bound >= 0 && cost >= bound) return cost;  // already no better than the incumbent
         for (int l = 0; l < 32; ++l, c += s.a + 1) {
             int sp = c[s.a];
-            for (int i = 0; i < s.a; ++i) sp += c[i] * sm[i];
+            for (int i = 0; i < s.av; ++i) sp += c[i] * sm[i];
             pos[l] = sp + 4096;  // relative positions may be negative: keep the low bits' meaning
         }
+        cost += (long)s.wt[q] * warp_wavefronts(pos, s.nl[q], esize);
+    }
+    return cost;
+}
+
+// The padding searches change one pad at a time.  Raising pad[i] by c adds
+// c * prod(ext[i..j-1]) to every stride sm[j], j >= i, so every sampled
+// lane's position is linear in c: pos = base + c * w.  smem_line fixes the
+// other pads, smem_cost_at then costs a candidate with one multiply-add per
+// lane (only the low 5 bits matter: bank = pos mod 32).
+struct SmemLine {
+    std::vector<int> base, w;  // [access][lane]
+};
+// Returns the period of the cost in the candidate pad: cand and cand + 32/g
+// give every lane the same bank (g = the largest power of two dividing every
+// w mod 32), so candidates past the first period can never improve on it.
+static int smem_line(const SmemSample& s, const int32_t* sm0, const int64_t* coef, SmemLine& ln) {
+    const size_t n = (size_t)s.nacc * 32;
+    ln.base.resize(n);
+    ln.w.resize(n);
+    const int* c = s.coord.data();
+    int orw = 0;
+    for (size_t k = 0; k < n; ++k, c += s.a + 1) {
+        int64_t b = c[s.a], w = 0;
+        for (int i = 0; i < s.av; ++i) {
+            b += (int64_t)c[i] * sm0[i];
+            w += (int64_t)c[i] * coef[i];
+        }
+        ln.base[k] = (int)(b & 1023);
+        ln.w[k] = (int)(w & 1023);
+        orw |= (int)(w & 31);
+    }
+    if (orw == 0) return 1;
+    return 32 / (orw & -orw);
+}
+static long smem_cost_at(const SmemSample& s, int esize, const SmemLine& ln, int cand, long bound) {
+    long cost = 0;
+    int pos[32];
+    for (int q = 0; q < s.nacc; ++q) {
+        if (bound >= 0 && cost >= bound) return cost;
+        const int* b = &ln.base[(size_t)q * 32];
+        const int* w = &ln.w[(size_t)q * 32];
+        for (int l = 0; l < 32; ++l) pos[l] = b[l] + cand * w[l];
         cost += (long)s.wt[q] * warp_wavefronts(pos, s.nl[q], esize);
     }
     return cost;
@@ -422,7 +496,8 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
         return best;
     };
     double bestFill = 0;
-    TileParams bestTp = tp;
+    Pick bL, bS;
+    int64_t bUL = 0, bUS = 0, bQL = 0, bQS = 0;
     for (int cfg = 0; cfg < 3; ++cfg) {
         const int QM = cfg == 0 ? 2 : cfg == 1 ? 1 : 4;
         const int RM = cfg == 0 ? 8 : cfg == 1 ? 16 : 4;
@@ -444,18 +519,17 @@ static bool build_sd(TileParams& tp, int esize, int64_t runIn, int64_t runOut, O
         if (fill >= 0.6 && per > 0 && score > bestFill + 1e-9) {
             ctasPerSm = per;
             bestFill = score;
-            bestTp = tp;
-            bestTp.sdSlot[0] = L.slot; bestTp.sdR[0] = L.R; bestTp.sdC[0] = L.C;
-            bestTp.sdU[0] = (int32_t)UL; bestTp.sdQ[0] = (int32_t)QL;
-            bestTp.sdSlot[1] = S.slot; bestTp.sdR[1] = S.R; bestTp.sdC[1] = S.C;
-            bestTp.sdU[1] = (int32_t)US; bestTp.sdQ[1] = (int32_t)QS;
+            bL = L; bS = S; bUL = UL; bUS = US; bQL = QL; bQS = QS;
             threads = (int)NT;
             sdq = QM;
             sdr = RM;
         }
     }
     if (bestFill <= 0) return false;
-    tp = bestTp;
+    tp.sdSlot[0] = bL.slot; tp.sdR[0] = bL.R; tp.sdC[0] = bL.C;
+    tp.sdU[0] = (int32_t)bUL; tp.sdQ[0] = (int32_t)bQL;
+    tp.sdSlot[1] = bS.slot; tp.sdR[1] = bS.R; tp.sdC[1] = bS.C;
+    tp.sdU[1] = (int32_t)bUS; tp.sdQ[1] = (int32_t)bQS;
     return true;
 }
 
@@ -498,19 +572,134 @@ static void tile_need(const Problem& pr, int64_t Tin, int64_t Tout, int64_t* nee
     }
 }
 
-// Build the tile with extents need[] (from tile_need).
-static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSplit, int outSplit,
-                                int Vmax, const DeviceInfo& dev, int forceThreads, int maxR,
-                                int forceR, int VmaxSd, bool full = true) {
-    TileCand c;
+// DRAM side of the tile model for extents need[] (no parameter block): the
+// contiguous runs inside a full tile, their sector counts at the runs'
+// alignment, and the modelled bytes of the whole launch.  False when the
+// tile cannot be built (too large, a split chunk over the kernel's 8-bit
+// packing, staging over the shared-memory limit).  The searches use
+// bytes / bandwidth + launch as a lower bound of a tile's cost.
+struct TileDram {
+    int32_t V = 0;
+    int64_t runIn = 0, runOut = 0;
+    int smem = 0;
+    double secIn = 0, secOut = 0, dram_eff = 0, bytes = 0;
+    double nTiles = 0;
+};
+static bool tile_dram(const Problem& pr, const int64_t* need, int Vlimit, const DeviceInfo& dev,
+                      TileDram& t) {
     const int n = pr.n;
-    long double V = 1;
-    for (int i = 0; i < n; ++i) V *= (long double)need[i];
-    if (V > std::max(Vmax, VmaxSd)) return c;
+    int64_t V = 1;
+    for (int i = 0; i < n; ++i)
+        if (__builtin_mul_overflow(V, need[i], &V) || V > Vlimit) return false;
+    t.V = (int32_t)V;
+    t.nTiles = 1;
+    for (int i = 0; i < n; ++i) {
+        if (need[i] == 1) {
+            t.nTiles *= (double)pr.d[i];
+        } else if (need[i] < pr.d[i]) {
+            if (need[i] > 256) return false;  // split chunk: 8-bit packing
+            t.nTiles *= (double)ceil_div(pr.d[i], need[i]);
+        }
+    }
+    {
+        int64_t r = 1;
+        for (int i = 0; i < n; ++i) {
+            r *= need[i];
+            if (need[i] < pr.d[i]) break;
+        }
+        t.runIn = std::min<int64_t>(r, t.V);
+        r = 1;
+        for (int j = 0; j < n; ++j) {
+            int i = pr.p[j];
+            r *= need[i];
+            if (need[i] < pr.d[i]) break;
+        }
+        t.runOut = std::min<int64_t>(r, t.V);
+    }
+    // smem footprint with the worst-case padding (layout chosen for the winner)
+    {
+        int64_t words = t.V + t.V / 4 + 64;  // choose_smem's padding cap
+        t.smem = (int)(2 * ((words + 3) / 4 * 4) * pr.esize);
+        if (t.smem > dev.max_smem_per_block) return false;
+    }
+    const double E = pr.esize;
+    // alignment of the runs' starts: strides of the tile dims outside the
+    // run and of the grid dims (need 1, or a split dim's chunk stride)
+    int64_t aIn = 256, aOut = 256;  // allocations are at least 256-byte aligned
+    for (int i = 0; i < n; ++i) {
+        const bool tileDim = need[i] > 1, gridDim = need[i] == 1 || need[i] < pr.d[i];
+        if (tileDim && pr.sin[i] >= t.runIn) aIn = std::min(aIn, pow2_align(pr.sin[i] * pr.esize));
+        if (tileDim && pr.sout[i] >= t.runOut) aOut = std::min(aOut, pow2_align(pr.sout[i] * pr.esize));
+        if (gridDim) {
+            aIn = std::min(aIn, pow2_align(need[i] * pr.sin[i] * pr.esize));
+            aOut = std::min(aOut, pow2_align(need[i] * pr.sout[i] * pr.esize));
+        }
+    }
+    aIn = std::max<int64_t>(aIn, pr.esize);
+    aOut = std::max<int64_t>(aOut, pr.esize);
+    t.secIn = run_sectors(t.runIn * E, aIn) * ((double)t.V / t.runIn);
+    t.secOut = run_sectors(t.runOut * E, aOut) * ((double)t.V / t.runOut);
+    // partial-sector reads of neighbouring runs usually hit in L2; partial
+    // writes cost a read-modify-write -- weight them fully.
+    const double usefulSec = 2.0 * t.V * E / model::kSector;
+    const double modelSec = 0.5 * (t.secIn + t.V * E / model::kSector) + t.secOut +
+                            ((double)t.V / t.runIn + (double)t.V / t.runOut) * model::kRunBytes /
+                                model::kSector;
+    t.dram_eff = usefulSec / modelSec;
+    // DRAM bytes scale with the elements actually moved (ragged tiles move fewer)
+    t.bytes = (double)pr.vol / t.V * modelSec * model::kSector;
+    return true;
+}
+// A lower bound of build_tile_need's cost over every launch shape it may
+// pick: memory time at full memory-level parallelism; issue time with the
+// fewest instructions any shape issues (every element one slot of the
+// cheaper slot-dim kind, one warp's per-tile overhead); the per-tile latency
+// floor at the most CTAs per SM any shape reaches (estimate_occupancy: the
+// shapes use >= V/16 threads and >= 4 V registers, the same staging bytes).
+// The cost combines max + 0.25 * rest, nondecreasing in each term; the 1e-9
+// margin keeps the bound below the rounded cost.
+static double tile_cost_lb(const TileDram& t, int esize, const DeviceInfo& dev) {
+    const double t_mem = t.bytes / model::kBwBytesPerUs;
+    const double perTile = model::kTileInstr + t.V / 32.0 * model::kSlotInstrSd * (esize > 4 ? 1.25 : 1.0);
+    const double t_issue = t.nTiles * perTile / model::kIssuePerClk / std::max(1, dev.num_sms) / model::kClockMHz;
+    const double bySmem = (double)(dev.max_smem_per_sm / (t.smem + 1024));
+    const double byThreads = dev.max_threads_per_sm / std::max(32.0, t.V / 16.0);
+    const double byRegs = dev.regs_per_sm / (4.0 * t.V);
+    const double occ = std::max(1.0, std::floor(std::min({32.0, bySmem, byThreads, byRegs})));
+    const double t_lat = std::ceil(t.nTiles / ((double)dev.num_sms * occ)) * model::kTileLatUs;
+    const double top = std::max({t_mem, t_issue, t_lat});
+    return (top + 0.25 * (t_mem + t_issue + t_lat - top) + model::kLaunchUs) * (1.0 - 1e-9);
+}
+
+// Build the tile with extents need[] (from tile_need).
+// `full`: the whole parameter block (the winner); otherwise only what the
+// searches compare is valid (c.tp's arrays beyond the tile's a / h entries
+// are left as they were -- the memo reuses one scratch candidate).
+static void build_tile_need(TileCand& c, const Problem& pr, const int64_t* need, int inSplit,
+                            int outSplit, int Vmax, const DeviceInfo& dev, int forceThreads,
+                            int maxR, int forceR, int VmaxSd, bool full = true,
+                            const TileDram* known = nullptr) {
+    c.runIn = c.runOut = 0;
+    c.threads = c.nreg = 0;
+    c.cost_us = 1e30;
+    c.dram_eff = c.secIn = c.secOut = c.inflight = 0;
+    c.smem = 0;
+    c.ok = false;
+    c.sd = false;
+    c.sdq = c.sdr = 0;
+    const int n = pr.n;
+    TileDram dr;
+    if (known) dr = *known;
+    else if (!tile_dram(pr, need, std::max(Vmax, VmaxSd), dev, dr)) return;
 
     TileParams& tp = c.tp;
-    std::memset(&tp, 0, sizeof(tp));
-    tp.V = (int32_t)V;
+    if (full) {
+        std::memset(&tp, 0, sizeof(tp));
+    } else {
+        tp.nSplit = 0;
+        for (int ph = 0; ph < 2; ++ph) tp.sdSlot[ph] = tp.sdR[ph] = tp.sdC[ph] = tp.sdU[ph] = tp.sdQ[ph] = 0;
+    }
+    tp.V = dr.V;
     // tile dims: need > 1, ascending input dim
     int tileOf[kMaxDims];
     tp.a = 0;
@@ -570,62 +759,20 @@ static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSp
     }
     tp.nTiles = acc;
     if (full) fill_magic(tp);  // the searches only compare costs; the winner is rebuilt in full
-    for (int s = 0; s < tp.nSplit; ++s)
-        if (tp.splitChunk[s] > 256) return c;  // kernel packs split coordinates in 8 bits
-
-    // contiguous runs inside a full tile
-    {
-        int64_t r = 1;
-        for (int i = 0; i < n; ++i) {
-            r *= need[i];
-            if (need[i] < pr.d[i]) break;
-        }
-        c.runIn = std::min<int64_t>(r, tp.V);
-        r = 1;
-        for (int j = 0; j < n; ++j) {
-            int i = pr.p[j];
-            r *= need[i];
-            if (need[i] < pr.d[i]) break;
-        }
-        c.runOut = std::min<int64_t>(r, tp.V);
-    }
-
-    // smem footprint with the worst-case padding (layout chosen for the winner)
-    {
-        int64_t words = tp.V + tp.V / 4 + 64;  // choose_smem's padding cap
-        c.smem = (int)(2 * ((words + 3) / 4 * 4) * pr.esize);
-        if (c.smem > dev.max_smem_per_block) return c;
-    }
+    c.runIn = dr.runIn;
+    c.runOut = dr.runOut;
+    c.smem = dr.smem;
 
     // model: DRAM sectors of full tiles + slot issue + per-tile overhead,
     // minimised over the launch shape (threads x slots, NT*NREG >= V)
     {
         const double E = pr.esize;
-        int64_t aIn = 256;  // allocations are at least 256-byte aligned
-        for (int t = 0; t < tp.a; ++t)
-            if (tp.tSin[t] >= c.runIn) aIn = std::min(aIn, pow2_align(tp.tSin[t] * pr.esize));
-        for (int g = 0; g < tp.h; ++g) aIn = std::min(aIn, pow2_align(tp.gSin[g] * pr.esize));
-        int64_t aOut = 256;
-        for (int t = 0; t < tp.a; ++t)
-            if (tp.tSout[t] >= c.runOut) aOut = std::min(aOut, pow2_align(tp.tSout[t] * pr.esize));
-        for (int g = 0; g < tp.h; ++g) aOut = std::min(aOut, pow2_align(tp.gSout[g] * pr.esize));
-        aIn = std::max<int64_t>(aIn, pr.esize);
-        aOut = std::max<int64_t>(aOut, pr.esize);
-        double secIn = run_sectors(c.runIn * E, aIn) * ((double)tp.V / c.runIn);
-        double secOut = run_sectors(c.runOut * E, aOut) * ((double)tp.V / c.runOut);
-        // partial-sector reads of neighbouring runs usually hit in L2; partial
-        // writes cost a read-modify-write -- weight them fully.
-        double usefulSec = 2.0 * tp.V * E / model::kSector;
-        double modelSec = 0.5 * (secIn + tp.V * E / model::kSector) + secOut +
-                          ((double)tp.V / c.runIn + (double)tp.V / c.runOut) * model::kRunBytes /
-                              model::kSector;
-        c.dram_eff = usefulSec / modelSec;
-        c.secIn = secIn;
-        c.secOut = secOut;
-        // slots of ragged tiles are partly idle but still issued
-        // DRAM bytes scale with the elements actually moved (ragged tiles move
-        // fewer), issue cost with the tiles launched (ragged slots still issue)
-        const double bytes = (double)pr.vol / tp.V * modelSec * model::kSector;
+        c.dram_eff = dr.dram_eff;
+        c.secIn = dr.secIn;
+        c.secOut = dr.secOut;
+        const double bytes = dr.bytes;
+        // slots of ragged tiles are partly idle but still issued (issue cost
+        // scales with the tiles launched)
         const bool idx64 = pr.span >= (int64_t(1) << 31);
         // cost of one launch shape: memory time at the loads in flight it
         // allows, issue time, per-tile latency floor
@@ -675,15 +822,15 @@ static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSp
         // tables, so more CTAs (tiles in flight) per SM and tiles up to
         // VmaxSd elements
         if (VmaxSd > 0 && !idx64 && !forceThreads && !forceR) {
-            TileParams tsd = tp;
             int thr = 0, q = 0, r = 0, per = 0;
             auto occOf = [&](int T, int qq, int rr) {
                 const OccQuery qs{TT_KERNEL_TILE, pr.esize, qq * rr, 1, T, c.smem, false, 0, 0, 0, qq, rr};
                 return estimate_occupancy(qs, dev);
             };
-            if (build_sd(tsd, pr.esize, c.runIn, c.runOut, occOf, thr, q, r, per)) {
+            // build_sd writes only the sd* fields of tp (kept if it wins)
+            if (build_sd(tp, pr.esize, c.runIn, c.runOut, occOf, thr, q, r, per)) {
                 double inflight = 0;
-                const int slots = std::max(tsd.sdQ[0] * tsd.sdR[0], tsd.sdQ[1] * tsd.sdR[1]);
+                const int slots = std::max(tp.sdQ[0] * tp.sdR[0], tp.sdQ[1] * tp.sdR[1]);
                 const double cost = shape_cost(thr, slots, per, model::kSlotInstrSd, inflight);
                 if (c.threads == 0 || cost < c.cost_us) {
                     c.cost_us = cost;
@@ -693,14 +840,15 @@ static TileCand build_tile_need(const Problem& pr, const int64_t* need, int inSp
                     c.sd = true;
                     c.sdq = q;
                     c.sdr = r;
-                    c.tp = tsd;
+                } else {
+                    for (int ph = 0; ph < 2; ++ph)
+                        tp.sdSlot[ph] = tp.sdR[ph] = tp.sdC[ph] = tp.sdU[ph] = tp.sdQ[ph] = 0;
                 }
             }
         }
-        if (c.threads == 0) return c;
+        if (c.threads == 0) return;
     }
     c.ok = true;
-    return c;
 }
 
 // Build the tile of candidate run targets (Tin, Tout) in elements.
@@ -710,7 +858,9 @@ static TileCand build_tile(const Problem& pr, int64_t Tin, int64_t Tout, int Vma
     int64_t need[kMaxDims];
     int inSplit, outSplit;
     tile_need(pr, Tin, Tout, need, inSplit, outSplit);
-    return build_tile_need(pr, need, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd);
+    TileCand c;
+    build_tile_need(c, pr, need, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd);
+    return c;
 }
 
 // Many run-target pairs give the same tile (a dim is taken whole from one
@@ -737,8 +887,24 @@ struct TileMemo {
                 return false;
         return true;
     }
-    std::vector<int64_t> keys;   // kMaxDims + 4 per entry
-    std::vector<TileSumm> val;
+    // One entry per distinct tile (extents, split dims, launch limits): the
+    // DRAM model (with the tile volume, checked against each query's limit)
+    // and, per slot-dim limit VmaxSd asked for, the full summary once the
+    // lower bound did not settle a query.
+    struct Slot {
+        int VmaxSd = -1;
+        bool full = false;
+        TileSumm sm;
+    };
+    struct Ent {
+        bool buildable = false;
+        TileDram dr;
+        double lb = 0;  // tile_cost_lb (buildable entries)
+        int64_t Tin = 0, Tout = 0;
+        Slot slot[2];
+    };
+    std::vector<int64_t> keys;   // kMaxDims + 3 per entry
+    std::vector<Ent> val;
     std::vector<int> table;      // open addressing over entry indices, -1 = empty
     int width = 0;
 
@@ -747,42 +913,39 @@ struct TileMemo {
         for (int i = 0; i < n; ++i) h = (h ^ (uint64_t)k[i]) * 1099511628211ull;
         return h ^ (h >> 29);
     }
-    TileSumm get(const Problem& p, int64_t Tin, int64_t Tout, int Vmax, const DeviceInfo& dev,
-                 int forceThreads, int maxR, int forceR, int VmaxSd) {
-        if (!same_problem(p)) {  // (re)bind to this problem
-            prob = p;
-            bound = true;
-            width = p.n + 4;
-            keys.clear();
-            val.clear();
-            table.assign(1024, -1);
-        }
-        int64_t k[kMaxDims + 4];
-        int inSplit, outSplit;
-        tile_need(p, Tin, Tout, k, inSplit, outSplit);
+    void bind(const Problem& p) {
+        if (same_problem(p)) return;
+        prob = p;
+        bound = true;
+        width = p.n + 3;
+        keys.clear();
+        val.clear();
+        table.assign(1024, -1);
+    }
+    // The entry of the tile with extents need[] (derived from run targets
+    // (Tin, Tout) by tile_need); the memo must be bound to p.
+    int lookup(const Problem& p, const int64_t* need, int inSplit, int outSplit, int64_t Tin, int64_t Tout,
+               int Vmax, const DeviceInfo& dev, int forceThreads, int maxR, int forceR) {
+        int64_t k[kMaxDims + 3];
+        std::memcpy(k, need, sizeof(int64_t) * p.n);
         k[p.n] = Vmax;
-        k[p.n + 1] = VmaxSd;
-        k[p.n + 2] = (int64_t)(inSplit + 1) * 64 + (outSplit + 1);
-        k[p.n + 3] = (int64_t)forceThreads * 4096 + maxR * 64 + forceR;
+        k[p.n + 1] = (int64_t)(inSplit + 1) * 64 + (outSplit + 1);
+        k[p.n + 2] = (int64_t)forceThreads * 4096 + maxR * 64 + forceR;
         const size_t mask = table.size() - 1;
         size_t h = hash(k, width) & mask;
         for (; table[h] >= 0; h = (h + 1) & mask) {
             const int64_t* y = &keys[(size_t)table[h] * width];
-            if (std::memcmp(k, y, sizeof(int64_t) * width) == 0) return val[table[h]];
+            if (std::memcmp(k, y, sizeof(int64_t) * width) == 0) return table[h];
         }
-        const TileCand c = build_tile_need(p, k, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR,
-                                           VmaxSd, false);
-        TileSumm sm;
-        sm.ok = c.ok;
-        sm.cost = c.cost_us;
-        sm.runIn = c.runIn;
-        sm.runOut = c.runOut;
-        sm.Tin = Tin;
-        sm.Tout = Tout;
-        sm.VmaxSd = VmaxSd;
-        table[h] = (int)val.size();
+        Ent e;
+        e.buildable = tile_dram(p, need, 1 << 30, dev, e.dr);  // volume limit: per query
+        if (e.buildable) e.lb = tile_cost_lb(e.dr, p.esize, dev);
+        e.Tin = Tin;
+        e.Tout = Tout;
+        const int idx = (int)val.size();
+        table[h] = idx;
         keys.insert(keys.end(), k, k + width);
-        val.push_back(sm);
+        val.push_back(e);
         if (val.size() * 2 > table.size()) {  // grow and rehash
             std::vector<int> t2(table.size() * 2, -1);
             const size_t m2 = t2.size() - 1;
@@ -793,7 +956,47 @@ struct TileMemo {
             }
             table.swap(t2);
         }
-        return sm;
+        return idx;
+    }
+    // The summary of entry e under slot-dim limit VmaxSd.  A tile whose cost
+    // cannot go below `below` (its DRAM lower bound is already >= below) is
+    // reported as not ok without running the launch-shape model: the
+    // searches only replace their incumbent on a strictly lower cost, so
+    // such a tile could not have won.
+    TileSumm summary(Ent& e, const Problem& p, const int64_t* need, int inSplit, int outSplit, int Vmax,
+                     const DeviceInfo& dev, int forceThreads, int maxR, int forceR, int VmaxSd,
+                     double below) {
+        TileSumm none;
+        none.Tin = e.Tin;
+        none.Tout = e.Tout;
+        none.VmaxSd = VmaxSd;
+        if (!e.buildable || e.dr.V > std::max(Vmax, VmaxSd)) return none;  // ok = false
+        Slot* sl = e.slot[0].VmaxSd == VmaxSd ? &e.slot[0] : e.slot[1].VmaxSd == VmaxSd ? &e.slot[1] : nullptr;
+        if (sl && sl->full) return sl->sm;
+        if (e.lb >= below) return none;  // cannot win against the caller's incumbent
+        if (!sl) {
+            sl = e.slot[0].VmaxSd < 0 ? &e.slot[0] : &e.slot[1];
+            sl->VmaxSd = VmaxSd;
+        }
+        thread_local TileCand c;  // scratch: summaries only
+        build_tile_need(c, p, need, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd, false,
+                        &e.dr);
+        sl->full = true;
+        sl->sm = none;
+        sl->sm.ok = c.ok;
+        sl->sm.cost = c.cost_us;
+        sl->sm.runIn = c.runIn;
+        sl->sm.runOut = c.runOut;
+        return sl->sm;
+    }
+    TileSumm get(const Problem& p, int64_t Tin, int64_t Tout, int Vmax, const DeviceInfo& dev,
+                 int forceThreads, int maxR, int forceR, int VmaxSd, double below = 1e300) {
+        bind(p);
+        int64_t need[kMaxDims];
+        int inSplit, outSplit;
+        tile_need(p, Tin, Tout, need, inSplit, outSplit);
+        Ent& e = val[lookup(p, need, inSplit, outSplit, Tin, Tout, Vmax, dev, forceThreads, maxR, forceR)];
+        return summary(e, p, need, inSplit, outSplit, Vmax, dev, forceThreads, maxR, forceR, VmaxSd, below);
     }
 };
 
@@ -860,18 +1063,32 @@ static void choose_smem_search(TileParams& tp, int esize) {
     // pad[i] moves the strides of dims >= i only: dims above the highest one
     // that varies inside a sampled access cannot change any cost
     const int hi = std::min(a - 1, sample.maxVary);
+    SmemLine ln;
+    // coordinate descent; a dim is re-searched only if another pad changed
+    // since its last search (otherwise it would find the same answer)
+    int changes = 0, seenAt[kMaxDims];
+    for (int i = 0; i < a; ++i) seenAt[i] = -1;
     for (int pass = 0; pass < 2 && best > ideal; ++pass) {
         for (int i = 1; i <= hi && best > ideal; ++i) {
+            if (seenAt[i] == changes) continue;
             int32_t keep = pad[i];
             int32_t bestPad = keep;
-            for (int c = 0; c < 32; ++c) {
-                pad[i] = c;
-                const int64_t foot = strides(pad, sm);
-                if (foot > limit) continue;
-                const long cst = smem_cost(sample, esize, sm, best);
+            pad[i] = 0;
+            const int64_t foot0 = strides(pad, sm);
+            int64_t coef[kMaxDims] = {}, footW = 0, acc = 1;
+            for (int j = i; j < a; acc *= tp.tExt[j], ++j) {
+                coef[j] = acc;
+                footW += (tp.tExt[j] - 1) * acc;
+            }
+            const int period = smem_line(sample, sm, coef, ln);
+            for (int c = 0; c < period; ++c) {
+                if (foot0 + c * footW > limit) continue;
+                const long cst = smem_cost_at(sample, esize, ln, c, best);
                 if (cst < best) { best = cst; bestPad = c; }
             }
             pad[i] = bestPad;
+            if (bestPad != keep) ++changes;
+            seenAt[i] = changes;
         }
     }
     const int64_t foot = strides(pad, sm);
@@ -941,13 +1158,21 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
     const SmemSample sample = smem_sample(tp, 2, qshift);
     strides();
     long best = smem_cost(sample, E, sm);
+    SmemLine ln;
     for (int pass = 0; pass < 2; ++pass)
         for (int t = M; t < tp.a; ++t) {
             int32_t bestPad = pad[t];
-            for (int c = 0; c < 32; c += VPC) {
-                pad[t] = c;
-                if (strides() * E > 65536 * 2) continue;
-                const long cst = smem_cost(sample, E, sm, best);
+            pad[t] = 0;
+            const int64_t foot0 = strides();
+            int64_t coef[kMaxDims] = {}, footW = 0, acc = 1;
+            for (int j = t; j < tp.a; acc *= tp.tExt[j], ++j) {
+                coef[j] = acc;
+                footW += (tp.tExt[j] - 1) * acc;
+            }
+            const int period = std::max(smem_line(sample, sm, coef, ln), VPC);
+            for (int c = 0; c < period; c += VPC) {
+                if ((foot0 + c * footW) * E > 65536 * 2) continue;
+                const long cst = smem_cost_at(sample, E, ln, c, best);
                 if (cst < best) { best = cst; bestPad = c; }
             }
             pad[t] = bestPad;
@@ -1338,54 +1563,149 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     const int forceR = opts ? opts->slots : 0;
     TileMemo localMemo;
     TileMemo& memo = sharedMemo ? *sharedMemo : localMemo;
-    auto search = [&](const std::vector<int64_t>& tin, const std::vector<int64_t>& tout, TileSumm& b) {
-        for (int64_t ti : tin) {
-            for (int64_t to : tout) {
-                int64_t Tin = opts && opts->run_in ? opts->run_in : ti;
-                int64_t Tout = opts && opts->run_out ? opts->run_out : to;
+    const bool runsForced = opts && (opts->run_in || opts->run_out);
+    if (runsForced) {
+        // forced run target(s): the other side still searches the targets
+        for (int64_t ti : targets)
+            for (int64_t to : targets) {
+                const int64_t Tin = opts->run_in ? opts->run_in : ti;
+                const int64_t Tout = opts->run_out ? opts->run_out : to;
                 const TileSumm c = memo.get(pr, Tin, Tout, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                            VmaxSd);
-                if (!c.ok) continue;
-                if (!b.ok || c.cost < b.cost) b = c;
+                                            VmaxSd, best.ok ? best.cost : 1e300);
+                if (c.ok && (!best.ok || c.cost < best.cost)) best = c;
+            }
+    } else {
+        // Three searches, each the first strictly cheapest tile over its pairs
+        // of run targets in ascending order: S1 over targets^2, S2 over
+        // (targets + prefix)^2, S3 (slot-dim tiles, VmaxSdRule) over (targets +
+        // prefix + slot-dim prefix)^2.  The lists are sorted, so one pass over
+        // the largest set visits each search's pairs in that search's order.
+        std::vector<int64_t> sdPrefix;
+        if (VmaxSdRule > 0) {
+            for (int i = 0, P = 1; i < pr.n && P * pr.d[i] <= VmaxSdRule; ++i) {
+                P *= (int)pr.d[i];
+                if (P >= 2) sdPrefix.push_back(P);
+            }
+            for (int j = 0, P = 1; j < pr.n && P * pr.d[pr.p[j]] <= VmaxSdRule; ++j) {
+                P *= (int)pr.d[pr.p[j]];
+                if (P >= 2) sdPrefix.push_back(P);
             }
         }
-    };
-    search(targets, targets, best);
-    if (!prefix.empty() && !(opts && (opts->run_in || opts->run_out))) {
-        std::vector<int64_t> all = targets;
-        all.insert(all.end(), prefix.begin(), prefix.end());
-        std::sort(all.begin(), all.end());
-        all.erase(std::unique(all.begin(), all.end()), all.end());
-        TileSumm px;
-        search(all, all, px);
-        const bool keepsOut = best.ok && px.ok && px.runOut >= best.runOut &&
-                              (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
-        if (px.ok && (!best.ok || (px.cost < best.cost && keepsOut)))
-            best = px;
-    }
-    if (VmaxSdRule > 0 && !(opts && (opts->run_in || opts->run_out)) && best.ok) {
-        std::vector<int64_t> all = targets;
-        all.insert(all.end(), prefix.begin(), prefix.end());
-        for (int i = 0, P = 1; i < pr.n && P * pr.d[i] <= VmaxSdRule; ++i) {
-            P *= (int)pr.d[i];
-            if (P >= 2) all.push_back(P);
-        }
-        for (int j = 0, P = 1; j < pr.n && P * pr.d[pr.p[j]] <= VmaxSdRule; ++j) {
-            P *= (int)pr.d[pr.p[j]];
-            if (P >= 2) all.push_back(P);
-        }
-        std::sort(all.begin(), all.end());
-        all.erase(std::unique(all.begin(), all.end()), all.end());
-        TileSumm sx;
-        for (int64_t ti : all)
-            for (int64_t to : all) {
-                const TileSumm c = memo.get(pr, ti, to, Vmax, dev, forceThreads, acc ? 8 : 16, forceR,
-                                            VmaxSdRule);
-                if (c.ok && (!sx.ok || c.cost < sx.cost)) sx = c;
+        std::vector<int64_t> cand = targets;
+        cand.insert(cand.end(), prefix.begin(), prefix.end());
+        cand.insert(cand.end(), sdPrefix.begin(), sdPrefix.end());
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        const int nc = (int)cand.size();
+        // per candidate: membership (bit 0: targets, bit 1: targets + prefix)
+        // and the tile extents each side asks for (tile_need, one side each)
+        std::vector<int> member(nc, 0);
+        std::vector<int64_t> sideIn((size_t)nc * pr.n), sideOut((size_t)nc * pr.n);
+        std::vector<int> splitIn(nc), splitOut(nc);
+        for (int k = 0; k < nc; ++k) {
+            const int64_t v = cand[k];
+            if (std::binary_search(targets.begin(), targets.end(), v)) member[k] |= 3;
+            if (std::binary_search(prefix.begin(), prefix.end(), v)) member[k] |= 2;
+            // one side of tile_need each: need = the elementwise max of both
+            int64_t P = 1;
+            splitIn[k] = -1;
+            for (int i = 0; i < pr.n; ++i) sideIn[(size_t)k * pr.n + i] = 1;
+            for (int i = 0; i < pr.n; ++i) {
+                if (P * pr.d[i] >= v) {
+                    const int64_t ch = std::min(pr.d[i], ceil_div(v, P));
+                    sideIn[(size_t)k * pr.n + i] = ch;
+                    if (ch < pr.d[i]) splitIn[k] = i;
+                    break;
+                }
+                sideIn[(size_t)k * pr.n + i] = pr.d[i];
+                P *= pr.d[i];
             }
-        const bool keepsOut = sx.ok && sx.runOut >= best.runOut &&
-                              (2 * sx.runIn >= best.runIn || sx.runOut >= 2 * best.runOut);
-        if (sx.ok && sx.cost < best.cost && keepsOut) best = sx;
+            P = 1;
+            splitOut[k] = -1;
+            for (int i = 0; i < pr.n; ++i) sideOut[(size_t)k * pr.n + i] = 1;
+            for (int j = 0; j < pr.n; ++j) {
+                const int i = pr.p[j];
+                if (P * pr.d[i] >= v) {
+                    const int64_t ch = std::min(pr.d[i], ceil_div(v, P));
+                    sideOut[(size_t)k * pr.n + i] = ch;
+                    if (ch < pr.d[i]) splitOut[k] = i;
+                    break;
+                }
+                sideOut[(size_t)k * pr.n + i] = pr.d[i];
+                P *= pr.d[i];
+            }
+        }
+        memo.bind(pr);
+        const bool s3 = VmaxSdRule > 0;
+        // Pass 1: the distinct tiles of every search and, per search, the
+        // first pair (in that search's order) giving each.  Pair index
+        // x * nc + y follows every search's own order.
+        std::vector<int> first[3];  // per memo entry: first pair index in S1 / S2 / S3, -1 = none
+        std::vector<int> ents;      // distinct entries in order of appearance
+        for (int x = 0; x < nc; ++x) {
+            const int64_t* ni = &sideIn[(size_t)x * pr.n];
+            for (int y = 0; y < nc; ++y) {
+                const int m = member[x] & member[y];
+                if (!m && !s3) continue;
+                const int64_t* no = &sideOut[(size_t)y * pr.n];
+                int64_t need[kMaxDims];
+                for (int i = 0; i < pr.n; ++i) need[i] = std::max(ni[i], no[i]);
+                const int e = memo.lookup(pr, need, splitIn[x], splitOut[y], cand[x], cand[y], Vmax, dev,
+                                          forceThreads, acc ? 8 : 16, forceR);
+                if ((size_t)e >= first[0].size())
+                    for (auto& f : first) f.resize(memo.val.size() + nc * nc, -1);
+                const int pi = x * nc + y;
+                if (first[0][e] < 0 && first[1][e] < 0 && first[2][e] < 0) ents.push_back(e);
+                if ((m & 1) && first[0][e] < 0) first[0][e] = pi;
+                if ((m & 2) && first[1][e] < 0) first[1][e] = pi;
+                if (s3 && first[2][e] < 0) first[2][e] = pi;
+            }
+        }
+        // Pass 2, per search: the tile with the lowest (cost, first pair) --
+        // the first strictly cheapest in the search's order.  Tiles are
+        // visited by ascending DRAM lower bound; once that bound exceeds the
+        // incumbent's cost no later tile can win (cost >= bound), so only the
+        // tiles that might are given the full launch-shape model.
+        auto run = [&](int k, int vsd, TileSumm& b) {
+            std::vector<std::pair<double, int>> order;  // (lower bound, entry)
+            for (int e : ents)
+                if (first[k][e] >= 0 && memo.val[e].buildable) order.push_back({memo.val[e].lb, e});
+            std::sort(order.begin(), order.end(), [&](const std::pair<double, int>& u, const std::pair<double, int>& v) {
+                return u.first < v.first || (u.first == v.first && first[k][u.second] < first[k][v.second]);
+            });
+            int bIdx = -1;
+            for (const auto& o : order) {
+                const int e = o.second, pi = first[k][e];
+                if (b.ok && (o.first > b.cost || (o.first == b.cost && pi > bIdx))) break;
+                const int x = pi / nc, y = pi % nc;
+                int64_t need[kMaxDims];
+                for (int i = 0; i < pr.n; ++i)
+                    need[i] = std::max(sideIn[(size_t)x * pr.n + i], sideOut[(size_t)y * pr.n + i]);
+                const TileSumm c = memo.summary(memo.val[e], pr, need, splitIn[x], splitOut[y], Vmax, dev,
+                                                forceThreads, acc ? 8 : 16, forceR, vsd, 1e300);
+                if (c.ok && (!b.ok || c.cost < b.cost || (c.cost == b.cost && pi < bIdx))) {
+                    b = c;
+                    bIdx = pi;
+                }
+            }
+        };
+        TileSumm b2, b3;
+        run(0, VmaxSd, best);
+        run(1, VmaxSd, b2);
+        if (s3) run(2, VmaxSdRule, b3);
+        if (!prefix.empty()) {
+            const TileSumm& px = b2;
+            const bool keepsOut = best.ok && px.ok && px.runOut >= best.runOut &&
+                                  (2 * px.runIn >= best.runIn || px.runOut >= 2 * best.runOut);
+            if (px.ok && (!best.ok || (px.cost < best.cost && keepsOut)))
+                best = px;
+        }
+        if (s3 && best.ok) {
+            const TileSumm& sx = b3;
+            const bool keepsOut = sx.ok && sx.runOut >= best.runOut &&
+                                  (2 * sx.runIn >= best.runIn || sx.runOut >= 2 * best.runOut);
+            if (sx.ok && sx.cost < best.cost && keepsOut) best = sx;
+        }
     }
     TileCand bestTile;
     if (best.ok)  // the winner in full
