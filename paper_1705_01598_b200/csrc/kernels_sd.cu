@@ -53,14 +53,20 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
         for (int q = 0; q < QM; ++q) {
             if (q >= QL) break;
             const uint32_t c = (cntL[q] >> sh) & 0xffu;
+            // slot addresses chained (one IMAD.WIDE per slot)
             const W* __restrict__ src = opaque(in + tb.in + gin[q]);
             if (c == (uint32_t)RM) {
 #pragma unroll
-                for (int r = 0; r < RM; ++r) v[q][r] = ldg_(elem_addr(src, (uint32_t)r * sIn));
+                for (int r = 0; r < RM; ++r) {
+                    v[q][r] = ldg_(src);
+                    src = elem_addr(src, sIn);
+                }
             } else {
 #pragma unroll
-                for (int r = 0; r < RM; ++r)
-                    if ((uint32_t)r < c) v[q][r] = ldg_(elem_addr(src, (uint32_t)r * sIn));
+                for (int r = 0; r < RM; ++r) {
+                    if ((uint32_t)r < c) v[q][r] = ldg_(src);
+                    src = elem_addr(src, sIn);
+                }
             }
         }
     };
@@ -76,10 +82,12 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             for (int q = 0; q < QM; ++q) {
                 if (q >= QL) break;
                 const uint32_t c = (cntL[q] >> sh) & 0xffu;
-                const uint32_t a0 = sb + (smp[q] & 0xffffu);
+                uint32_t a = sb + (smp[q] & 0xffffu);
 #pragma unroll
-                for (int r = 0; r < RM; ++r)
-                    if ((uint32_t)r < c) sts(a0 + (uint32_t)r * mIn, v[q][r]);
+                for (int r = 0; r < RM; ++r) {
+                    if ((uint32_t)r < c) sts(a, v[q][r]);
+                    a += mIn;
+                }
             }
         }
         __syncthreads();
@@ -100,16 +108,21 @@ tile_sd_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
                 if (q >= QS) break;
                 const uint32_t c = (cntS[q] >> sh) & 0xffu;
                 W* __restrict__ dst = opaque(out + now.out + gout[q]);
-                const uint32_t a0 = sb + (smp[q] >> 16);
+                uint32_t a = sb + (smp[q] >> 16);
                 if (c == (uint32_t)RM) {
 #pragma unroll
-                    for (int r = 0; r < RM; ++r)
-                        stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                    for (int r = 0; r < RM; ++r) {
+                        stg_(dst, lds<W>(a));
+                        dst = elem_addr(dst, sOut);
+                        a += mOut;
+                    }
                 } else {
 #pragma unroll
-                    for (int r = 0; r < RM; ++r)
-                        if ((uint32_t)r < c)
-                            stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                    for (int r = 0; r < RM; ++r) {
+                        if ((uint32_t)r < c) stg_(dst, lds<W>(a));
+                        dst = elem_addr(dst, sOut);
+                        a += mOut;
+                    }
                 }
             }
         }
@@ -174,10 +187,13 @@ tile_sd_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__
             if (q >= QL) break;
             const uint32_t c = (cntL[q] >> sh) & 0xffu;
             const W* src = in + tb.in + gin[q];
-            const uint32_t a0 = sb + (smp[q] & 0xffffu);
+            uint32_t a = sb + (smp[q] & 0xffffu);
 #pragma unroll
-            for (int r = 0; r < RM; ++r)
-                if ((uint32_t)r < c) cp_async<sizeof(W)>(a0 + (uint32_t)r * mIn, elem_addr(src, (uint32_t)r * sIn));
+            for (int r = 0; r < RM; ++r) {
+                if ((uint32_t)r < c) cp_async<sizeof(W)>(a, src);
+                src = elem_addr(src, sIn);
+                a += mIn;
+            }
         }
     };
 #pragma unroll
@@ -209,16 +225,21 @@ tile_sd_async_kernel(const __grid_constant__ TileParams p, const W* __restrict__
             if (q >= QS) break;
             const uint32_t c = (cntS[q] >> sh) & 0xffu;
             W* __restrict__ dst = opaque(out + now.out + gout[q]);
-            const uint32_t a0 = sb + (smp[q] >> 16);
+            uint32_t a = sb + (smp[q] >> 16);
             if (c == (uint32_t)RM) {
 #pragma unroll
-                for (int r = 0; r < RM; ++r)
-                    stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                for (int r = 0; r < RM; ++r) {
+                    stg_(dst, lds<W>(a));
+                    dst = elem_addr(dst, sOut);
+                    a += mOut;
+                }
             } else {
 #pragma unroll
-                for (int r = 0; r < RM; ++r)
-                    if ((uint32_t)r < c)
-                        stg_(elem_addr(dst, (uint32_t)r * sOut), lds<W>(a0 + (uint32_t)r * mOut));
+                for (int r = 0; r < RM; ++r) {
+                    if ((uint32_t)r < c) stg_(dst, lds<W>(a));
+                    dst = elem_addr(dst, sOut);
+                    a += mOut;
+                }
             }
         }
         k = (k + 1 == (uint32_t)S) ? 0u : k + 1;
