@@ -671,6 +671,11 @@ def run_ours(args):
         nv_bytes = (world - 1) / world * shard_bytes
         keys = ("entry_barrier_ms", "fused_ms", "exit_barrier_ms") if p2p else ("pack_ms", "alltoall_ms", "unpack_ms")
         split = dict(zip(keys, [round(v, 4) for v in sp]))
+        if not p2p and redist:
+            split["a2a_chunks"] = int(plan.describe().get("chunks", 1))
+            if split["a2a_chunks"] > 1:
+                split["split_note"] = ("chunked exchange: each value is that step's span (first chunk's "
+                                       "start to last chunk's end); the spans overlap")
         split["nvlink_bytes_per_gpu_per_direction"] = int(nv_bytes)
         if redist and world > 1:
             t_x = sp[1] if not p2p else ms_step

@@ -114,6 +114,10 @@ typedef struct {
     int tma;             /* TILED2D: 1 = stage the tiles with the Tensor Memory Accelerator
                             (tiled2d_tma_kernel) when every stride is a multiple of 16 bytes
                             and there are at most 3 batch dims; else TT_UNSUPPORTED */
+    int a2a_chunks;      /* sharded redistribution (tt_plan_sharded_ex): cut the exchange into
+                            this many chunks along the split dim so that pack, all-to-all and
+                            unpack of successive chunks overlap; 1 = one serial exchange,
+                            0 = planner (4 chunks from 32 MB of shard, else 1) */
 } tt_plan_options_t;
 
 /* Device description for tt_plan_offline (planning without a GPU). */
@@ -295,7 +299,7 @@ tt_status_t tt_plan_sharded(tt_plan_t* plan, tt_comm_t comm, int rank, const int
                             const int* perm, size_t elem_size, tt_stream_t stream);
 
 /* tt_plan_sharded with options (NULL = tt_plan_sharded); only
- * force_redistribute is read. */
+ * force_redistribute and a2a_chunks are read. */
 tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int rank, const int64_t* global_dims,
                                const int* perm, size_t elem_size, tt_stream_t stream,
                                const tt_plan_options_t* opts);
@@ -307,17 +311,28 @@ tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int rank, const 
  */
 tt_status_t tt_plan_sharded_offline(tt_plan_t* plan, int nranks, int proc, int rank,
                                     const int64_t* global_dims, const int* perm, size_t elem_size);
+/* tt_plan_sharded_offline with options (force_redistribute, a2a_chunks; NULL = defaults). */
+tt_status_t tt_plan_sharded_offline_ex(tt_plan_t* plan, int nranks, int proc, int rank,
+                                       const int64_t* global_dims, const int* perm, size_t elem_size,
+                                       const tt_plan_options_t* opts);
 
 /*
  * tt_execute_sharded -- local input slab -> local output slab (device
  * pointers, shard bytes each), enqueued on the plan's stream.  Collective:
  * every rank of the communicator must call it.  Local case: 1 kernel;
- * redistribution: pack kernel, ncclAlltoAll, unpack kernel.
+ * redistribution: pack kernel, ncclAlltoAll, unpack kernel -- per chunk when
+ * the exchange is chunked (a2a_chunks): chunk k's pack runs on the plan's
+ * stream, its all-to-all on an internal high-priority stream once that pack
+ * is done, its unpack on a second internal stream once that all-to-all is
+ * done, so the three steps of successive chunks overlap; the plan's stream
+ * waits for the last unpack.
  */
 tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_local);
 
 /* Milliseconds of the last tt_execute_sharded's pack / all-to-all / unpack
- * (synchronises on that execution); zeros for the local case. */
+ * (synchronises on that execution); zeros for the local case.  Chunked
+ * exchanges report each step's span (first chunk's start to last chunk's
+ * end), which overlap. */
 tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3);
 
 /* ------------------------------------------------------------------------

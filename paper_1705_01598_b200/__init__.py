@@ -49,7 +49,7 @@ class PlanOptions(ctypes.Structure):
                 ("slot_dims", ctypes.c_int), ("sd_vmax", ctypes.c_int),
                 ("vector_gather", ctypes.c_int), ("t2d_vec2", ctypes.c_int),
                 ("force_redistribute", ctypes.c_int), ("vg_policy", ctypes.c_int),
-                ("tma", ctypes.c_int)]
+                ("tma", ctypes.c_int), ("a2a_chunks", ctypes.c_int)]
 
 
 class DeviceProps(ctypes.Structure):
@@ -90,6 +90,8 @@ def _load():
                                ctypes.POINTER(PlanOptions)],
         "tt_plan_sharded_offline": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     i64p, ip, ctypes.c_size_t],
+        "tt_plan_sharded_offline_ex": [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       i64p, ip, ctypes.c_size_t, ctypes.POINTER(PlanOptions)],
         "tt_sharded_timings": [vp, ctypes.POINTER(ctypes.c_float)],
         "tt_execute_sharded": [vp, vp, vp],
         "tt_plan_shard_dims": [vp, i64p, i64p],
@@ -140,12 +142,12 @@ def _arrays(dims, perm):
 def _options(kernel=0, run_in=0, run_out=0, threads=0, ctas_per_sm=0, no_fusion=False,
              grid_order=0, no_widen=False, stages=0, accumulate=False, slots=0, slot_dims=0,
              sd_vmax=0, vector_gather=0, t2d_vec2=0, force_redistribute=False,
-             vg_policy=0, tma=0):
+             vg_policy=0, tma=0, a2a_chunks=0):
     return PlanOptions(int(kernel), int(run_in), int(run_out), int(threads), int(ctas_per_sm),
                        1 if no_fusion else 0, int(grid_order), 1 if no_widen else 0, int(stages),
                        1 if accumulate else 0, int(slots), int(slot_dims), int(sd_vmax),
                        int(vector_gather), int(t2d_vec2), 1 if force_redistribute else 0, int(vg_policy),
-                       int(tma))
+                       int(tma), int(a2a_chunks))
 
 
 def _ptr(x) -> int:

@@ -60,14 +60,15 @@ class ShardedPlan:
     block-sharded along its outermost output dim."""
 
     def __init__(self, comm: Comm, global_dims, perm, elem_size: int, stream=None,
-                 force_redistribute: bool = False):
+                 force_redistribute: bool = False, a2a_chunks: int = 0):
         """``force_redistribute``: the pack / all-to-all / unpack path even
-        with one rank (single-GPU tests)."""
+        with one rank (single-GPU tests); ``a2a_chunks``: chunks of the
+        overlapped exchange (0 = planner, 1 = serial)."""
         n, d, p = _arrays(global_dims, perm)
         self.comm = comm
         self.global_dims, self.perm, self.elem_size = tuple(global_dims), tuple(perm), int(elem_size)
         h = ctypes.c_void_p()
-        o = _options(force_redistribute=force_redistribute)
+        o = _options(force_redistribute=force_redistribute, a2a_chunks=a2a_chunks)
         _check(lib.tt_plan_sharded_ex(ctypes.byref(h), comm._h, n, d, p, self.elem_size,
                                       _stream_handle(stream), ctypes.byref(o)), "tt_plan_sharded")
         self._h = h
@@ -181,13 +182,16 @@ def plan_sharded_p2p_offline(nranks: int, proc: int, global_dims, perm, elem_siz
         lib.tt_destroy(h)
 
 
-def plan_sharded_offline(nranks: int, proc: int, global_dims, perm, elem_size: int) -> dict:
+def plan_sharded_offline(nranks: int, proc: int, global_dims, perm, elem_size: int,
+                         a2a_chunks: int = 0) -> dict:
     """Sharded geometry and sub-plans for process ``proc`` of ``nranks``,
-    without a communicator or GPU (JSON description)."""
+    without a communicator or GPU (JSON description); ``a2a_chunks`` as
+    for ShardedPlan."""
     n, d, p = _arrays(global_dims, perm)
     h = ctypes.c_void_p()
-    _check(lib.tt_plan_sharded_offline(ctypes.byref(h), int(nranks), int(proc), n, d, p,
-                                       int(elem_size)), "tt_plan_sharded_offline")
+    o = _options(a2a_chunks=a2a_chunks)
+    _check(lib.tt_plan_sharded_offline_ex(ctypes.byref(h), int(nranks), int(proc), n, d, p,
+                                          int(elem_size), ctypes.byref(o)), "tt_plan_sharded_offline")
     try:
         return _describe(h)
     finally:

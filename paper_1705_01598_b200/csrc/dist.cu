@@ -72,6 +72,20 @@ struct ShardInfo {
     std::vector<int64_t> local_in, local_out;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool timed = false;
+    // chunked exchange (redistribute mode, chunks > 1): the split dim t's
+    // per-destination extent c is cut into chunks of ct (the last one
+    // ctail); pack / all-to-all / unpack of chunk k overlap those of k+-1
+    int chunks = 1;
+    int64_t ct = 0, ctail = 0;
+    int64_t w = 0;                  // elements per destination per unit of t
+    int64_t sinT = 0;               // slab stride of input dim t (elements)
+    Plan* pack_tail = nullptr;      // plans of the last chunk when ctail != ct
+    Plan* unpack_tail = nullptr;
+    cudaStream_t cstream = nullptr; // all-to-all (high priority)
+    cudaStream_t ustream = nullptr; // unpack
+    std::vector<cudaEvent_t> evPack, evA2a;
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
+    cudaEvent_t evT[4] = {nullptr, nullptr, nullptr, nullptr};  // a2a start/end, unpack start/end
     // p2p mode (f-1)
     bool p2p = false;
     int proc = 0;                   // this process's slab index
@@ -100,6 +114,16 @@ void destroy_shard(ShardInfo* s) {
     destroy_plan(s->pack);
     destroy_plan(s->unpack);
     destroy_plan(s->fused);
+    destroy_plan(s->pack_tail);
+    destroy_plan(s->unpack_tail);
+    if (s->cstream) cudaStreamDestroy(s->cstream);
+    if (s->ustream) cudaStreamDestroy(s->ustream);
+    for (cudaEvent_t e : s->evPack) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->evA2a) cudaEventDestroy(e);
+    if (s->evFork) cudaEventDestroy(s->evFork);
+    if (s->evJoin) cudaEventDestroy(s->evJoin);
+    for (auto& e : s->evT)
+        if (e) cudaEventDestroy(e);
     for (void* b : s->ipc_bases) cudaIpcCloseMemHandle(b);
     if (s->sig) cudaFree(s->sig);
     for (cudaStream_t x : s->sub) cudaStreamDestroy(x);
@@ -115,7 +139,7 @@ void destroy_shard(ShardInfo* s) {
 int shard_launches(const ShardInfo* s) {
     if (!s->redistribute) return 1;
     if (s->p2p) return s->nranks + (s->comm ? 2 : 0);  // P sub-box launches (+ 2 barriers)
-    return s->nranks > 1 ? 3 : 2;  // pack, (NCCL all-to-all), unpack
+    return s->chunks * (s->nranks > 1 ? 3 : 2);  // per chunk: pack, (NCCL all-to-all), unpack
 }
 
 std::string describe_shard_json(const Plan& plan) {
@@ -140,8 +164,14 @@ std::string describe_shard_json(const Plan& plan) {
     o << ",\"shard_bytes\":" << s->shard_bytes << ",\"a2a_count\":" << s->a2a_count
       << ",\"launches\":" << shard_launches(s);
     if (s->local) o << ",\"local\":" << describe_json(*s->local);
+    if (s->redistribute && !s->p2p)
+        o << ",\"chunks\":" << s->chunks << ",\"chunk_t\":" << (long long)s->ct
+          << ",\"chunk_tail\":" << (long long)s->ctail << ",\"chunk_w\":" << (long long)s->w
+          << ",\"chunk_in_step\":" << (long long)s->sinT;
     if (s->pack) o << ",\"pack\":" << describe_json(*s->pack);
     if (s->unpack) o << ",\"unpack\":" << describe_json(*s->unpack);
+    if (s->pack_tail) o << ",\"pack_tail\":" << describe_json(*s->pack_tail);
+    if (s->unpack_tail) o << ",\"unpack_tail\":" << describe_json(*s->unpack_tail);
     if (s->fused) {
         o << ",\"in_step\":" << (long long)s->in_step << ",\"out_offset\":" << (long long)s->out_off
           << ",\"dest_order\":[";
@@ -156,7 +186,7 @@ std::string describe_shard_json(const Plan& plan) {
 static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int rank, int n,
                                  const int64_t* gd, const int* perm, size_t esize, void* stream,
                                  const DeviceInfo& dev, OccupancyFn occ, bool p2p = false,
-                                 bool forceRedist = false) {
+                                 bool forceRedist = false, int chunksOpt = 0) {
     *out = nullptr;
     tt_status_t st = validate(n, gd, perm, esize);
     if (st != TT_SUCCESS) return st;
@@ -234,32 +264,70 @@ static tt_status_t build_shard_n(Plan** out, tt_comm_impl* comm, int nranks, int
         return TT_SUCCESS;
     }
 
-    // pack: split input dim t into (c = D[t]/P, P), P-part outermost
-    std::vector<int64_t> pd;
-    auto ni = [&](int i) { return i < t ? i : (i == t ? t : i + 1); };
-    for (int i = 0; i < n; ++i) {
-        if (i == t) { pd.push_back(c); pd.push_back(P); }
-        else pd.push_back(L[i]);
+    // chunks of the exchange along t (per destination: c -> K chunks of ct,
+    // the last ctail): default 4 from 32 MB of shard (below that the extra
+    // launches and all-to-alls cost more than the overlap wins)
+    int K = chunksOpt > 0 ? chunksOpt : (s->shard_bytes >= (size_t(32) << 20) ? 4 : 1);
+    if (K > c) K = (int)c;
+    s->ct = ceil_div_i64(c, K);
+    s->chunks = (int)ceil_div_i64(c, s->ct);
+    s->ctail = c - (int64_t)(s->chunks - 1) * s->ct;
+    s->w = shard_vol / L[t];
+    {
+        int64_t acc = 1;
+        for (int i = 0; i < t; ++i) acc *= L[i];
+        s->sinT = acc;
     }
+
+    // pack: split input dim t into (e, P) -- e = c, or a chunk's extent --
+    // P-part outermost, so the block for destination q is contiguous.
+    // Unchunked: a dense problem; chunk k: the sub-box x_t in
+    // q*c + k*ct + [0, e) of every destination q, input strides of the slab
+    // (the P part steps c * S_t), base offset k*ct*S_t (launch time).
+    auto ni = [&](int i) { return i < t ? i : (i == t ? t : i + 1); };
     std::vector<int> pp;
     for (int j = 0; j < n; ++j) pp.push_back(ni(perm[j]));
     pp.push_back(t + 1);
-    st = create_plan(&s->pack, n + 1, pd.data(), pp.data(), esize, stream, dev, nullptr, occ);
+    auto make_pack = [&](int64_t e, Plan** dst) {
+        std::vector<int64_t> pd, ps;
+        int64_t acc = 1;
+        for (int i = 0; i < n; ++i) {
+            if (i == t) {
+                pd.push_back(e); ps.push_back(acc);
+                pd.push_back(P); ps.push_back(acc * c);
+            } else {
+                pd.push_back(L[i]); ps.push_back(acc);
+            }
+            acc *= L[i];
+        }
+        if (s->chunks == 1)
+            return create_plan(dst, n + 1, pd.data(), pp.data(), esize, stream, dev, nullptr, occ);
+        return create_plan_s(dst, n + 1, pd.data(), pp.data(), esize, stream, dev, nullptr, occ, ps.data(),
+                             nullptr);
+    };
+    st = make_pack(s->chunks == 1 ? c : s->ct, &s->pack);
+    if (st == TT_SUCCESS && s->chunks > 1 && s->ctail != s->ct) st = make_pack(s->ctail, &s->pack_tail);
     if (st != TT_SUCCESS) { destroy_plan(outer); return st; }
 
     // unpack: received [e'_0 .. e'_{n-1}, P_src] -> move P_src after j*
-    std::vector<int64_t> ep(n);
+    // (chunk k: e'_{n-1} is the chunk's extent; its output is the contiguous
+    // range of output dim n-1 starting at k*ct)
     int jstar = -1;
-    for (int j = 0; j < n; ++j) {
-        ep[j] = (j == n - 1) ? c : L[perm[j]];
+    for (int j = 0; j < n; ++j)
         if (perm[j] == n - 1) jstar = j;
-    }
-    int64_t inner = 1, middle = 1;
-    for (int j = 0; j <= jstar; ++j) inner *= ep[j];
-    for (int j = jstar + 1; j < n; ++j) middle *= ep[j];
-    const int64_t ud[3] = {inner, middle, (int64_t)P};
-    const int up[3] = {0, 2, 1};
-    st = create_plan(&s->unpack, 3, ud, up, esize, stream, dev, nullptr, occ);
+    auto make_unpack = [&](int64_t e, Plan** dst) {
+        int64_t inner = 1, middle = 1;
+        for (int j = 0; j < n; ++j) {
+            const int64_t ej = (j == n - 1) ? e : L[perm[j]];
+            if (j <= jstar) inner *= ej;
+            else middle *= ej;
+        }
+        const int64_t ud[3] = {inner, middle, (int64_t)P};
+        const int up[3] = {0, 2, 1};
+        return create_plan(dst, 3, ud, up, esize, stream, dev, nullptr, occ);
+    };
+    st = make_unpack(s->chunks == 1 ? c : s->ct, &s->unpack);
+    if (st == TT_SUCCESS && s->chunks > 1 && s->ctail != s->ct) st = make_unpack(s->ctail, &s->unpack_tail);
     if (st != TT_SUCCESS) { destroy_plan(outer); return st; }
     s->a2a_count = (size_t)(shard_vol / P);
     *out = outer;
@@ -315,6 +383,55 @@ __global__ void p2p_barrier_kernel(const __grid_constant__ BarrierArgs a) {
         }
         __nanosleep(200);
     }
+}
+
+// Chunked exchange: chunk k = x_t in q*c + k*ct + [0, e_k) for every
+// destination q.  Its pack (plan stream) fills send[k*P*w*ct ..) as P
+// contiguous blocks of w*e_k words; its all-to-all (cstream) waits for that
+// pack; its unpack (ustream) waits for that all-to-all and writes output
+// slab range k*ct*w*P (output dim n-1 from k*ct).  The buffers are reused
+// by the next execute only after the plan stream joined the last unpack.
+static tt_status_t execute_chunked(ShardInfo* s, const void* in, void* out, cudaStream_t st) {
+    const int P = s->nranks, K = s->chunks;
+    const size_t E = (size_t)s->esize;
+    const ncclDataType_t dt = s->esize == 4 ? ncclUint32 : ncclUint64;
+    const char* ib = static_cast<const char*>(in);
+    char* ob = static_cast<char*>(out);
+    char* sb = static_cast<char*>(s->send);
+    char* rb = static_cast<char*>(s->recv);
+    NvtxRange nv("tt_execute_sharded chunked (pack | all-to-all | unpack)");
+    if (cudaEventRecord(s->ev[0], st) != cudaSuccess || cudaEventRecord(s->evFork, st) != cudaSuccess ||
+        cudaStreamWaitEvent(s->cstream, s->evFork, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(s->ustream, s->evFork, 0) != cudaSuccess)
+        return TT_CUDA_ERROR;
+    for (int k = 0; k < K; ++k) {
+        const bool tail = k == K - 1 && s->pack_tail != nullptr;
+        const int64_t e = k == K - 1 ? s->ctail : s->ct;
+        const size_t blk = (size_t)k * (size_t)s->ct;  // t offset of the chunk
+        const size_t off = blk * (size_t)s->w * (size_t)P * E;
+        if (launch_plan(tail ? *s->pack_tail : *s->pack, ib + blk * (size_t)s->sinT * E, sb + off, st) != 0)
+            return TT_CUDA_ERROR;
+        if (cudaEventRecord(s->evPack[k], st) != cudaSuccess ||
+            cudaStreamWaitEvent(s->cstream, s->evPack[k], 0) != cudaSuccess)
+            return TT_CUDA_ERROR;
+        if (k == 0 && cudaEventRecord(s->evT[0], s->cstream) != cudaSuccess) return TT_CUDA_ERROR;
+        if (ncclAlltoAll(sb + off, rb + off, (size_t)s->w * (size_t)e, dt, s->comm->nccl, s->cstream) !=
+            ncclSuccess)
+            return TT_NCCL_ERROR;
+        if (cudaEventRecord(s->evA2a[k], s->cstream) != cudaSuccess ||
+            cudaStreamWaitEvent(s->ustream, s->evA2a[k], 0) != cudaSuccess)
+            return TT_CUDA_ERROR;
+        if (k == 0 && cudaEventRecord(s->evT[2], s->ustream) != cudaSuccess) return TT_CUDA_ERROR;
+        if (launch_plan(tail ? *s->unpack_tail : *s->unpack, rb + off, ob + off, s->ustream) != 0)
+            return TT_CUDA_ERROR;
+    }
+    if (cudaEventRecord(s->ev[1], st) != cudaSuccess || cudaEventRecord(s->evT[1], s->cstream) != cudaSuccess ||
+        cudaEventRecord(s->evT[3], s->ustream) != cudaSuccess ||
+        cudaEventRecord(s->evJoin, s->ustream) != cudaSuccess || cudaStreamWaitEvent(st, s->evJoin, 0) != cudaSuccess ||
+        cudaEventRecord(s->ev[3], st) != cudaSuccess)
+        return TT_CUDA_ERROR;
+    s->timed = true;
+    return TT_SUCCESS;
 }
 
 static int launch_barrier(ShardInfo* s, cudaStream_t st, int epoch) {
@@ -533,12 +650,34 @@ tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int ndims, const
     if (dev.device != c->device) return TT_INVALID_DEVICE;
     Plan* p = nullptr;
     st = build_shard_n(&p, c, c->nranks, rank, ndims, global_dims, perm, elem_size, stream, dev,
-                       &cuda_occupancy, false, opts && opts->force_redistribute);
+                       &cuda_occupancy, false, opts && opts->force_redistribute, opts ? opts->a2a_chunks : 0);
     if (st != TT_SUCCESS) return st;
     ShardInfo* s = p->shard;
     if (s->redistribute) {
         if (cudaMalloc(&s->send, s->shard_bytes) != cudaSuccess ||
             cudaMalloc(&s->recv, s->shard_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            destroy_plan(p);
+            return TT_CUDA_ERROR;
+        }
+    }
+    if (s->redistribute && s->chunks > 1) {
+        // the exchange gets the highest stream priority: the pack and unpack
+        // kernels' persistent grids must not keep NCCL's kernels off the SMs
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        bool ok = cudaStreamCreateWithPriority(&s->cstream, cudaStreamNonBlocking, hi) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&s->ustream, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&s->evFork, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&s->evJoin, cudaEventDisableTiming) == cudaSuccess;
+        s->evPack.assign(s->chunks, nullptr);
+        s->evA2a.assign(s->chunks, nullptr);
+        for (int k = 0; k < s->chunks && ok; ++k)
+            ok = cudaEventCreateWithFlags(&s->evPack[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&s->evA2a[k], cudaEventDisableTiming) == cudaSuccess;
+        for (auto& e : s->evT)
+            if (ok) ok = cudaEventCreate(&e) == cudaSuccess;
+        if (!ok) {
             cudaGetLastError();
             destroy_plan(p);
             return TT_CUDA_ERROR;
@@ -557,6 +696,12 @@ tt_status_t tt_plan_sharded_ex(tt_plan_t* plan, tt_comm_t comm, int ndims, const
 
 tt_status_t tt_plan_sharded_offline(tt_plan_t* plan, int nranks, int rank, int ndims,
                                     const int64_t* global_dims, const int* perm, size_t elem_size) {
+    return tt_plan_sharded_offline_ex(plan, nranks, rank, ndims, global_dims, perm, elem_size, nullptr);
+}
+
+tt_status_t tt_plan_sharded_offline_ex(tt_plan_t* plan, int nranks, int rank, int ndims,
+                                       const int64_t* global_dims, const int* perm, size_t elem_size,
+                                       const tt_plan_options_t* opts) {
     if (ndims < 1) return TT_INVALID_PARAMETER;
     if (plan == nullptr) return TT_INVALID_PARAMETER;
     *plan = nullptr;
@@ -564,7 +709,8 @@ tt_status_t tt_plan_sharded_offline(tt_plan_t* plan, int nranks, int rank, int n
     dev.device = -1;
     Plan* p = nullptr;
     tt_status_t st = build_shard_n(&p, nullptr, nranks, rank, ndims, global_dims, perm, elem_size,
-                                   nullptr, dev, nullptr);
+                                   nullptr, dev, nullptr, false, opts && opts->force_redistribute,
+                                   opts ? opts->a2a_chunks : 0);
     if (st == TT_SUCCESS) *plan = reinterpret_cast<tt_plan_t>(publish_handle(p));
     return st;
 }
@@ -604,6 +750,7 @@ tt_status_t tt_execute_sharded(tt_plan_t plan, const void* in_local, void* out_l
         s->timed = true;
         return TT_SUCCESS;
     }
+    if (s->chunks > 1) return execute_chunked(s, in_local, out_local, st);
     cudaEventRecord(s->ev[0], st);
     {
         NvtxRange nv("tt_execute_sharded pack");
@@ -634,6 +781,15 @@ tt_status_t tt_sharded_timings(tt_plan_t plan, float* ms3) {
     ms3[0] = ms3[1] = ms3[2] = 0.f;
     if (!s->redistribute || !s->timed) return TT_SUCCESS;
     if (cudaEventSynchronize(s->ev[3]) != cudaSuccess) { cudaGetLastError(); return TT_CUDA_ERROR; }
+    if (s->chunks > 1) {  // spans: packs on the plan stream, all-to-alls, unpacks (they overlap)
+        if (cudaEventElapsedTime(&ms3[0], s->ev[0], s->ev[1]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms3[1], s->evT[0], s->evT[1]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms3[2], s->evT[2], s->evT[3]) != cudaSuccess) {
+            cudaGetLastError();
+            return TT_CUDA_ERROR;
+        }
+        return TT_SUCCESS;
+    }
     for (int i = 0; i < 3; ++i)
         if (cudaEventElapsedTime(&ms3[i], s->ev[i], s->ev[i + 1]) != cudaSuccess) {
             cudaGetLastError();

@@ -101,6 +101,38 @@ def test_single_rank_nccl_redistribution_path(monkeypatch):
     comm.destroy()
 
 
+@pytest.mark.parametrize("K", [2, 3, 5])
+def test_single_rank_nccl_chunked_exchange(K):
+    """The chunked, overlapped exchange (a2a_chunks) with one rank (forced):
+    per chunk a strided pack on the plan stream, ncclAlltoAll on the
+    high-priority stream, the unpack on the second stream; repeated executes
+    reuse the staging buffers."""
+    _dev()
+    comm = tt.Comm(tt.unique_id(), 1, 0)
+    for perm, esize in [((3, 2, 1, 0), 8), ((2, 3, 0, 1), 4), ((0, 3, 1, 2), 8), ((1, 3, 2, 0), 4)]:
+        gdims = (14, 24, 9, 40)
+        words = wl.random_words(int(np.prod(gdims)), esize, 8)
+        x = torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
+        y = torch.empty_like(x)
+        s = torch.cuda.Stream()
+        sp = tt.ShardedPlan(comm, gdims, perm, esize, stream=s, force_redistribute=True, a2a_chunks=K)
+        d = sp.describe()
+        c = gdims[perm[-1]]
+        assert d["mode"] == "redistribute" and d["chunks"] == -(-c // d["chunk_t"]) and d["chunks"] > 1
+        assert d["launches"] == 2 * d["chunks"]
+        want = orc.permute(gdims, perm, words)
+        for _ in range(3):
+            y.fill_(-1)
+            with torch.cuda.stream(s):
+                sp.execute(x, y)
+            s.synchronize()
+            np.testing.assert_array_equal(y.cpu().numpy().view(words.dtype), want)
+        pack_ms, a2a_ms, unpack_ms = sp.timings()
+        assert pack_ms > 0 and unpack_ms > 0 and a2a_ms >= 0
+        sp.destroy()
+    comm.destroy()
+
+
 # ---- fused redistribution (SURVEY f-1): tt_plan_sharded_p2p ----------------
 
 @pytest.mark.parametrize("P", [2, 4, 8])

@@ -91,7 +91,11 @@ def test_sharded_offline_geometry_and_errors():
     assert j["mode"] == "local" and j["local_in_dims"] == [112, 112, 112, 13]
     assert j["launches"] == 1
     j = tt.plan_sharded_offline(8, 3, (112, 112, 112, 104), (3, 2, 1, 0), 8)
-    assert j["mode"] == "redistribute" and j["launches"] == 3
+    # 146 MB shards: the exchange is chunked by default, 14 = 4 + 4 + 4 + 2 along t
+    assert j["mode"] == "redistribute" and j["chunks"] == 4 and j["launches"] == 3 * 4
+    assert (j["chunk_t"], j["chunk_tail"]) == (4, 2) and "pack_tail" in j and "unpack_tail" in j
+    j1 = tt.plan_sharded_offline(8, 3, (112, 112, 112, 104), (3, 2, 1, 0), 8, a2a_chunks=1)
+    assert j1["chunks"] == 1 and j1["launches"] == 3
     assert j["local_out_dims"] == [104, 112, 112, 14]
     assert j["a2a_count"] * 8 == j["shard_bytes"] // 8
     with pytest.raises(tt.TTError):   # shard dim not divisible
@@ -170,3 +174,74 @@ def test_p2p_offline_errors():
     j = tt.plan_sharded_p2p_offline(8, 3, (112, 112, 112, 104), (3, 2, 1, 0), 8)
     assert j["mode"] == "p2p" and j["local_out_dims"] == [104, 112, 112, 14]
     assert j["in_step"] == 14 and j["out_offset"] == 3 * 13   # input dim 3 is output dim 0
+
+
+CHUNK_CASES = [
+    ((6, 4, 5, 8), (3, 2, 1, 0), 8, 2, 2),    # c = 3: chunks 2 + 1 (ragged tail)
+    ((6, 4, 6, 8), (2, 3, 0, 1), 4, 2, 3),    # c = 3: three chunks of 1
+    ((8, 4, 8, 8), (1, 0, 3, 2), 8, 4, 2),    # c = 2: two chunks of 1
+    ((8, 4, 8, 8), (1, 0, 3, 2), 8, 4, 5),    # c = 2: asked for 5, clamped to 2
+    ((12, 4, 8, 8), (0, 3, 2, 1), 4, 2, 4),   # t = 0 (c = 6): chunks 2 + 2 + 2
+    ((7, 4, 10), (2, 0, 1), 8, 2, 3),         # rank 3, c = 2 -> 2 chunks
+    ((10, 3, 6, 6), (3, 1, 0, 2), 4, 3, 2),   # P = 3, t = 2 (c = 2): two chunks
+]
+
+
+@pytest.mark.parametrize("gdims,perm,esize,P,K", CHUNK_CASES)
+def test_chunked_exchange_geometry_emulated_ranks(gdims, perm, esize, P, K):
+    """Chunked redistribution: every emulated rank replays its chunk pack
+    plans (strided sub-boxes at the plan's input offsets) into its send
+    buffer, the all-to-all of each chunk is emulated block by block, and the
+    chunk unpack plans write the output slabs at the chunk offsets; the slabs
+    must equal the oracle's output."""
+    sys.path[:0] = [ROOT, HERE]
+    import paper_1705_01598_b200 as tt
+    from oracle import oracle as orc
+    import tt_workloads as wl
+    from plan_interp import interpret_plan, interpret_tile_plan, interpret_tiled2d_plan
+    n = len(gdims)
+    if gdims[perm[-1]] % P or gdims[-1] % P:
+        pytest.skip("not divisible")
+    vol = int(np.prod(gdims))
+    words = wl.random_words(vol, esize, 91)
+    slab = vol // P
+    js = [tt.plan_sharded_offline(P, r, gdims, perm, esize, a2a_chunks=K) for r in range(P)]
+    j0 = js[0]
+    assert j0["mode"] == "redistribute"
+    c = gdims[perm[-1]] // P
+    Kc = j0["chunks"]
+    assert Kc == -(-c // j0["chunk_t"]) and j0["chunk_tail"] == c - (Kc - 1) * j0["chunk_t"]
+    assert j0["launches"] == Kc * (3 if P > 1 else 2)
+    w = j0["chunk_w"]
+    sends = [np.zeros(slab, dtype=words.dtype) for _ in range(P)]
+
+    def replay(pj, src, dst):
+        fj = dict(pj)
+        fj["dims"] = pj["fused"]["dims"]
+        if pj["kernel"] == "tiled2d":
+            interpret_tiled2d_plan(fj, src, out=dst)
+        else:
+            interpret_tile_plan(fj, src, out=dst)
+
+    chunk_of = lambda k: (j0["chunk_tail"] if k == Kc - 1 else j0["chunk_t"])
+    for r, j in enumerate(js):
+        local_in = words[r * slab:(r + 1) * slab]
+        for k in range(Kc):
+            off = k * j["chunk_t"] * w * P
+            e = chunk_of(k)
+            pj = j["pack_tail"] if (k == Kc - 1 and "pack_tail" in j) else j["pack"]
+            assert int(np.prod(pj["dims"])) == P * w * e
+            if Kc == 1:
+                sends[r][:] = interpret_plan(pj, local_in)
+            else:
+                replay(pj, local_in[k * j["chunk_t"] * j["chunk_in_step"]:], sends[r][off:off + P * w * e])
+    outs = [np.zeros(slab, dtype=words.dtype) for _ in range(P)]
+    for r, j in enumerate(js):
+        for k in range(Kc):
+            off = k * j["chunk_t"] * w * P
+            e = chunk_of(k)
+            recv = np.concatenate([sends[q][off + r * w * e:off + (r + 1) * w * e] for q in range(P)])
+            uj = j["unpack_tail"] if (k == Kc - 1 and "unpack_tail" in j) else j["unpack"]
+            outs[r][off:off + P * w * e] = interpret_plan(uj, recv)
+    want = orc.permute(gdims, perm, words)
+    np.testing.assert_array_equal(np.concatenate(outs), want)
