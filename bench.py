@@ -450,6 +450,7 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
              "sd": "sd" in d.get("tile", {}), "ms": round(ms, 5),
              "gbs": round(2 * c.nbytes / ms / 1e6, 1), "frac_memcpy": round(memcpy_ms[c.nbytes] / ms, 4),
              "plan_us": round(statistics.median(warm), 1), "plan_us_first": round(plan_first, 1),
+             "plan_us_lib": round(float(d.get("plan_us", 0.0)), 1),
              "verified": ok, "elements": c.vol}
         r.update(mrow)
         rows.append(r)
@@ -480,6 +481,11 @@ def run_suites(tt, dev, which, reps, out_path="", measured=False):
                   "plan_us_median": statistics.median(pu), "plan_us_max": pu[-1],
                   "plan_us_first_median": statistics.median(r["plan_us_first"] for r in rs),
                   "plan_us_first_max": max(r["plan_us_first"] for r in rs),
+                  # the library's own planning time of that first plan (tt_plan
+                  # internal clock: no Python / ctypes; the oracle's host
+                  # threads run concurrently in this loop)
+                  "plan_us_lib_median": statistics.median(r["plan_us_lib"] for r in rs),
+                  "plan_us_lib_max": max(r["plan_us_lib"] for r in rs),
                   "verified": f"{sum(r['verified'] for r in rs)}/{len(rs)} cases, full memcmp vs oracle, "
                               f"{sum(r['elements'] for r in rs)} elements",
                   "all_verified": all(r["verified"] for r in rs)}

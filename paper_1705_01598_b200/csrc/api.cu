@@ -457,6 +457,7 @@ static tt_status_t make_plan(tt_plan_t* out, int rank, const int64_t* dims, cons
         }
     }
     tt_status_t st = create_plan(&p, rank, dims, perm, elem_size, stream, dev, opts, occ);
+    if (st == TT_SUCCESS) p->plan_us = us();
     if (st == TT_SUCCESS && log_level() > 0) log_plan(*p, us(), false);
     if (st == TT_SUCCESS && cacheable) cache_put(key, *p);
     if (out) *out = reinterpret_cast<tt_plan_t>(publish_handle(p));

@@ -1990,7 +1990,7 @@ std::string describe_json(const Plan& plan) {
       << ",\"threads\":" << kc.threads
       << ",\"grid\":" << kc.grid << ",\"smem\":" << kc.smem << ",\"nreg\":" << kc.nreg
       << ",\"vec\":" << kc.vec << ",\"idx64\":" << (kc.idx64 ? "true" : "false")
-      << ",\"launches\":1,\"predicted_us\":" << kc.predicted_us
+      << ",\"launches\":1,\"plan_us\":" << plan.plan_us << ",\"predicted_us\":" << kc.predicted_us
       << ",\"model_dram_eff\":" << kc.model_dram_eff << ",\"widen\":" << plan.widen
       << ",\"dense\":" << (pr.dense ? "true" : "false") << ",\"span\":" << (long long)pr.span;
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D)

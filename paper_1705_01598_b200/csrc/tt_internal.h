@@ -232,6 +232,7 @@ struct Plan {
     bool measured = false;         // chosen by tt_plan_measure
     float measured_ms = 0.f, heuristic_ms = 0.f;
     int n_candidates = 0;
+    double plan_us = 0.0;          // host time of the planning that built this plan (0: cache hit / clone)
     int widen = 1;                 // words of the fused problem = widen original elements
     Plan* narrow = nullptr;        // un-widened plan, for pointers not aligned to E*widen
     HostPipe* pipe = nullptr;      // lazily built by tt_execute_host
