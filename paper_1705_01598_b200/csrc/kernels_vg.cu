@@ -108,9 +108,13 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
     const uint32_t nch = (uint32_t)p.vgNch;
 
     // --- load items: item k = (run r, chunk c), u = tid + k*NT -----------------
-    // roff = run offset in bytes from the tile base (Eq. 4 over the non-run
-    // dims); pk = slot byte offset + 16c (bits 0-17) | validity in the four
-    // ragged states (18-21) | q_r / 4 (22-23) | c (24-31)
+    // roff = (run offset in bytes from the tile base, Eq. 4 over the non-run
+    // dims, rounded down to 16) + 16c, with q_r = that offset mod 16 in its
+    // low 4 bits; pk = slot byte offset + 16c (bits 0-17) | validity in the
+    // four ragged states (18-21) | c (24-31).  Per tile, with sh = the tile
+    // base's offset inside its 16-byte chunk: t = sh + q_r, the chunk's source
+    // is the tile base rounded down to 16 + (roff - q_r) + (t & 16), its
+    // staging slot + (t & 16), its run's shift t & 15.
     uint32_t roff[K], pk[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -131,8 +135,8 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             uint32_t valid = 0;
             for (uint32_t n = 0; n < 4; ++n)
                 if ((bad & n) == 0) valid |= 1u << n;
-            roff[k] = off * E;
-            pk[k] = (smb * E + 16u * c) | (valid << 18) | ((((off * E) & 15u) >> 2) << 22) | (c << 24);
+            roff[k] = (off * E & ~15u) + 16u * c + ((off * E) & 15u);
+            pk[k] = (smb * E + 16u * c) | (valid << 18) | (c << 24);
         }
     }
 
@@ -205,17 +209,20 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
         const char* const tb = inB + (size_t)e.x * E;
         const uint32_t vs = 18u + nd;
         if (e.z & 4u) {
+            const uint32_t sh = (uint32_t)reinterpret_cast<uintptr_t>(tb) & 15u;
+            const char* const tbA = tb - sh;
+            const uint32_t vmask = 1u << vs;
             auto items = [&](auto polc) {
                 constexpr int POL = decltype(polc)::value;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const char* a = tb + roff[k];
-                    const uint32_t s = (uint32_t)reinterpret_cast<uintptr_t>(a) & 15u;
+                    const uint32_t q = roff[k] & 15u;
+                    const uint32_t t = sh + q;
+                    const uint32_t cy = t & 16u;       // the run's first byte is in the next chunk
                     const uint32_t c16 = (pk[k] >> 20) & 0xff0u;
-                    const uint32_t q = ((pk[k] >> 22) & 3u) << 2;
-                    const bool ok = ((pk[k] >> vs) & 1u) && c16 < s + Lb;
-                    const uint32_t dst = sb + (pk[k] & 0x3ffffu) + (s < q ? 16u : 0u);
-                    cp_async16_pred<POL>(dst, a - s + c16, ok);
+                    const bool ok = (pk[k] & vmask) && c16 < (t & 15u) + Lb;
+                    const uint32_t dst = sb + (pk[k] & 0x3ffffu) + cy;
+                    cp_async16_pred<POL>(dst, tbA + (roff[k] - q + cy), ok);
                 }
             };
             if (pol == 1) items(std::integral_constant<int, 1>());
@@ -225,10 +232,10 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             const char* const hi = inB + p.vgInBytes;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const char* a = tb + roff[k];
-                const uint32_t s = (uint32_t)reinterpret_cast<uintptr_t>(a) & 15u;
+                const uint32_t q = roff[k] & 15u;
                 const uint32_t c16 = (pk[k] >> 20) & 0xff0u;
-                const uint32_t q = ((pk[k] >> 22) & 3u) << 2;
+                const char* a = tb + (roff[k] - q - c16) + q;   // the run's first byte
+                const uint32_t s = (uint32_t)reinterpret_cast<uintptr_t>(a) & 15u;
                 if (!(((pk[k] >> vs) & 1u) && c16 < s + Lb)) continue;
                 const uint32_t dst = sb + (pk[k] & 0x3ffffu) + (s < q ? 16u : 0u);
                 const char* src = a - s + c16;
@@ -271,7 +278,7 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
             } else {
 #pragma unroll
                 for (int r = 0; r < NREG; ++r)
-                    stg_pred(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]), (m >> r) & 1u);
+                    stg_pred(elem_addr(dst, gout[r]), lds<W>(sbsh + spk[r]), (m & (1u << r)) != 0u);
             }
         }
         __syncwarp();
@@ -290,10 +297,11 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
 }
 
 // vector-gather tile: 4/8-byte words, NREG store slots in {4, 8, 16}, K load
-// items in {2, 4}, 3 or 4 stages, 32-bit indices
+// items in {2, 3, 4}, 3 or 4 stages, 32-bit indices
 const void* pick_tile_vg(int esize, int nreg, int items, int stages) {
 #define TT_VG_K(W, R, S)                                                        \
     if (items <= 2) return (const void*)&tile_vg_kernel<W, R, 2, S>;          \
+    if (items <= 3) return (const void*)&tile_vg_kernel<W, R, 3, S>;          \
     if (items <= 4) return (const void*)&tile_vg_kernel<W, R, 4, S>;          \
     return nullptr;
 #define TT_VG_R(W, S)                       \

@@ -1196,7 +1196,7 @@ static bool build_vg(TileParams& tp, const Problem& pr, int S, int maxSmem, int 
         if (K > 4) continue;
         threads = T;
         nreg = R;
-        tp.vgK = K <= 2 ? 2 : 4;
+        tp.vgK = K <= 2 ? 2 : (int32_t)K;  // kernels: 2, 3 or 4 items
         break;
     }
     return threads > 0;
