@@ -77,8 +77,11 @@ def main():
         groups.setdefault(key, []).append(mb / ma)
 
         def shape(d):
-            return f"{d['kernel']}/T{d.get('threads')}/R{d.get('nreg')}/G{d.get('grid')}"
-        print(f"{c.name:14s} E{c.esize} A {shape(da):22s} {ma*1e3:8.1f}us  B {shape(db):22s} {mb*1e3:8.1f}us"
+            t = d.get("tile") or {}
+            fl = ("/vg" if t.get("vg") else "") + ("/sd" if "sd" in t and not t.get("vg") else "")
+            return (f"{d['kernel']}/T{d.get('threads')}/R{d.get('nreg')}/G{d.get('grid')}"
+                    f"/S{d.get('stages')}/W{d.get('widen')}{fl}")
+        print(f"{c.name:14s} E{c.esize} A {shape(da):34s} {ma*1e3:8.1f}us  B {shape(db):34s} {mb*1e3:8.1f}us"
               f"  ratio {mb/ma:.4f}{'' if same else '  OUTPUT DIFFERS'}", flush=True)
         pa.destroy()
         pb.destroy()
