@@ -711,21 +711,28 @@ def run_ours(args):
                     "elements": int(case.vol if sharded else case.vol * world)}
         del got
 
-    # memcpy roofline of the same bytes on the same stream (P:L252 GPU-STREAM analogue)
+    # memcpy roofline of the same bytes on the same stream (P:L252 GPU-STREAM
+    # analogue).  It runs after the host-side verification leg, when the GPU
+    # has idled and its clocks may still be ramping: 10 warm-up copies, then
+    # the best of three timed batches
     z = torch.empty_like(x)
     with torch.cuda.stream(stream):
-        for _ in range(3):
+        for _ in range(10):
             z.copy_(x)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     reps = max(10, min(50, args.steps))
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(reps):
-            z.copy_(x)
-    e1.record(stream)
-    e1.synchronize()
-    memcpy_gbs = 2.0 * local_vol * E / (e0.elapsed_time(e1) / reps * 1e-3) / 1e9
+    best_ms = None
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                z.copy_(x)
+        e1.record(stream)
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        best_ms = t if best_ms is None else min(best_ms, t)
+    memcpy_gbs = 2.0 * local_vol * E / (best_ms * 1e-3) / 1e9
     del z
 
     # end-to-end through the C ABI with pinned host buffers (H2D + kernel + D2H)
