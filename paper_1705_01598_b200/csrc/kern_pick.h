@@ -13,7 +13,7 @@ const void* pick_tile_sd(int esize, int q, int r, int stages);
 const void* pick_rowcopy(int esize, bool idx64);
 const void* pick_tiled2d(int esize, int vec, int ta, int tb, bool idx64);
 const void* pick_tiled2d_async(int esize, int ta, int tb, int stages);
-const void* pick_tile_vg(int esize, int nreg, int items, int stages);
+const void* pick_tile_vg(int esize, int nreg, int items, int stages, int threads);
 const void* pick_tiled2d_tma(int esize, int rank);
 
 }  // namespace tt

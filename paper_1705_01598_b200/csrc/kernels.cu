@@ -69,7 +69,7 @@ int cuda_occupancy(const OccQuery& q, const DeviceInfo& dev) {
     (void)dev;
     const void* fn = q.tma ? pick_tiled2d_tma(q.esize, q.tma)
                      : q.kernel == TT_KERNEL_TILE
-                         ? (q.vg ? pick_tile_vg(q.esize, q.nreg, q.vg, q.vec)
+                         ? (q.vg ? pick_tile_vg(q.esize, q.nreg, q.vg, q.vec, q.threads)
                             : q.sdq ? pick_tile_sd(q.esize, q.sdq, q.sdr, q.vec >= 3 ? q.vec : 0)
                             : q.acc ? pick_tile_acc(q.esize, q.nreg)
                                       : (q.vec >= 3 ? pick_tile_async(q.esize, q.nreg, q.idx64)
@@ -219,7 +219,7 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
         const void* fn = t2 ? (kc.vec == 1 && kc.stages >= 3 && !kc.idx64
                                    ? pick_tiled2d_async(E, kc.tile0, kc.tile1, kc.stages)
                                    : pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64))
-                            : kc.vg ? pick_tile_vg(E, kc.nreg, plan.tile.vgK, kc.stages)
+                            : kc.vg ? pick_tile_vg(E, kc.nreg, plan.tile.vgK, kc.stages, kc.threads)
                             : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr, kc.stages)
                             : kc.acc ? pick_tile_acc(E, kc.nreg)
                                      : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)

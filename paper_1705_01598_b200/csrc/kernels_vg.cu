@@ -94,8 +94,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
     } while (!done);
 }
 
-template <typename W, int NREG, int K, int S>
-__global__ void __launch_bounds__(NREG >= 16 ? 512 : 1024, 1)
+// Launch bound: up to 512 threads with 16 store slots; with fewer slots a
+// "wide" instantiation for up to 1024 threads (64 registers) and a narrow
+// one for up to 768 (85 registers: room to keep the per-tile pipeline
+// addresses instead of recomputing them), picked by the plan's thread count.
+template <typename W, int NREG, int K, int S, bool WIDE>
+__global__ void __launch_bounds__(NREG >= 16 ? 512 : (WIDE ? 1024 : 768), 1)
 tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W* __restrict__ out) {
     constexpr uint32_t E = sizeof(W);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -297,30 +301,34 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
 }
 
 // vector-gather tile: 4/8-byte words, NREG store slots in {4, 8, 16}, K load
-// items in {2, 3, 4}, 3 or 4 stages, 32-bit indices
-const void* pick_tile_vg(int esize, int nreg, int items, int stages) {
-#define TT_VG_K(W, R, S)                                                        \
-    if (items <= 2) return (const void*)&tile_vg_kernel<W, R, 2, S>;          \
-    if (items <= 3) return (const void*)&tile_vg_kernel<W, R, 3, S>;          \
-    if (items <= 4) return (const void*)&tile_vg_kernel<W, R, 4, S>;          \
+// items in {2, 3, 4}, 3 or 4 stages, 32-bit indices; threads picks the launch
+// bound (above; 16-slot plans have one)
+template <typename W, int R, int S, bool WD>
+static const void* pick_vg_k(int items) {
+    if (items <= 2) return (const void*)&tile_vg_kernel<W, R, 2, S, WD>;
+    if (items <= 3) return (const void*)&tile_vg_kernel<W, R, 3, S, WD>;
+    if (items <= 4) return (const void*)&tile_vg_kernel<W, R, 4, S, WD>;
     return nullptr;
-#define TT_VG_R(W, S)                       \
-    switch (nreg) {                         \
-        case 4: { TT_VG_K(W, 4, S) }        \
-        case 8: { TT_VG_K(W, 8, S) }        \
-        case 16: { TT_VG_K(W, 16, S) }      \
-        default: return nullptr;            \
+}
+template <typename W, int S>
+static const void* pick_vg_r(int nreg, int items, int threads) {
+    const bool wide = threads > 768;
+    switch (nreg) {
+        case 4: return wide ? pick_vg_k<W, 4, S, true>(items) : pick_vg_k<W, 4, S, false>(items);
+        case 8: return wide ? pick_vg_k<W, 8, S, true>(items) : pick_vg_k<W, 8, S, false>(items);
+        case 16: return pick_vg_k<W, 16, S, false>(items);
+        default: return nullptr;
     }
+}
+const void* pick_tile_vg(int esize, int nreg, int items, int stages, int threads) {
     if (esize == 4) {
-        if (stages == 3) { TT_VG_R(uint32_t, 3) }
-        if (stages == 4) { TT_VG_R(uint32_t, 4) }
+        if (stages == 3) return pick_vg_r<uint32_t, 3>(nreg, items, threads);
+        if (stages == 4) return pick_vg_r<uint32_t, 4>(nreg, items, threads);
     } else if (esize == 8) {
-        if (stages == 3) { TT_VG_R(uint64_t, 3) }
-        if (stages == 4) { TT_VG_R(uint64_t, 4) }
+        if (stages == 3) return pick_vg_r<uint64_t, 3>(nreg, items, threads);
+        if (stages == 4) return pick_vg_r<uint64_t, 4>(nreg, items, threads);
     }
     return nullptr;
-#undef TT_VG_R
-#undef TT_VG_K
 }
 
 }  // namespace tt
