@@ -207,7 +207,7 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
     if (kc.tma) return launch_tma(plan, in, out, stream);
     if (kc.kernel == TT_KERNEL_TILE || kc.kernel == TT_KERNEL_TILED2D) {
         bool t2 = kc.kernel == TT_KERNEL_TILED2D;
-        int threads = kc.threads, grid = kc.grid, smem = kc.smem;
+        int threads = kc.threads, grid = kc.grid, smem = kc.smem, stages = kc.stages;
         if (t2 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) &
                    (uintptr_t)(kc.vec * E - 1)) != 0) {
             // pointers not aligned to the vector width: generic tile fallback
@@ -215,15 +215,16 @@ int launch_plan_scaled(const Plan& plan0, const void* in, void* out, void* strea
             threads = kc.fb_threads;
             grid = kc.fb_grid;
             smem = kc.fb_smem;
+            stages = kc.fb_stages;
         }
         const void* fn = t2 ? (kc.vec == 1 && kc.stages >= 3 && !kc.idx64
                                    ? pick_tiled2d_async(E, kc.tile0, kc.tile1, kc.stages)
                                    : pick_tiled2d(E, kc.vec, kc.tile0, kc.tile1, kc.idx64))
-                            : kc.vg ? pick_tile_vg(E, kc.nreg, plan.tile.vgK, kc.stages, kc.threads)
-                            : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr, kc.stages)
+                            : kc.vg ? pick_tile_vg(E, kc.nreg, plan.tile.vgK, stages, threads)
+                            : kc.sdq ? pick_tile_sd(E, kc.sdq, kc.sdr, stages)
                             : kc.acc ? pick_tile_acc(E, kc.nreg)
-                                     : (kc.stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
-                                                       : pick_tile(E, kc.nreg, kc.idx64));
+                                     : (stages >= 3 ? pick_tile_async(E, kc.nreg, kc.idx64)
+                                                    : pick_tile(E, kc.nreg, kc.idx64));
         if (!fn) return (int)cudaErrorInvalidConfiguration;
         if (smem > 48 * 1024) {
             cudaError_t e = ensure_max_smem(fn);

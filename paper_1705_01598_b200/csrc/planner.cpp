@@ -1846,6 +1846,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     kc.fb_threads = kc.threads;
     kc.fb_grid = kc.grid;
     kc.fb_smem = kc.smem;
+    kc.fb_stages = kc.stages;
 
     // TMA-staged 2-D kernel (option tma): whole boxes through the Tensor
     // Memory Accelerator, ragged tiles clipped by the hardware

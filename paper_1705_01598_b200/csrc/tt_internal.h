@@ -172,6 +172,7 @@ struct KernelChoice {
     bool idx64 = false;
     int tile0 = 0, tile1 = 0;      // TILED2D tile
     int fb_threads = 0, fb_grid = 0, fb_smem = 0;  // generic-tile fallback launch
+    int fb_stages = 0;                               // its pipeline stages (the 2-D choice reuses `stages`)
     int stages = 0;                // generic tile: 0 = register double buffer, >= 3 = cp.async ring
     int acc = 0;                   // accumulate plan (f-3): generic tile with alpha/beta
     int sdq = 0, sdr = 0;          // generic tile, slot-dim variant: passes x slots (0 = classic)

@@ -342,6 +342,22 @@ def test_misaligned_pointers():
                 np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
 
 
+@pytest.mark.parametrize("opts", [{}, {"vector_gather": 1}, {"slot_dims": 1}, {"stages": 3}])
+def test_vector_2d_fallback_on_misaligned_pointers(opts):
+    """A vector 2-D plan whose pointers are not aligned to its vector width
+    runs its generic-tile fallback with the fallback's own kernel choice
+    (stages, vector gather, slot-dim map), not the 2-D plan's."""
+    for esize, dims in [(4, (256, 132)), (4, (260, 128, 3)), (8, (130, 66))]:
+        perm = (1, 0) + tuple(range(2, len(dims)))
+        j = tt.Plan(dims, perm, esize, **opts).describe()
+        if j["kernel"] != "tiled2d" or j["vec"] == 1:
+            continue
+        words = wl.random_words(int(np.prod(dims)), esize, 10)
+        for off in (1, 3):
+            got = run_gpu(dims, perm, words, offset=off, **opts)
+            np.testing.assert_array_equal(got, orc.permute(dims, perm, words))
+
+
 @pytest.mark.parametrize("idx", range(0, 57, 4))
 def test_ttc_suite_scaled(idx):
     c = wl.s2_ttc()[idx]
