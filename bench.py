@@ -80,6 +80,10 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dry-run", action="store_true")
+    ap.add_argument("--stream-first", action="store_true",
+                    help="create the plan's stream before the first device allocation (order check)")
+    ap.add_argument("--no-order-check", action="store_true",
+                    help="skip the stream-first re-measurement of the S1 headline")
     return ap.parse_args(argv)
 
 
@@ -573,7 +577,10 @@ def run_ours(args):
     batch = args.config == "s5batch"
 
     # seeded input, uploaded before timing.  Allocated BEFORE the plan's
-    # stream is created (tools/stream_exp3.py: ~4 % on S1 otherwise).
+    # stream is created (tools/stream_exp3.py: ~4 % on S1 otherwise; the
+    # default run re-measures the headline with the other order in a child
+    # process and reports both, "order_check").
+    early_stream = torch.cuda.Stream(device=dev) if args.stream_first else None
     if sharded:
         words_all = case.words()
         slab = case.vol // world
@@ -596,7 +603,7 @@ def run_ours(args):
         y = torch.empty_like(x)
     local_vol = x.numel()
     torch.cuda.synchronize()
-    stream = torch.cuda.Stream(device=dev)
+    stream = early_stream if early_stream is not None else torch.cuda.Stream(device=dev)
 
     if p2p:
         comm = tt.Comm.from_process_group() if world > 1 else tt.Comm(tt.unique_id(), 1, 0)
@@ -802,6 +809,25 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if (args.config == "s1" and world == 1 and not args.stream_first and not args.no_order_check
+                and not args.dry_run):
+            # the same headline in a child process whose stream exists before
+            # its first allocation (the order a caller may well use)
+            import subprocess
+            cmd = [sys.executable, os.path.abspath(__file__), "--steps", str(args.steps), "--warmup",
+                   str(args.warmup), "--suites", "none", "--no-e2e", "--no-cpu-baseline", "--verify", "none",
+                   "--stream-first", "--no-order-check"]
+            try:
+                r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+                alt = json.loads(r.stdout.strip().splitlines()[-1])
+                line["order_check"] = {
+                    "stream_first_value": alt["value"], "unit": alt["unit"],
+                    "stream_first_frac": alt["roofline"]["frac"],
+                    "note": "same workload, plan and timing in a child process that creates its CUDA stream "
+                            "before the first device allocation; `value` allocates first (DESIGN.md, "
+                            "'A measured environment effect')"}
+            except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+                line["order_check"] = {"error": str(ex)[:200]}
         if not sharded:
             line["plan_us"] = round(plan_us, 1)
             line["plan_us_cached"] = round(plan_us_cached, 1)
