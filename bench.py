@@ -813,8 +813,7 @@ def run_ours(args):
                 and not args.dry_run):
             # the same headline in a child process whose stream exists before
             # its first allocation (the order a caller may well use)
-            import subprocess
-            cmd = [sys.executable, os.path.abspath(__file__), "--steps", str(args.steps), "--warmup",
+            cmd =[sys.executable, os.path.abspath(__file__), "--steps", str(args.steps), "--warmup",
                    str(args.warmup), "--suites", "none", "--no-e2e", "--no-cpu-baseline", "--verify", "none",
                    "--stream-first", "--no-order-check"]
             try:
