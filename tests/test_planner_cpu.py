@@ -416,3 +416,12 @@ def test_planner_log_lines():
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
     assert "[tt] plan" not in p.stderr
     assert tt.lib.tt_set_log_level(0) in (0, 1)
+
+
+def test_describe_reports_planning_time():
+    """describe() carries the library-side planning time of the plan (the
+    bench reports it per suite); a rank-12 problem plans in well under a
+    second even on a slow host."""
+    import paper_1705_01598_b200 as tt
+    j = tt.plan_offline((5,) * 12, (0, 8, 4, 10, 1, 3, 9, 5, 7, 2, 6, 11), 4)
+    assert 0 < j["plan_us"] < 1e6
