@@ -1642,6 +1642,10 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
         // x * nc + y follows every search's own order.
         std::vector<int> first[3];  // per memo entry: first pair index in S1 / S2 / S3, -1 = none
         std::vector<int> ents;      // distinct entries in order of appearance
+        // Both sides' extents grow with the run target, so the tile volume is
+        // nondecreasing along each row and column of pairs: past the largest
+        // volume any search accepts, the rest of a row cannot be used.
+        const double vAll = (double)std::max({Vmax, VmaxSd, s3 ? VmaxSdRule : 0});
         for (int x = 0; x < nc; ++x) {
             const int64_t* ni = &sideIn[(size_t)x * pr.n];
             for (int y = 0; y < nc; ++y) {
@@ -1649,7 +1653,12 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
                 if (!m && !s3) continue;
                 const int64_t* no = &sideOut[(size_t)y * pr.n];
                 int64_t need[kMaxDims];
-                for (int i = 0; i < pr.n; ++i) need[i] = std::max(ni[i], no[i]);
+                double vol = 1;
+                for (int i = 0; i < pr.n; ++i) {
+                    need[i] = std::max(ni[i], no[i]);
+                    vol *= (double)need[i];
+                }
+                if (vol > vAll) break;
                 const int e = memo.lookup(pr, need, splitIn[x], splitOut[y], cand[x], cand[y], Vmax, dev,
                                           forceThreads, acc ? 8 : 16, forceR);
                 if ((size_t)e >= first[0].size())
