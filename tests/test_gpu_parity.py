@@ -33,19 +33,25 @@ def to_dev(words):
     return torch.from_numpy(words.view(_ND[esize]).copy()).to(_dev())
 
 
+GUARD = 4096  # sentinel words after every output buffer (no compute-sanitizer on this pool)
+
+
 def run_gpu(dims, perm, words, offset=0, **opts):
-    """Permute on the GPU through tt_plan/tt_execute; returns numpy words."""
+    """Permute on the GPU through tt_plan/tt_execute; returns numpy words.
+    The output sits between sentinel words (``offset`` before, GUARD after)
+    that must survive: a write outside the output fails the test."""
     esize = words.dtype.itemsize
     n = words.size
     src = torch.empty(n + offset, dtype=_TD[esize], device=_dev())
     src[offset:] = to_dev(words)
-    dst = torch.full((n + offset,), -0x21524111, dtype=_TD[esize], device=_dev())
+    dst = torch.full((n + offset + GUARD,), -0x21524111, dtype=_TD[esize], device=_dev())
     plan = tt.Plan(dims, perm, esize, **opts)
-    plan.execute(src[offset:], dst[offset:])
+    plan.execute(src[offset:], dst[offset:offset + n])
     torch.cuda.synchronize()
-    out = dst[offset:].cpu().numpy().view(words.dtype)
+    out = dst[offset:offset + n].cpu().numpy().view(words.dtype)
     if offset:
         assert (dst[:offset].cpu().numpy() == -0x21524111).all(), "wrote before the output"
+    assert (dst[offset + n:].cpu().numpy() == -0x21524111).all(), "wrote after the output"
     plan.destroy()
     return out
 
