@@ -300,6 +300,7 @@ __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT
             int rem = k;
             I off = 0;
             int sp = 0;
+#pragma unroll 1  // setup, once per thread: keep the code small
             for (int i = 0; i < p.a; ++i) {
                 const int c = rem % p.tExt[i];
                 rem /= p.tExt[i];
@@ -314,6 +315,7 @@ __device__ __forceinline__ void build_slots(const TileParams& p, int tid, int NT
             rem = k;
             off = 0;
             int sh = 0;
+#pragma unroll 1
             for (int jj = 0; jj < p.a; ++jj) {
                 const int t = p.tOutOrder[jj];
                 const int c = rem % p.tExt[t];
@@ -443,6 +445,7 @@ __device__ __forceinline__ void build_sd_phase(const TileParams& p, int ph, int 
         uint32_t off = 0, sp = 0;
         int xs = 0;         // slot-dim coordinate of slot 0
         uint32_t bad = 0;   // ragged states (split bits) under which this pass is idle
+#pragma unroll 1  // setup, once per thread: keep the code small
         for (int jj = 0; jj < p.a; ++jj) {
             const int t = ph == 0 ? jj : p.tOutOrder[jj];
             const int e = (t == sl) ? p.sdC[ph] : p.tExt[t];

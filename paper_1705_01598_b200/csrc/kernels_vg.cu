@@ -128,6 +128,7 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
         if (u < (uint32_t)p.vgNR * nch) {
             const uint32_t r = u / nch, c = u - r * nch;
             uint32_t rem = r, off = 0, smb = 0, bad = 0;
+#pragma unroll 1  // setup, once per thread: keep the code small
             for (int t = M; t < p.a; ++t) {
                 const uint32_t x = rem % (uint32_t)p.tExt[t];
                 rem /= (uint32_t)p.tExt[t];
@@ -157,6 +158,7 @@ tile_vg_kernel(const __grid_constant__ TileParams p, const W* __restrict__ in, W
         if (kk < p.V) {
             int rem = kk;
             uint32_t go = 0, inrun = 0, smb = 0, ro = 0, f = 0;
+#pragma unroll 1  // setup, once per thread: keep the code small
             for (int jj = 0; jj < p.a; ++jj) {
                 const int t = p.tOutOrder[jj];
                 const uint32_t x = (uint32_t)(rem % p.tExt[t]);
