@@ -1502,6 +1502,14 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     // (up to 1.5x); 8-byte words lost above 0.8.
     const double fillB2d = can2d ? (double)pr.d[pr.p[0]] / ((double)tb2d * ceil_div(pr.d[pr.p[0]], tb2d)) : 0.0;
     const double fillBMin = E == 4 ? rule::kT2dFillB4 : rule::kT2dFillB8;
+    // Plans that end on the 2-D kernel (want2d below; TMA plans) keep the
+    // generic tile only as the fallback for misaligned pointers: its launch
+    // shape takes the estimated occupancy, so planning them does not load the
+    // generic kernels' CUDA modules (the first plan of a process pays those).
+    const bool want2dEarly = forced == TT_KERNEL_TILED2D ||
+                             (forced == TT_KERNEL_AUTO && can2d && fill2d >= rule::kT2dFill &&
+                              fillB2d >= fillBMin && !(opts && (opts->run_in || opts->run_out)));
+    const OccupancyFn occG = (want2dEarly || (opts && opts->tma > 0)) ? nullptr : occ;
 
     // generic staged tile (Tiled / Packed / PackedSplit classes)
     // 512 threads x 8 slots, and staging byte offsets < 2^16 (16-bit packing)
@@ -1755,7 +1763,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     constexpr int kRing = 64 * 16;  // slot-dim kernels: tile-base ring behind the staging buffers
     auto occOf = [&](int T, int q, int r) {
         OccQuery qs{TT_KERNEL_TILE, E, q * r, 1, T, kc.smem + kRing, false, 0, 0, 0, q, r};
-        int v = occ ? occ(qs, dev) : 0;
+        int v = occG ? occG(qs, dev) : 0;
         return v > 0 ? v : estimate_occupancy(qs, dev);
     };
     if (bt.sd) {
@@ -1769,7 +1777,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     }
     OccQuery q{TT_KERNEL_TILE, E, kc.nreg, kc.stages ? kc.stages : 1, kc.threads, kc.smem,
                kc.idx64, 0, 0, kc.acc};
-    int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(q, dev) : 0);
+    int perSm = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occG ? occG(q, dev) : 0);
     if (perSm <= 0) perSm = estimate_occupancy(q, dev);
     if (!bt.sd)
         kc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.tile.nTiles, (int64_t)dev.num_sms * perSm));
@@ -1801,7 +1809,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
             kc.stages = S;
             kc.smem = S * plan.tile.sbuf * E + kRing;
             OccQuery qa{TT_KERNEL_TILE, E, kc.sdq * kc.sdr, S, kc.threads, kc.smem, false, 0, 0, 0, kc.sdq, kc.sdr};
-            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qa, dev) : 0);
+            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occG ? occG(qa, dev) : 0);
             if (per <= 0)
                 per = std::max(1, std::min({dev.max_smem_per_sm / (kc.smem + 1024),
                                             dev.max_threads_per_sm / kc.threads,
@@ -1838,7 +1846,7 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
             kc.nreg = nr;
             kc.smem = sm;
             OccQuery qv{TT_KERNEL_TILE, E, nr, S, thr, sm, false, 0, 0, 0, 0, 0, vt.vgK};
-            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occ ? occ(qv, dev) : 0);
+            int per = opts && opts->ctas_per_sm ? opts->ctas_per_sm : (occG ? occG(qv, dev) : 0);
             if (per <= 0)
                 per = std::max(1, std::min({dev.max_smem_per_sm / (sm + 1024), dev.max_threads_per_sm / thr,
                                             dev.regs_per_sm / (thr * 64)}));
