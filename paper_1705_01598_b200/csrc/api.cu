@@ -289,6 +289,34 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
         delete p;
         return st;
     }
+    // 8-byte elements whose rows the row copy would move as widened 16-byte
+    // words: the un-widened generic tile is faster (same-box A/B over the
+    // suites' row-copy cases, profiles/round2_ab_rowcopy_tile/: 9 of 9 such
+    // cases 0.89-0.94x the time; un-widened 8-byte rows were mixed and keep
+    // the row copy; so do few long rows, cut into segments -- e.g. the
+    // sharded unpack -- which the A/B did not cover).  Planner-chosen plans
+    // only.
+    static const tt_plan_options_t zeroOpts{};
+    const bool noOpts = opts == nullptr || std::memcmp(opts, &zeroOpts, sizeof(zeroOpts)) == 0;
+    if (noOpts && elem_size == 8 && p->widen > 1 && p->kc.kernel == TT_KERNEL_ROWCOPY && p->row.nseg == 1) {
+        Plan* t = new (std::nothrow) Plan();
+        if (t != nullptr) {
+            t->device = p->device;
+            t->stream = p->stream;
+            t->rank = rank;
+            t->dims = p->dims;
+            t->perm = p->perm;
+            t->prob = normalize(rank, dims, perm, (int)elem_size, !(opts && opts->no_fusion));
+            tt_plan_options_t o{};
+            o.kernel = TT_KERNEL_TILE;
+            if (choose_plan(*t, dev, &o, occ) == TT_SUCCESS) {
+                delete p;
+                p = t;
+            } else {
+                delete t;
+            }
+        }
+    }
     if (p->kc.tma) p->tmaCache = new (std::nothrow) Plan::TmaCache();
     *out = p;
     return TT_SUCCESS;

@@ -564,6 +564,16 @@ def test_classification_threshold_shapes(case):
     check(dims, perm, esize, seed=case)
 
 
+def test_widened_8byte_rows_generic_tile():
+    """The rule that sends many widened 8-byte rows to the un-widened generic
+    tile: the plan it picks, bit-exact (with and without pointer offsets)."""
+    dims, perm = (512, 20000, 2), (0, 2, 1)
+    assert tt.Plan(dims, perm, 8).describe()["kernel"] == "tile"
+    check(dims, perm, 8, seed=12)
+    words = wl.random_words(int(np.prod(dims)), 8, 13)
+    np.testing.assert_array_equal(run_gpu(dims, perm, words, offset=1), orc.permute_threaded(dims, perm, words))
+
+
 @pytest.mark.parametrize("dims,perm,esize", [((597, 41, 85), (2, 1, 0), 8), ((45, 45, 45, 45), (0, 3, 2, 1), 8),
                                              ((5, 29, 7, 31, 81), (4, 0, 3, 1, 2), 8),
                                              ((11, 11, 11, 11, 11, 11), (2, 1, 5, 0, 4, 3), 8),

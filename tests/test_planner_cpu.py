@@ -387,7 +387,10 @@ RULE_SHAPES = [((1304, 101, 50), (1, 0, 2), 8, "tile"),    # B fill 101/128 < 0.
                ((300, 57, 40), (1, 0, 2), 4, "tile"),      # B fill 57/64 < 0.9
                ((1000, 125, 24), (1, 0, 2), 8, "tiled2d"),  # B fill 125/128
                ((138, 21, 16, 10), (0, 2, 3, 1), 4, "tile"),    # 2 x 69 words, 552-byte rows
-               ((1304, 21, 16, 10), (0, 2, 3, 1), 8, "rowcopy"),  # 16-byte words, 10 KB rows
+               # 16-byte words, 10 KB rows, few enough to be segmented: the row
+               # copy (the round-2 rule moving widened 8-byte rows to the
+               # generic tile applies to unsegmented rows only)
+               ((1304, 21, 16, 10), (0, 2, 3, 1), 8, "rowcopy"),
                ((1001, 3, 4), (0, 2, 1), 8, "rowcopy")]   # un-widened 8 KB rows
 
 
@@ -425,3 +428,14 @@ def test_describe_reports_planning_time():
     import paper_1705_01598_b200 as tt
     j = tt.plan_offline((5,) * 12, (0, 8, 4, 10, 1, 3, 9, 5, 7, 2, 6, 11), 4)
     assert 0 < j["plan_us"] < 1e6
+
+
+def test_widened_8byte_rows_take_the_generic_tile():
+    """Round-2 rule (api.cu create_plan_w, same-box A/B in
+    profiles/round2_ab_rowcopy_tile/): many rows of 8-byte elements that the
+    row copy would move as widened 16-byte words go to the un-widened generic
+    tile; few (segmented) rows and un-widened rows keep the row copy."""
+    j = tt.plan_offline((512, 20000, 2), (0, 2, 1), 8)
+    assert j["kernel"] == "tile" and j["widen"] == 1
+    assert tt.plan_offline((513, 20000, 2), (0, 2, 1), 8)["kernel"] == "rowcopy"   # odd rows: not widened
+    assert tt.plan_offline((2048, 3, 7), (0, 2, 1), 8)["kernel"] == "rowcopy"      # few rows: segmented
