@@ -293,12 +293,13 @@ tt_status_t create_plan_w(Plan** out, int rank, const int64_t* dims, const int* 
     // words: the un-widened generic tile is faster (same-box A/B over the
     // suites' row-copy cases, profiles/round2_ab_rowcopy_tile/: 9 of 9 such
     // cases 0.89-0.94x the time; un-widened 8-byte rows were mixed and keep
-    // the row copy; so do few long rows, cut into segments -- e.g. the
-    // sharded unpack -- which the A/B did not cover).  Planner-chosen plans
-    // only.
+    // the row copy; so do problems of fewer than 8192 rows -- e.g. the
+    // sharded unpack's few long rows -- which the A/B did not cover).
+    // Planner-chosen plans only.
     static const tt_plan_options_t zeroOpts{};
     const bool noOpts = opts == nullptr || std::memcmp(opts, &zeroOpts, sizeof(zeroOpts)) == 0;
-    if (noOpts && elem_size == 8 && p->widen > 1 && p->kc.kernel == TT_KERNEL_ROWCOPY && p->row.nseg == 1) {
+    if (noOpts && elem_size == 8 && p->widen > 1 && p->kc.kernel == TT_KERNEL_ROWCOPY &&
+        p->row.nRows / std::max<int64_t>(1, p->row.nseg) >= 8192) {
         Plan* t = new (std::nothrow) Plan();
         if (t != nullptr) {
             t->device = p->device;

@@ -222,6 +222,8 @@ static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 namespace rule {
 constexpr double kRowMinBytes = 512;      // row copy: rows of un-widened words (profiles/round1_ab_rowmin.txt)
 constexpr double kRowMinBytesWide = 4096; // row copy: rows of widened words
+constexpr double kRowMinBytes4 = 8192;    // row copy: un-widened 4-byte rows (round 2,
+                                          // profiles/round2_ab_rowcopy_tile/)
 constexpr double kT2dFill = 0.6;          // 2-D kernel: overall tile fill
 constexpr double kT2dFillB4 = 0.9;        // 2-D kernel: output-side fill, 4-byte words (round1_ab_fillb.txt)
 constexpr double kT2dFillB8 = 0.8;        // ... 8-byte words
@@ -1418,7 +1420,11 @@ static tt_status_t choose_plan_m(Plan& plan, const DeviceInfo& dev, const tt_pla
     // (several elements per word) the generic tile beat the row copy on 12
     // of 13 cases below 4 KB rows (up to 1.39x, one loss of 0.95x); for
     // un-widened rows it lost on 7 of 8, so those keep 512 B.
-    const double rowMin = pr.widen > 1 ? rule::kRowMinBytesWide : rule::kRowMinBytes;
+    // Round 2: un-widened 4-byte rows under 8 KB measured faster on the
+    // generic tile (the tile-base ring and vector-gather kernels came after
+    // the round-1 A/B; profiles/round2_ab_rowcopy_tile/).
+    const double rowMin = pr.widen > 1 ? rule::kRowMinBytesWide
+                          : (E == 4 ? rule::kRowMinBytes4 : rule::kRowMinBytes);
     if (forced == TT_KERNEL_ROWCOPY && !rowClass) return TT_UNSUPPORTED;
     if (!acc && rowClass && (forced == TT_KERNEL_ROWCOPY ||
                      (forced == TT_KERNEL_AUTO && pr.d[0] * E >= rowMin &&
